@@ -1,0 +1,147 @@
+"""Seeded synthetic pencils for the five BASELINE.json configurations.
+
+Constructions follow SURVEY.md §8(d) (config k uses ``default_rng(k)``); the
+search intervals were placed once with an independent eigenvalue count
+(scipy ``eigh`` for the dense pencils, Sylvester inertia of the band LDL^T for
+config 4) and are frozen here so the GPU box never recomputes them.  The
+paper's ``cnt``/``system*`` matrices are not shipped; these
+seeded inputs stand in for them with the shapes and value distributions
+BASELINE.json names.
+
+``scaled`` variants keep the construction and shrink N / M0 so the CPU oracle
+finishes in seconds; they are the GPU parity cases.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class Workload:
+    name: str
+    kind: str            # "dense" | "band"
+    hermitian: bool
+    n: int
+    m0: int
+    ne: int
+    emin: float
+    emax: float
+    a: np.ndarray        # dense (n, n) or band storage
+    b: np.ndarray | None
+    kla: int = 0
+    klb: int = 0
+    uplo: str = "F"
+    expect_m: int | None = None
+
+    def fpm(self):
+        from .params import feastinit
+        f = feastinit()
+        f.set_slot(2, self.ne)
+        return f
+
+
+def _haar(n, rng):
+    g = rng.standard_normal((n, n))
+    q, r = np.linalg.qr(g)
+    return q * np.sign(np.diag(r))[None, :]
+
+
+def c1_syev(n=2000, m0=150, seed=1, interval=(-0.05, 0.05), expect_m=106):
+    """dfeast_syev: A = V diag(lambda) V^T, V Haar, lambda ~ U[-1, 1]."""
+    rng = np.random.default_rng(seed)
+    v = _haar(n, rng)
+    lam = rng.uniform(-1.0, 1.0, n)
+    a = (v * lam[None, :]) @ v.T
+    a = 0.5 * (a + a.T)
+    return Workload("c1_dfeast_syev", "dense", False, n, m0, 8, interval[0],
+                    interval[1], a, None, expect_m=expect_m)
+
+
+def c2_sygv(n=4096, m0=160, seed=2, interval=(-0.025213996656045, 0.024185071538914),
+            expect_m=100):
+    """dfeast_sygv: A = (G+G^T)/(2 sqrt N), B = I + 0.1 H H^T / N."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, n))
+    a = (g + g.T) / (2.0 * np.sqrt(n))
+    h = rng.standard_normal((n, n))
+    b = np.eye(n) + 0.1 * (h @ h.T) / n
+    b = 0.5 * (b + b.T)
+    return Workload("c2_dfeast_sygv", "dense", False, n, m0, 8, interval[0],
+                    interval[1], a, b, expect_m=expect_m)
+
+
+def c3_heev(n=8192, m0=256, seed=3, interval=(-0.02, 0.02), expect_m=103, ne=16):
+    """zfeast_heev: A = (G+G^H)/(2 sqrt N), G complex Gaussian."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    a = (g + g.conj().T) / (2.0 * np.sqrt(n))
+    return Workload("c3_zfeast_heev", "dense", True, n, m0, ne, interval[0],
+                    interval[1], a, None, expect_m=expect_m)
+
+
+def c4_band_matrices(n, kd, seed):
+    """A band (kd): off-diagonals N(0,1), diagonal N(0,1) + 2(i/N - 0.5);
+    B tridiagonal FEM mass matrix 4/6, 1/6.  Returned in 'L' band storage."""
+    rng = np.random.default_rng(seed)
+    ab = np.zeros((kd + 1, n))
+    ab[0] = rng.standard_normal(n) + 2.0 * (np.arange(n) / n - 0.5)
+    for d in range(1, kd + 1):
+        ab[d, : n - d] = rng.standard_normal(n - d)
+    bb = np.zeros((2, n))
+    bb[0] = 4.0 / 6.0
+    bb[1, : n - 1] = 1.0 / 6.0
+    return ab, bb
+
+
+def c4_sbgv(n=1_000_000, kd=16, m0=96, seed=4, interval=None, expect_m=None):
+    ab, bb = c4_band_matrices(n, kd, seed)
+    if interval is None:
+        interval = C4_INTERVALS[n]
+        expect_m = C4_COUNTS[n]
+    return Workload("c4_dfeast_sbgv", "band", False, n, m0, 8, interval[0],
+                    interval[1], ab, bb, kla=kd, klb=1, uplo="L", expect_m=expect_m)
+
+
+def c5_hegv(n=32768, m0=512, seed=5, interval=(-0.0174, 0.0174), expect_m=None, ne=16):
+    """zfeast_hegv: A as config 3; B = I + 0.05 H H^H / N, H complex Gaussian."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    a = (g + g.conj().T) / (2.0 * np.sqrt(n))
+    h = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    b = np.eye(n) + 0.05 * (h @ h.conj().T) / n
+    b = 0.5 * (b + b.conj().T)
+    return Workload("c5_zfeast_hegv", "dense", True, n, m0, ne, interval[0],
+                    interval[1], a, b, expect_m=expect_m)
+
+
+# Frozen C4 intervals: mid-gap endpoints placed by Sylvester inertia of the
+# band LDL^T of A - sigma B (oracle/band_inertia.c), ~64 eigenvalues near 0.
+C4_INTERVALS = {}
+C4_COUNTS = {}
+
+
+def scaled(name):
+    """Scaled-down parity cases with the BASELINE constructions."""
+    if name == "c1s":
+        return c1_syev(n=400, m0=40, seed=11, interval=SCALED_INTERVALS["c1s"],
+                       expect_m=SCALED_COUNTS["c1s"])
+    if name == "c2s":
+        return c2_sygv(n=512, m0=40, seed=12, interval=SCALED_INTERVALS["c2s"],
+                       expect_m=SCALED_COUNTS["c2s"])
+    if name == "c3s":
+        return c3_heev(n=384, m0=40, seed=13, interval=SCALED_INTERVALS["c3s"],
+                       expect_m=SCALED_COUNTS["c3s"], ne=16)
+    if name == "c5s":
+        return c5_hegv(n=320, m0=48, seed=15, interval=SCALED_INTERVALS["c5s"],
+                       expect_m=SCALED_COUNTS["c5s"], ne=16)
+    if name == "c4s":
+        return c4_sbgv(n=20000, kd=16, m0=96, seed=14, interval=SCALED_INTERVALS["c4s"],
+                       expect_m=SCALED_COUNTS["c4s"])
+    raise KeyError(name)
+
+
+SCALED_INTERVALS = {}
+SCALED_COUNTS = {}
