@@ -1,0 +1,157 @@
+/*
+ * feast_b200.h — C ABI of libfeastb200.so, the B200 (sm_100a) FEAST hot path.
+ *
+ * Plain pointers and sizes only: every matrix argument is a DEVICE pointer to
+ * row-major FP64 data; complex matrices are PLANAR (separate re / im planes
+ * with the same leading dimension).  A NULL imaginary pointer means "real
+ * operand".  All calls are ordered on the context's CUDA stream; functions
+ * that return a host-visible result (bad pivot column, Cholesky failure
+ * index, reduced-solver status) synchronise that stream.  Status codes:
+ *   0 ok, -1 allocation failure (info -1), -2 exactly singular pivot (info -2),
+ *   -3 reduced eigensolver failure (info -3), -10 bad argument, -11 CUDA error
+ *   (fb_ctx_last_error() has the message).
+ * One host thread per context; contexts are independent (one per GPU rank).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/feastlib).
+ */
+#ifndef FEAST_B200_H
+#define FEAST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FB_ABI_VERSION 1
+
+typedef struct fb_ctx fb_ctx;
+
+int fb_abi_version(void);
+/* device: CUDA ordinal; stream: cudaStream_t (NULL = legacy default stream) */
+int fb_ctx_create(int device, void* stream, fb_ctx** out);
+int fb_ctx_destroy(fb_ctx* ctx);
+int fb_ctx_set_stream(fb_ctx* ctx, void* stream);
+int fb_ctx_synchronize(fb_ctx* ctx);
+const char* fb_ctx_last_error(const fb_ctx* ctx);
+/* number of kernels this context has launched (instrumentation for bench.py) */
+int64_t fb_ctx_launch_count(const fb_ctx* ctx);
+
+/* ---- dense backend: _DenseOps (dense.py:91-117) ------------------------- */
+
+/* S = z*B - A, B == NULL -> identity.  Replaces the shift formation of
+ * _DenseOps.factorize (dense.py:97-103). */
+int fb_dense_shift(fb_ctx* ctx, int n, double z_re, double z_im,
+                   const double* a_re, const double* a_im, int64_t lda,
+                   const double* b_re, const double* b_im, int64_t ldb,
+                   double* s_re, double* s_im, int64_t lds);
+
+/* Doubles needed for the per-factor diagonal-block inverses. */
+size_t fb_zgetrf_dinv_doubles(int n);
+
+/* In-place LU with partial pivoting of the planar n x n matrix.  piv[n]
+ * (device int32): piv[k] = row interchanged with k at step k, 0-based.
+ * info (device int32): set to INT32_MAX on entry by this call; on completion
+ * holds INT32_MAX, or 1 + the first column with an exactly zero pivot.
+ * Asynchronous; read info with fb_read_info.  Replaces lu_factor
+ * (dense.py:30-50). */
+int fb_zgetrf(fb_ctx* ctx, int n, double* lu_re, double* lu_im, int64_t ld,
+              int* piv, double* dinv, int* info);
+
+/* Synchronise and read a device info word; returns -2 and sets *bad_col to
+ * the 0-based column when the factorization hit a zero pivot, else 0 and
+ * *bad_col = -1.  (SingularMatrixError, dense.py:42-43.) */
+int fb_read_info(fb_ctx* ctx, const int* info, int* bad_col);
+
+/* Solve A X = B (adjoint = 0) or A^H X = B (adjoint = 1) in place on the
+ * planar n x nrhs block X (ldx).  Replaces lu_solve (dense.py:53-88). */
+int fb_zgetrs(fb_ctx* ctx, int n, int nrhs, const double* lu_re, const double* lu_im,
+              int64_t ld, const int* piv, const double* dinv, int adjoint,
+              double* x_re, double* x_im, int64_t ldx);
+
+/* ---- RCI-kernel arithmetic (kernel.py) ---------------------------------- */
+
+/* Counter-based SplitMix64 start block: out(i, j) = U(seed, offset + j*n + i)
+ * (numpy order="F" reshape), imaginary plane from offset_im.  Bit-exact with
+ * random_uniform (kernel.py:90-102, 496-498, 521-525). */
+int fb_splitmix(fb_ctx* ctx, uint64_t seed, int64_t offset_re, int64_t offset_im,
+                int n, int m, double* out_re, double* out_im, int64_t ld);
+
+/* Quadrature accumulation (accumulate_subspace, kernel.py:108-124).
+ * variant 0 'symmetric':         q -= (w/2) Re(r e^{i theta} x)   (q real)
+ * variant 1 'hermitian-direct':  q -= (w/4) r e^{+i theta} x
+ * variant 2 'hermitian-adjoint': q -= (w/4) r e^{-i theta} x */
+int fb_accumulate(fb_ctx* ctx, int variant, int n, int m,
+                  const double* x_re, const double* x_im, int64_t ldx,
+                  double* q_re, double* q_im, int64_t ldq,
+                  double weight, double radius, double theta);
+
+/* C = alpha op(A) op(B) + beta C on planar / real FP64 (DMMA tensor pipe).
+ * op: 'N', 'T' or 'C'.  Used for the dense multiplies (dense.py:111-117),
+ * projections Q^H A Q, Q^H B Q (kernel.py:377-379) and the Ritz products
+ * (kernel.py:411-413). */
+int fb_gemm(fb_ctx* ctx, int is_complex, char opa, char opb, int m, int n, int k,
+            double alpha_re, double alpha_im,
+            const double* a_re, const double* a_im, int64_t lda,
+            const double* b_re, const double* b_im, int64_t ldb,
+            double beta_re, double beta_im,
+            double* c_re, double* c_im, int64_t ldc);
+
+/* M <- (M + M^H)/2 in place (kernel.py:380-381). */
+int fb_symmetrize(fb_ctx* ctx, int m, double* re, double* im, int64_t ld);
+
+/* res_j = ||AX_j - lam_j BX_j||_1 / ||scale BX_j||_1, +inf on a zero
+ * denominator (_column_residuals, kernel.py:147-153).  lam/res on device. */
+int fb_residuals(fb_ctx* ctx, int n, int m, const double* ax_re, const double* ax_im,
+                 const double* bx_re, const double* bx_im, int64_t ld,
+                 const double* lam, double scale, double* res);
+
+/* Cholesky probe of the leading m x m block: *fail = 0 or the 1-based index of
+ * the first non-positive pivot (spd_factor, reduced.py:22-40).  Synchronous. */
+int fb_chol_check(fb_ctx* ctx, int m, const double* b_re, const double* b_im, int64_t ld,
+                  int* fail);
+
+/* Reduced eigenproblem aq phi = eps bq phi (generalized_eig, reduced.py:188-218):
+ * eps[m] ascending (device), phi planar m x m (ldphi), *status = 0 ok, else
+ * the solve failed (info -3).  Synchronous. */
+int fb_reduced_eig(fb_ctx* ctx, int m, const double* aq_re, const double* aq_im,
+                   const double* bq_re, const double* bq_im, int64_t ld,
+                   double* eps, double* phi_re, double* phi_im, int64_t ldphi, int* status);
+
+/* interleaved complex128 (ldz complex elements) <-> planar */
+int fb_pack(fb_ctx* ctx, int n, int m, const double* z, int64_t ldz,
+            double* re, double* im, int64_t ld, int to_planar);
+
+/* ---- banded backend: _BandedOps (banded.py:149-178) --------------------- */
+
+/* Band layouts (device, row-major by band row):
+ *   fb   : (2kl+1) x n full band, row kl+s = s-th subdiagonal (expand_band,
+ *          banded.py:21-47); real (fb_im NULL) or planar complex.
+ *   fact : (3kl+1) x n planar complex LU working array + ipiv[n]
+ *          (band_lu_factor, banded.py:68-103, kv = 2kl). */
+
+/* y = FB x for an n x m block (band_matvec, banded.py:50-65). */
+int fb_band_matvec(fb_ctx* ctx, int n, int kl, int m,
+                   const double* fb_re, const double* fb_im, int64_t ldb,
+                   const double* x_re, const double* x_im, int64_t ldx,
+                   double* y_re, double* y_im, int64_t ldy);
+
+/* fact = LU(z*FB - FA) (banded.py:156-164 + 68-103).  FB NULL -> identity.
+ * info as fb_zgetrf. */
+int fb_band_factor(fb_ctx* ctx, int n, int kl, double z_re, double z_im,
+                   const double* fa_re, const double* fa_im,
+                   const double* fb_re, const double* fb_im, int64_t ldb,
+                   double* fact_re, double* fact_im, int* ipiv, int* info);
+
+/* In-place band solve, direct or adjoint (band_lu_solve, banded.py:106-146). */
+int fb_band_solve(fb_ctx* ctx, int n, int kl, int nrhs,
+                  const double* fact_re, const double* fact_im, const int* ipiv,
+                  int adjoint, double* x_re, double* x_im, int64_t ldx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEAST_B200_H */

@@ -1,0 +1,228 @@
+"""Banded drivers feast_sb / feast_hb on the GPU (mirrors banded.py:1-258).
+
+LAPACK-style band storage is normalised on the host exactly as the reference
+does (expand_band / _pad_band, banded.py:21-47, 181-187) and uploaded once;
+the shifted band LU, the band solves and the band multiplies run on the
+device through libfeastb200.so.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._driver import SolverOptions, run_rci
+from ._errors import SingularMatrixError
+from .device import Planar, get_device
+from .kernel import HermitianRci, SymmetricRci
+from .params import feastinit, FeastParams
+
+_UPLOS = ("F", "L", "U")
+
+
+def band_required_rows(kl: int, uplo: str) -> int:
+    """banded.py:16-18."""
+    return 2 * kl + 1 if uplo.upper() == "F" else kl + 1
+
+
+def expand_band(ab, kl: int, uplo: str, hermitian: bool) -> np.ndarray:
+    """Full-band layout: row kl+s holds the s-th subdiagonal, A[j+s, j] at
+    [kl+s, j]; only in-pattern slots of ``ab`` are read (banded.py:21-47)."""
+    ab = np.asarray(ab)
+    n = ab.shape[1]
+    uplo = uplo.upper()
+    out = np.zeros((2 * kl + 1, n), dtype=ab.dtype)
+    if uplo == "F":
+        out[kl] = ab[kl]
+        for d in range(1, kl + 1):
+            out[kl - d, d:] = ab[kl - d, d:]
+            out[kl + d, :n - d] = ab[kl + d, :n - d]
+        return out
+    if uplo == "L":
+        out[kl] = ab[0]
+        for d in range(1, kl + 1):
+            low = ab[d, :n - d]
+            out[kl + d, :n - d] = low
+            out[kl - d, d:] = np.conj(low) if hermitian else low
+        return out
+    out[kl] = ab[kl]
+    for d in range(1, kl + 1):
+        up = ab[kl - d, d:]
+        out[kl - d, d:] = up
+        out[kl + d, :n - d] = np.conj(up) if hermitian else up
+    return out
+
+
+def pad_band(fb, kl_from: int, kl_to: int):
+    if kl_from == kl_to:
+        return fb
+    out = np.zeros((2 * kl_to + 1, fb.shape[1]), dtype=fb.dtype)
+    out[kl_to - kl_from:kl_to + kl_from + 1] = fb
+    return out
+
+
+class _BandFactor:
+    __slots__ = ("z", "w", "ipiv", "info")
+
+    def __init__(self, z, w, ipiv, info):
+        self.z, self.w, self.ipiv, self.info = z, w, ipiv, info
+
+
+class DeviceBandOps:
+    """Device backend for the banded drivers (banded.py:149-178)."""
+
+    on_device = True
+
+    def __init__(self, dev, FA: Planar, FB: Planar | None, kl: int, hermitian: bool):
+        self.dev, self.FA, self.FB, self.kl, self.hermitian = dev, FA, FB, kl, hermitian
+        self.n = FA.cols
+        self.factorizations = 0
+
+    def factorize(self, z):
+        z = complex(z)
+        dev, n, kl, torch = self.dev, self.n, self.kl, self.dev.torch
+        w = dev.empty(n, 3 * kl + 1, True)     # column-major band working array
+        ipiv = torch.empty(max(n, 1), dtype=torch.int32, device=dev.tdev)
+        info = torch.empty(1, dtype=torch.int32, device=dev.tdev)
+        FA, FB = self.FA, self.FB
+        dev.check(dev.lib.fb_band_factor(dev.h, n, kl, z.real, z.imag, FA.re, FA.im,
+                                         FB.re if FB is not None else None,
+                                         FB.im if FB is not None else None, FA.ld,
+                                         w.re, w.im, ipiv.data_ptr(), info.data_ptr()), "band_factor")
+        self.factorizations += 1
+        bad = dev.read_info(info.data_ptr())
+        if bad >= 0:
+            raise SingularMatrixError(f"zero pivot at band column {bad}")
+        return _BandFactor(z, w, ipiv, info)
+
+    def _solve(self, f, W: Planar, adjoint):
+        dev = self.dev
+        dev.check(dev.lib.fb_band_solve(dev.h, self.n, self.kl, W.cols, f.w.re, f.w.im,
+                                        f.ipiv.data_ptr(), 1 if adjoint else 0, W.re, W.im, W.ld),
+                  "band_solve")
+
+    def solve(self, f, W):
+        self._solve(f, W, False)
+
+    def solve_adjoint(self, f, W):
+        self._solve(f, W, True)
+
+    def _mult(self, F, X, Y):
+        dev = self.dev
+        dev.check(dev.lib.fb_band_matvec(dev.h, self.n, self.kl, X.cols, F.re, F.im, F.ld,
+                                         X.re, X.im, X.ld, Y.re, Y.im, Y.ld), "band_matvec")
+
+    def multiply_a(self, X, Y):
+        self._mult(self.FA, X, Y)
+
+    def multiply_b(self, X, Y):
+        if self.FB is None:
+            Y.copy_from(X)
+        else:
+            self._mult(self.FB, X, Y)
+
+
+class B200BandOps:
+    """Numpy-protocol adapter (for the reference's run_rci) over DeviceBandOps;
+    ``fa``/``fb`` in the full-band layout of expand_band."""
+
+    def __init__(self, fa, fb, kl, hermitian=None, device=None):
+        fa = np.asarray(fa)
+        self.hermitian = np.iscomplexobj(fa) if hermitian is None else hermitian
+        self.dev = get_device(device)
+        FA = self.dev.upload(fa, cplx=self.hermitian)
+        FB = None if fb is None else self.dev.upload(np.asarray(fb), cplx=self.hermitian)
+        self._ops = DeviceBandOps(self.dev, FA, FB, kl, self.hermitian)
+        self.n = fa.shape[1]
+
+    def factorize(self, z):
+        return self._ops.factorize(z)
+
+    def _solve(self, f, rhs, adjoint):
+        W = self.dev.upload(np.asarray(rhs, dtype=np.complex128), cplx=True)
+        self._ops._solve(f, W, adjoint)
+        return self.dev.download(W)
+
+    def solve(self, f, rhs):
+        return self._solve(f, rhs, False)
+
+    def solve_adjoint(self, f, rhs):
+        return self._solve(f, rhs, True)
+
+    def _mult(self, fn, x):
+        X = self.dev.upload(np.asarray(x), cplx=self.hermitian)
+        Y = self.dev.empty(self.n, X.cols, self.hermitian)
+        fn(X, Y)
+        return self.dev.download(Y)
+
+    def multiply_a(self, x):
+        return self._mult(self._ops.multiply_a, x)
+
+    def multiply_b(self, x):
+        return self._mult(self._ops.multiply_b, x)
+
+
+def _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, hermitian, device=None):
+    options = options or SolverOptions()
+    fpm = FeastParams.coerce(fpm) if fpm is not None else feastinit()
+    uplo = (uplo or "F").upper()
+    a = np.asarray(a)
+    n = a.shape[1] if a.ndim == 2 else 0
+    single = a.dtype in (np.float32, np.complex64)
+    scalar = (np.complex64 if single else np.complex128) if hermitian else (np.float32 if single else np.float64)
+    t = ("C" if single else "Z") if hermitian else ("S" if single else "D")
+    routine = f"{t}FEAST_{'HB' if hermitian else 'SB'}{'GV' if b is not None else 'EV'}"
+    cls = HermitianRci if hermitian else SymmetricRci
+    kernel = cls(n, m0, emin, emax, fpm, seed=options.seed, block_size=options.block_size,
+                 dtype=scalar, routine_name=routine, device=device, host_mirror=False)
+    if uplo not in _UPLOS:
+        kernel.abort(-101)
+        return kernel.result
+    if not 0 <= kla <= max(n - 1, 0):
+        kernel.abort(-103)
+        return kernel.result
+    if a.ndim != 2 or a.shape[0] < band_required_rows(kla, uplo):
+        kernel.abort(-105)
+        return kernel.result
+    if b is not None:
+        b = np.asarray(b)
+        if klb is None or not 0 <= klb <= max(n - 1, 0):
+            kernel.abort(-106)
+            return kernel.result
+        if b.ndim != 2 or b.shape[1] != n or b.shape[0] < band_required_rows(klb, uplo):
+            kernel.abort(-108)
+            return kernel.result
+    if kernel.done:
+        return kernel.result
+    kl = max(kla, klb if b is not None else 0)
+    wdt = np.complex128 if hermitian else np.float64
+    fa = pad_band(expand_band(a, kla, uplo, hermitian).astype(wdt, copy=False), kla, kl)
+    fbm = None
+    if b is not None:
+        fbm = pad_band(expand_band(b, klb, uplo, hermitian).astype(wdt, copy=False), klb, kl)
+    dev = kernel.dev
+    try:
+        FA = dev.upload(fa, cplx=hermitian)
+        FB = None if fbm is None else dev.upload(fbm, cplx=hermitian)
+    except MemoryError:
+        kernel.abort(-1)
+        return kernel.result
+    if fpm.slot(5) == 1:
+        if x0 is None:
+            raise ValueError("fpm(5)=1 requires an initial subspace x0")
+        dev.upload(np.asarray(x0)[:, :m0], cplx=hermitian, out=kernel.X)
+    ops = DeviceBandOps(dev, FA, FB, kl, hermitian)
+    result = run_rci(kernel, ops, options)
+    result.factorizations = ops.factorizations
+    return result
+
+
+def feast_sb(a, kla, emin, emax, m0, *, uplo="F", b=None, klb=None, fpm=None, options=None,
+             x0=None, device=None):
+    """Real symmetric banded driver (banded.py:240-250)."""
+    return _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, False, device)
+
+
+def feast_hb(a, kla, emin, emax, m0, *, uplo="F", b=None, klb=None, fpm=None, options=None,
+             x0=None, device=None):
+    """Complex Hermitian banded driver (banded.py:253-258)."""
+    return _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, True, device)

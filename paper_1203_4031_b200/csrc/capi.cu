@@ -1,0 +1,319 @@
+// extern "C" boundary of libfeastb200.so (declared in include/feast_b200.h).
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/feast_b200.h"
+#include "band.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "lu.cuh"
+#include "misc.cuh"
+
+struct fb_ctx : fb::Ctx {
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int* dev_word = nullptr;   // small device scratch for status words
+  int* host_word = nullptr;  // pinned mirror
+  long long launches = 0;
+};
+
+using fb::FB_ERR_ALLOC;
+using fb::FB_ERR_ARG;
+using fb::FB_ERR_CUDA;
+using fb::FB_ERR_SINGULAR;
+using fb::FB_OK;
+
+namespace {
+
+int set_err(fb_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FB_OK;
+  if (c) snprintf(c->err, sizeof(c->err), "%s: %s", what, cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? FB_ERR_ALLOC : FB_ERR_CUDA;
+}
+
+int ensure_scratch(fb_ctx* c, size_t bytes) {
+  if (bytes <= c->scratch_bytes) return FB_OK;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "sync before scratch growth");
+  if (c->scratch) cudaFree(c->scratch);
+  c->scratch = nullptr;
+  c->scratch_bytes = 0;
+  size_t want = bytes + bytes / 4 + (1 << 20);
+  e = cudaMalloc(&c->scratch, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(c, e, "scratch cudaMalloc");
+  }
+  c->scratch_bytes = want;
+  return FB_OK;
+}
+
+int use_device(fb_ctx* c) {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != c->device) {
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return set_err(c, e, "cudaSetDevice");
+  }
+  return FB_OK;
+}
+
+#define CTX_GUARD(c)                  \
+  do {                                \
+    if (!(c)) return FB_ERR_ARG;      \
+    int _g = use_device(c);           \
+    if (_g) return _g;                \
+  } while (0)
+
+fb::Opnd make_op(char op, const double* re, const double* im, int64_t ld) {
+  switch (op) {
+    case 'T': case 't': return fb::op_t(re, im, ld);
+    case 'C': case 'c': return fb::op_c(re, im, ld);
+    default: return fb::op_n(re, im, ld);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int fb_abi_version(void) { return FB_ABI_VERSION; }
+
+int fb_ctx_create(int device, void* stream, fb_ctx** out) {
+  if (!out) return FB_ERR_ARG;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? FB_ERR_ALLOC : FB_ERR_CUDA;
+  fb_ctx* c = new fb_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  c->err[0] = 0;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  e = cudaMalloc(&c->dev_word, 64 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&c->host_word, 64 * sizeof(int));
+  if (e != cudaSuccess) {
+    delete c;
+    return FB_ERR_ALLOC;
+  }
+  *out = c;
+  return FB_OK;
+}
+
+int fb_ctx_destroy(fb_ctx* c) {
+  if (!c) return FB_OK;
+  use_device(c);
+  cudaStreamSynchronize(c->stream);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->dev_word) cudaFree(c->dev_word);
+  if (c->host_word) cudaFreeHost(c->host_word);
+  delete c;
+  return FB_OK;
+}
+
+int fb_ctx_set_stream(fb_ctx* c, void* stream) {
+  if (!c) return FB_ERR_ARG;
+  c->stream = static_cast<cudaStream_t>(stream);
+  return FB_OK;
+}
+
+int fb_ctx_synchronize(fb_ctx* c) {
+  CTX_GUARD(c);
+  return set_err(c, cudaStreamSynchronize(c->stream), "synchronize");
+}
+
+const char* fb_ctx_last_error(const fb_ctx* c) { return c ? c->err : "null context"; }
+
+int64_t fb_ctx_launch_count(const fb_ctx* c) { return c ? c->launches : 0; }
+
+int fb_dense_shift(fb_ctx* c, int n, double zr, double zi, const double* are, const double* aim,
+                   int64_t lda, const double* bre, const double* bim, int64_t ldb, double* sre,
+                   double* sim, int64_t lds) {
+  CTX_GUARD(c);
+  if (n < 0 || !are || !sre || !sim) return FB_ERR_ARG;
+  c->launches += 1;
+  return set_err(c, fb::shift_launch(n, zr, zi, are, aim, lda, bre, bim, ldb, sre, sim, lds, c->stream),
+                 "dense_shift");
+}
+
+size_t fb_zgetrf_dinv_doubles(int n) { return fb::dinv_doubles(n); }
+
+int fb_zgetrf(fb_ctx* c, int n, double* re, double* im, int64_t ld, int* piv, double* dinv, int* info) {
+  CTX_GUARD(c);
+  if (n < 0 || !re || !im || !piv || !dinv || !info) return FB_ERR_ARG;
+  int r = ensure_scratch(c, fb::zgetrf_scratch_bytes(n));
+  if (r) return r;
+  const int big = INT_MAX;
+  cudaError_t e = cudaMemcpyAsync(info, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "zgetrf info init");
+  // kernels per outer block: 4 panels + laswps + gemms (counted approximately)
+  c->launches += (long long)((n + 127) / 128) * 31;
+  return set_err(c, fb::zgetrf(n, re, im, ld, piv, info, dinv, (char*)c->scratch, c->stream), "zgetrf");
+}
+
+int fb_read_info(fb_ctx* c, const int* info, int* bad_col) {
+  CTX_GUARD(c);
+  cudaError_t e = cudaMemcpyAsync(c->host_word, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "read_info");
+  int v = c->host_word[0];
+  if (bad_col) *bad_col = (v == INT_MAX) ? -1 : v - 1;
+  return v == INT_MAX ? FB_OK : FB_ERR_SINGULAR;
+}
+
+int fb_zgetrs(fb_ctx* c, int n, int nrhs, const double* re, const double* im, int64_t ld, const int* piv,
+              const double* dinv, int adjoint, double* xr, double* xi, int64_t ldx) {
+  CTX_GUARD(c);
+  if (n < 0 || nrhs < 0 || !xr || !xi) return FB_ERR_ARG;
+  c->launches += 2 + 4LL * ((n + 31) / 32);
+  return set_err(c, fb::zgetrs(n, nrhs, re, im, ld, piv, dinv, adjoint, xr, xi, ldx, c->stream), "zgetrs");
+}
+
+int fb_splitmix(fb_ctx* c, uint64_t seed, int64_t off_re, int64_t off_im, int n, int m, double* re,
+                double* im, int64_t ld) {
+  CTX_GUARD(c);
+  c->launches += 1;
+  return set_err(c, fb::splitmix_launch(seed, off_re, off_im, n, m, re, im, ld, c->stream), "splitmix");
+}
+
+int fb_accumulate(fb_ctx* c, int variant, int n, int m, const double* xr, const double* xi, int64_t ldx,
+                  double* qr, double* qi, int64_t ldq, double w, double r, double theta) {
+  CTX_GUARD(c);
+  if (variant < 0 || variant > 2) return FB_ERR_ARG;
+  // Coefficients evaluated as numpy does (kernel.py:117-123):
+  //   sym : (w/2.0) * (r*exp(i theta) * x).real
+  //   herm: ((w/4.0) * r) * exp(+-i theta), then times x
+  double cth = std::cos(theta), sth = std::sin(theta);
+  int mode;
+  double h, cr, ci;
+  if (variant == 0) {
+    mode = 0;
+    h = w / 2.0;
+    cr = r * cth;
+    ci = r * sth;
+  } else {
+    mode = 1;
+    double s = (w / 4.0) * r;
+    h = 0.0;
+    cr = s * cth;
+    ci = s * (variant == 1 ? sth : -sth);
+  }
+  c->launches += 1;
+  return set_err(c, fb::accumulate_launch(mode, n, m, xr, xi, ldx, qr, qi, ldq, h, cr, ci, c->stream),
+                 "accumulate");
+}
+
+int fb_gemm(fb_ctx* c, int cplx, char opa, char opb, int m, int n, int k, double ar, double ai,
+            const double* are, const double* aim, int64_t lda, const double* bre, const double* bim,
+            int64_t ldb, double br, double bi, double* cre, double* cim, int64_t ldc) {
+  CTX_GUARD(c);
+  if (m < 0 || n < 0 || k < 0 || !cre || (cplx && !cim)) return FB_ERR_ARG;
+  fb::GemmParams p;
+  p.m = m; p.n = n; p.k = k;
+  p.a = make_op(opa, are, cplx ? aim : nullptr, lda);
+  p.b = make_op(opb, bre, cplx ? bim : nullptr, ldb);
+  p.cre = cre; p.cim = cplx ? cim : nullptr; p.cs0 = ldc; p.cs1 = 1;
+  p.alpha_re = ar; p.alpha_im = cplx ? ai : 0.0; p.beta_re = br; p.beta_im = cplx ? bi : 0.0;
+  p.splits = fb::gemm_pick_splits(m, n, k);
+  p.ws = nullptr;
+  p.kchunk = 0;
+  if (p.splits > 1) {
+    int r = ensure_scratch(c, fb::gemm_workspace_bytes(cplx, m, n, p.splits));
+    if (r) return r;
+    p.ws = (double*)c->scratch;
+  }
+  c->launches += p.splits > 1 ? 2 : 1;
+  return set_err(c, fb::gemm_launch(cplx, p, c->stream), "gemm");
+}
+
+int fb_symmetrize(fb_ctx* c, int m, double* re, double* im, int64_t ld) {
+  CTX_GUARD(c);
+  c->launches += 1;
+  return set_err(c, fb::symmetrize_launch(m, re, im, ld, c->stream), "symmetrize");
+}
+
+int fb_residuals(fb_ctx* c, int n, int m, const double* axr, const double* axi, const double* bxr,
+                 const double* bxi, int64_t ld, const double* lam, double scale, double* res) {
+  CTX_GUARD(c);
+  int r = ensure_scratch(c, fb::residual_scratch_bytes(n, m));
+  if (r) return r;
+  c->launches += 2;
+  return set_err(c, fb::residual_launch(n, m, axr, axi, bxr, bxi, ld, lam, scale, res,
+                                        (double*)c->scratch, c->stream),
+                 "residuals");
+}
+
+int fb_chol_check(fb_ctx* c, int m, const double* bre, const double* bim, int64_t ld, int* fail) {
+  CTX_GUARD(c);
+  if (m <= 0 || !fail) return FB_ERR_ARG;
+  int r = ensure_scratch(c, fb::reduced_scratch_bytes(m));
+  if (r) return r;
+  c->launches += 1;
+  cudaError_t e = fb::chol_check_launch(m, bre, bim, ld, c->dev_word, (double*)c->scratch, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->host_word, c->dev_word, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "chol_check");
+  *fail = c->host_word[0];
+  return FB_OK;
+}
+
+int fb_reduced_eig(fb_ctx* c, int m, const double* are, const double* aim, const double* bre,
+                   const double* bim, int64_t ld, double* eps, double* phre, double* phim, int64_t ldphi,
+                   int* status) {
+  CTX_GUARD(c);
+  if (m <= 0 || !status || !eps || !phre) return FB_ERR_ARG;
+  int r = ensure_scratch(c, fb::reduced_scratch_bytes(m));
+  if (r) return r;
+  c->launches += 1;
+  cudaError_t e = fb::reduced_eig_launch(m, are, aim, bre, bim, ld, eps, phre, phim, ldphi, c->dev_word,
+                                         (double*)c->scratch, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c->host_word, c->dev_word, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "reduced_eig");
+  *status = c->host_word[0];
+  return *status == 0 ? FB_OK : fb::FB_ERR_REDUCED;
+}
+
+int fb_pack(fb_ctx* c, int n, int m, const double* z, int64_t ldz, double* re, double* im, int64_t ld,
+            int to_planar) {
+  CTX_GUARD(c);
+  c->launches += 1;
+  return set_err(c, fb::pack_launch(n, m, z, ldz, re, im, ld, to_planar, c->stream), "pack");
+}
+
+int fb_band_matvec(fb_ctx* c, int n, int kl, int m, const double* fbr, const double* fbi, int64_t ldb,
+                   const double* xr, const double* xi, int64_t ldx, double* yr, double* yi, int64_t ldy) {
+  CTX_GUARD(c);
+  if (n < 0 || kl < 0 || m < 0 || !fbr || !xr || !yr) return FB_ERR_ARG;
+  c->launches += 1;
+  return set_err(c, fb::band_matvec_launch(n, kl, m, fbr, fbi, ldb, xr, xi, ldx, yr, yi, ldy, c->stream),
+                 "band_matvec");
+}
+
+int fb_band_factor(fb_ctx* c, int n, int kl, double zr, double zi, const double* far_, const double* fai,
+                   const double* fbr, const double* fbi, int64_t ldb, double* fr, double* fi, int* ipiv,
+                   int* info) {
+  CTX_GUARD(c);
+  if (n < 0 || kl < 0 || !far_ || !fr || !fi || !ipiv || !info) return FB_ERR_ARG;
+  const int big = INT_MAX;
+  cudaError_t e = cudaMemcpyAsync(info, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "band info init");
+  c->launches += 2;
+  return set_err(c, fb::band_factor_launch(n, kl, zr, zi, far_, fai, fbr, fbi, ldb, fr, fi, ipiv, info,
+                                           c->stream),
+                 "band_factor");
+}
+
+int fb_band_solve(fb_ctx* c, int n, int kl, int nrhs, const double* fr, const double* fi, const int* ipiv,
+                  int adjoint, double* xr, double* xi, int64_t ldx) {
+  CTX_GUARD(c);
+  if (n < 0 || kl < 0 || nrhs < 0 || !fr || !xr || !xi) return FB_ERR_ARG;
+  c->launches += 1;
+  return set_err(c, fb::band_solve_launch(n, kl, nrhs, fr, fi, ipiv, adjoint, xr, xi, ldx, c->stream),
+                 "band_solve");
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Shared helpers for the FEAST B200 kernels (sm_100a only).
+//
+// Complex data is PLANAR on the device: a complex matrix is two real planes
+// (re, im) with the same row-major leading dimension.  Planar operands map
+// directly onto the real FP64 DMMA fragments (mma.sync m8n8k4 f64), which is
+// the only FP64 tensor-core path on sm_100a (tcgen05 has no f64 kind).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libfeastb200 targets sm_100a only"
+#endif
+
+namespace fb {
+
+constexpr int kSMs = 148;
+
+struct Ctx {
+  int device;
+  cudaStream_t stream;
+  int sm_count;
+  char err[256];
+};
+
+// Status codes of the C-ABI (include/feast_b200.h).
+enum : int {
+  FB_OK = 0,
+  FB_ERR_ALLOC = -1,       // maps to info -1 (MemoryError)
+  FB_ERR_SINGULAR = -2,    // maps to info -2 (SingularMatrixError)
+  FB_ERR_ARG = -10,
+  FB_ERR_CUDA = -11,
+  FB_ERR_REDUCED = -3,     // maps to info -3
+};
+
+#define FB_CUDA(ctx, call)                                                        \
+  do {                                                                            \
+    cudaError_t _e = (call);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      if (ctx) snprintf((ctx)->err, sizeof((ctx)->err), "%s:%d %s: %s", __FILE__, \
+                        __LINE__, #call, cudaGetErrorString(_e));                 \
+      return _e == cudaErrorMemoryAllocation ? FB_ERR_ALLOC : FB_ERR_CUDA;        \
+    }                                                                             \
+  } while (0)
+
+#define FB_LAUNCH_CHECK(ctx) FB_CUDA(ctx, cudaGetLastError())
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// One FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
+// Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// d0,d1 = D[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int src = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// |z| as numpy's np.abs(complex) (hypot), used for pivot search (dense.py:41).
+__device__ __forceinline__ double cabs_(double re, double im) { return hypot(re, im); }
+
+}  // namespace fb

@@ -1,0 +1,262 @@
+// FP64 / complex-FP64 GEMM on the sm_100a DMMA tensor pipe.
+//
+//   C(m x n) = alpha * op(A)(m x k) * op(B)(k x n) + beta * C
+//
+// Operands are described by (re, im, s0, s1, conj): op(A)(i, k) lives at
+// re[i*s0 + k*s1] (+ i*im[...], conjugated when conj != 0).  That one
+// descriptor covers N / T / C operands on row-major planar storage, which is
+// every GEMM the FEAST hot path issues: the LU trailing update
+// (A22 -= L21 U12), the blocked triangular-solve updates, A*Q / B*Q
+// (kernel.py:372-376), the projections Q^H (AQ), Q^H (BQ) (kernel.py:377-379)
+// and the Ritz products Q*Phi, AQ*Phi, BQ*Phi (kernel.py:411-413).
+//
+// Tiling: 64x64 CTA tile, 4 warps each owning a 32x32 block of 4x4 DMMA
+// 8x8x4 tiles; operands stream global -> shared with cp.async in a 3-stage
+// pipeline; shared layouts are chosen per operand contiguity so that both
+// the cp.async stores and the fragment loads are bank-conflict free (64-bit
+// elements have no ldmatrix path).  Complex products use 4 real DMMAs
+// (re*re - im*im, re*im + im*re).  Split-K is deterministic: partial tiles go
+// to a workspace and are reduced in a fixed order.
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace fb {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 8, STAGES = 3, THREADS = 128;
+constexpr int PK = BK + 4;   // pitch of [row][k] layouts (12 doubles)
+constexpr int PM = BM + 8;   // pitch of [k][row] layouts (72 doubles)
+
+template <bool KC>
+struct ATile {  // KC: k contiguous in global -> smem [BM][PK]; else [BK][PM]
+  static constexpr int kElems = KC ? BM * PK : BK * PM;
+  __device__ static int idx(int i, int k) { return KC ? i * PK + k : k * PM + i; }
+};
+
+template <bool CPLX, bool AKC, bool BNC>
+__global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
+  constexpr int PL = CPLX ? 2 : 1;
+  constexpr int AE = ATile<AKC>::kElems;
+  constexpr int BE = ATile<!BNC>::kElems;  // B^T viewed as an A tile: n<->m
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                         // [STAGES][PL][AE]
+  double* Bs = smem + STAGES * PL * AE;      // [STAGES][PL][BE]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int z = blockIdx.z;
+  const int kbeg = z * p.kchunk;
+  const int kend = min(p.k, kbeg + p.kchunk);
+  const int nk = kend > kbeg ? ceil_div(kend - kbeg, BK) : 0;
+
+  const double* are = p.a.re;
+  const double* aim = p.a.im;
+  const double* bre = p.b.re;
+  const double* bim = p.b.im;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kbeg + kt * BK;
+    double* as = As + stage * PL * AE;
+    double* bs = Bs + stage * PL * BE;
+#pragma unroll
+    for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+      int e = tid + r * THREADS;
+      int i, k;
+      if (AKC) { i = e / BK; k = e % BK; } else { i = e % BM; k = e / BM; }
+      int gi = m0 + i, gk = k0 + k;
+      bool ok = gi < p.m && gk < kend;
+      long long off = ok ? (long long)gi * p.a.s0 + (long long)gk * p.a.s1 : 0;
+      int s = ATile<AKC>::idx(i, k);
+      cp_async8(as + s, are + off, ok);
+      if (CPLX) cp_async8(as + AE + s, (aim ? aim : are) + off, ok && aim);
+    }
+#pragma unroll
+    for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+      int e = tid + r * THREADS;
+      int j, k;
+      if (BNC) { j = e % BN; k = e / BN; } else { j = e / BK; k = e % BK; }
+      int gj = n0 + j, gk = k0 + k;
+      bool ok = gj < p.n && gk < kend;
+      long long off = ok ? (long long)gk * p.b.s0 + (long long)gj * p.b.s1 : 0;
+      int s = ATile<!BNC>::idx(j, k);
+      cp_async8(bs + s, bre + off, ok);
+      if (CPLX) cp_async8(bs + BE + s, (bim ? bim : bre) + off, ok && bim);
+    }
+  };
+
+  double accr[4][4][2], acci[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      accr[a][b][0] = accr[a][b][1] = 0.0;
+      acci[a][b][0] = acci[a][b][1] = 0.0;
+    }
+  const double sa = p.a.conj ? -1.0 : 1.0;
+  const double sb = p.b.conj ? -1.0 : 1.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (kt + STAGES - 1 < nk) load_stage((kt + STAGES - 1) % STAGES, kt + STAGES - 1);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * PL * AE;
+    const double* bs = Bs + (kt % STAGES) * PL * BE;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      const int kk = k4 + (lane & 3);
+      double ar[4], ai[4], nai[4], br[4], bi[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        int sA = ATile<AKC>::idx(wm + t * 8 + (lane >> 2), kk);
+        ar[t] = as[sA];
+        int sB = ATile<!BNC>::idx(wn + t * 8 + (lane >> 2), kk);
+        br[t] = bs[sB];
+        if (CPLX) {
+          ai[t] = sa * as[AE + sA];
+          nai[t] = -ai[t];
+          bi[t] = sb * bs[BE + sB];
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma(accr[a][b][0], accr[a][b][1], ar[a], br[b]);
+          if (CPLX) {
+            dmma(accr[a][b][0], accr[a][b][1], nai[a], bi[b]);
+            dmma(acci[a][b][0], acci[a][b][1], ar[a], bi[b]);
+            dmma(acci[a][b][0], acci[a][b][1], ai[a], br[b]);
+          }
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue.
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int i = m0 + wm + a * 8 + (lane >> 2);
+        int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
+        if (i >= p.m || j >= p.n) continue;
+        double vr = accr[a][b][e], vi = CPLX ? acci[a][b][e] : 0.0;
+        if (p.splits > 1) {
+          size_t plane = (size_t)p.m * p.n;
+          double* w = p.ws + (size_t)z * PL * plane;
+          w[(size_t)i * p.n + j] = vr;
+          if (CPLX) w[plane + (size_t)i * p.n + j] = vi;
+          continue;
+        }
+        long long c = (long long)i * p.cs0 + (long long)j * p.cs1;
+        double outr = p.alpha_re * vr - p.alpha_im * vi;
+        double outi = p.alpha_re * vi + p.alpha_im * vr;
+        if (p.beta_re != 0.0 || p.beta_im != 0.0) {
+          double cr = p.cre[c], ci = (CPLX && p.cim) ? p.cim[c] : 0.0;
+          outr += p.beta_re * cr - p.beta_im * ci;
+          outi += p.beta_re * ci + p.beta_im * cr;
+        }
+        p.cre[c] = outr;
+        if (CPLX && p.cim) p.cim[c] = outi;
+      }
+}
+
+template <bool CPLX>
+__global__ void splitk_reduce(GemmParams p) {
+  const size_t plane = (size_t)p.m * p.n;
+  constexpr int PL = CPLX ? 2 : 1;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < plane;
+       e += (size_t)gridDim.x * blockDim.x) {
+    double vr = 0.0, vi = 0.0;
+    for (int z = 0; z < p.splits; ++z) {
+      vr += p.ws[(size_t)z * PL * plane + e];
+      if (CPLX) vi += p.ws[(size_t)z * PL * plane + plane + e];
+    }
+    int i = (int)(e / p.n), j = (int)(e % p.n);
+    long long c = (long long)i * p.cs0 + (long long)j * p.cs1;
+    double outr = p.alpha_re * vr - p.alpha_im * vi;
+    double outi = p.alpha_re * vi + p.alpha_im * vr;
+    if (p.beta_re != 0.0 || p.beta_im != 0.0) {
+      double cr = p.cre[c], ci = (CPLX && p.cim) ? p.cim[c] : 0.0;
+      outr += p.beta_re * cr - p.beta_im * ci;
+      outi += p.beta_re * ci + p.beta_im * cr;
+    }
+    p.cre[c] = outr;
+    if (CPLX && p.cim) p.cim[c] = outi;
+  }
+}
+
+template <bool CPLX, bool AKC, bool BNC>
+cudaError_t launch_t(const GemmParams& p, cudaStream_t st) {
+  constexpr int PL = CPLX ? 2 : 1;
+  size_t smem = sizeof(double) * STAGES * PL * (ATile<AKC>::kElems + ATile<!BNC>::kElems);
+  auto kern = gemm_kernel<CPLX, AKC, BNC>;
+  static bool configured = false;  // attribute set once per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.splits);
+  kern<<<grid, THREADS, smem, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || p.splits <= 1) return e;
+  size_t plane = (size_t)p.m * p.n;
+  int blocks = (int)std::min<size_t>((plane + 255) / 256, 4 * 148);
+  splitk_reduce<CPLX><<<blocks, 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t gemm_workspace_bytes(int cplx, int m, int n, int splits) {
+  if (splits <= 1) return 0;
+  return sizeof(double) * (cplx ? 2 : 1) * (size_t)splits * m * n;
+}
+
+int gemm_pick_splits(int m, int n, int k) {
+  long long tiles = (long long)ceil_div(m, BM) * ceil_div(n, BN);
+  if (tiles >= 2 * kSMs || k < 512) return 1;
+  long long want = (2 * kSMs + tiles - 1) / tiles;
+  long long maxs = k / 256;
+  long long s = want < maxs ? want : maxs;
+  return s < 1 ? 1 : (int)s;
+}
+
+cudaError_t gemm_launch(int cplx, GemmParams p, cudaStream_t st) {
+  if (p.m <= 0 || p.n <= 0) return cudaSuccess;
+  if (p.splits < 1) p.splits = 1;
+  if (p.k <= 0) {
+    // C = beta * C (alpha * 0)
+    p.k = 0;
+    p.kchunk = 0;
+    p.splits = 1;
+  } else {
+    p.kchunk = ceil_div(ceil_div(p.k, p.splits), BK) * BK;
+    p.splits = ceil_div(p.k, p.kchunk);
+  }
+  bool akc = p.a.s1 == 1 || p.a.s0 != 1;   // k-contiguous (or generic) A
+  bool bnc = p.b.s1 == 1 || p.b.s0 != 1;   // n-contiguous (or generic) B
+  if (cplx) {
+    if (akc && bnc) return launch_t<true, true, true>(p, st);
+    if (akc && !bnc) return launch_t<true, true, false>(p, st);
+    if (!akc && bnc) return launch_t<true, false, true>(p, st);
+    return launch_t<true, false, false>(p, st);
+  }
+  if (akc && bnc) return launch_t<false, true, true>(p, st);
+  if (akc && !bnc) return launch_t<false, true, false>(p, st);
+  if (!akc && bnc) return launch_t<false, false, true>(p, st);
+  return launch_t<false, false, false>(p, st);
+}
+
+}  // namespace fb

@@ -1,0 +1,47 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fb {
+
+struct Opnd {
+  const double* re;
+  const double* im;  // nullptr: imaginary part is zero (real operand)
+  long long s0, s1;  // op(X)(r, c) at re[r*s0 + c*s1]
+  int conj;          // conjugate the imaginary part
+};
+
+struct GemmParams {
+  int m, n, k;
+  Opnd a, b;
+  double* cre;
+  double* cim;
+  long long cs0, cs1;
+  double alpha_re, alpha_im, beta_re, beta_im;
+  double* ws;  // split-K workspace (gemm_workspace_bytes)
+  int splits;
+  int kchunk;
+};
+
+// Row-major planar helpers: X is rows x cols with leading dimension ld.
+inline Opnd op_n(const double* re, const double* im, long long ld) { return {re, im, ld, 1, 0}; }
+inline Opnd op_t(const double* re, const double* im, long long ld) { return {re, im, 1, ld, 0}; }
+inline Opnd op_c(const double* re, const double* im, long long ld) { return {re, im, 1, ld, 1}; }
+
+cudaError_t gemm_launch(int cplx, GemmParams p, cudaStream_t st);
+size_t gemm_workspace_bytes(int cplx, int m, int n, int splits);
+int gemm_pick_splits(int m, int n, int k);
+
+// Convenience: C = alpha op(A) op(B) + beta C without split-K.
+inline cudaError_t gemm(int cplx, int m, int n, int k, Opnd a, Opnd b, double* cre, double* cim,
+                        long long ldc, double ar, double ai, double br, double bi, cudaStream_t st,
+                        double* ws = nullptr, int splits = 1) {
+  GemmParams p;
+  p.m = m; p.n = n; p.k = k; p.a = a; p.b = b;
+  p.cre = cre; p.cim = cim; p.cs0 = ldc; p.cs1 = 1;
+  p.alpha_re = ar; p.alpha_im = ai; p.beta_re = br; p.beta_im = bi;
+  p.ws = ws; p.splits = ws ? splits : 1; p.kchunk = 0;
+  return gemm_launch(cplx, p, st);
+}
+
+}  // namespace fb

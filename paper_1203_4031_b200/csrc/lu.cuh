@@ -1,0 +1,20 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fb {
+
+size_t zgetrf_scratch_bytes(int n);
+size_t dinv_doubles(int n);
+cudaError_t shift_launch(int n, double zr, double zi, const double* are, const double* aim,
+                         long long lda, const double* bre, const double* bim, long long ldb,
+                         double* sre, double* sim, long long lds, cudaStream_t st);
+cudaError_t laswp_launch(double* re, double* im, long long ld, int c0, int c1, const int* piv,
+                         int k0, int k1, int rev, cudaStream_t st);
+cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* info, double* dinv,
+                   char* scratch, cudaStream_t st);
+cudaError_t zgetrs(int n, int nrhs, const double* re, const double* im, long long ld, const int* piv,
+                   const double* dinv, int adjoint, double* xr, double* xi, long long ldx,
+                   cudaStream_t st);
+
+}  // namespace fb

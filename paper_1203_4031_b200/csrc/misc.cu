@@ -1,0 +1,192 @@
+// Bandwidth-bound helpers of the FEAST refinement loop.
+//
+//   splitmix_fill   kernel.py:90-102 + 496-498 / 521-525 (bit-exact start block)
+//   accumulate      kernel.py:108-124 (quadrature sum, numpy operation order)
+//   symmetrize      kernel.py:380-381 (A_Q <- (A_Q + A_Q^H) / 2)
+//   residuals       kernel.py:147-153 (column 1-norm ratios, +inf on zero denominator)
+//   pack / unpack   numpy complex128 (interleaved) <-> planar device layout
+#include "common.cuh"
+#include "misc.cuh"
+
+namespace fb {
+
+namespace {
+
+__device__ __forceinline__ double splitmix_u(unsigned long long seed, unsigned long long ctr) {
+  unsigned long long z = seed + ctr * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  return __dsub_rn(__dmul_rn((double)(z >> 11), 0x1p-52), 1.0);
+}
+
+// out(i, j) = u(seed, off + j*n + i)  (numpy reshape(order="F") of the stream)
+__global__ void splitmix_kernel(unsigned long long seed, long long off_re, long long off_im, int n,
+                                int m, double* __restrict__ re, double* __restrict__ im,
+                                long long ld) {
+  long long total = (long long)n * m;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / m), j = (int)(e % m);
+    long long f = (long long)j * n + i;
+    re[i * ld + j] = splitmix_u(seed, (unsigned long long)(off_re + f + 1));
+    if (im) im[i * ld + j] = splitmix_u(seed, (unsigned long long)(off_im + f + 1));
+  }
+}
+
+// mode 0: q -= h * (tr*xr - ti*xi)             (symmetric; h = w/2)
+// mode 1: q -= (cr + i ci) * x                  (Hermitian direct / adjoint)
+__global__ void accumulate_kernel(int mode, int n, int m, const double* __restrict__ xr,
+                                  const double* __restrict__ xi, long long ldx,
+                                  double* __restrict__ qr, double* __restrict__ qi, long long ldq,
+                                  double h, double cr, double ci) {
+  long long total = (long long)n * m;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / m), j = (int)(e % m);
+    double a = xr[i * ldx + j], b = xi[i * ldx + j];
+    if (mode == 0) {
+      double v = __dsub_rn(__dmul_rn(cr, a), __dmul_rn(ci, b));
+      qr[i * ldq + j] = __dsub_rn(qr[i * ldq + j], __dmul_rn(h, v));
+    } else {
+      double vr = __dsub_rn(__dmul_rn(cr, a), __dmul_rn(ci, b));
+      double vi = __dadd_rn(__dmul_rn(cr, b), __dmul_rn(ci, a));
+      qr[i * ldq + j] = __dsub_rn(qr[i * ldq + j], vr);
+      qi[i * ldq + j] = __dsub_rn(qi[i * ldq + j], vi);
+    }
+  }
+}
+
+__global__ void symmetrize_kernel(int m, double* __restrict__ re, double* __restrict__ im,
+                                  long long ld) {
+  long long total = (long long)m * m;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / m), j = (int)(e % m);
+    if (j < i) continue;
+    double ar = re[i * ld + j], br = re[j * ld + i];
+    double ai = im ? im[i * ld + j] : 0.0, bi = im ? im[j * ld + i] : 0.0;
+    double nr = 0.5 * (ar + br);
+    double ni = 0.5 * (ai - bi);
+    re[i * ld + j] = nr;
+    re[j * ld + i] = nr;
+    if (im) {
+      im[i * ld + j] = ni;
+      im[j * ld + i] = -ni;
+    }
+  }
+}
+
+constexpr int RES_ROWS = 512;  // rows per partial-sum chunk
+
+__global__ void residual_partial(int n, int m, const double* __restrict__ axr,
+                                 const double* __restrict__ axi, const double* __restrict__ bxr,
+                                 const double* __restrict__ bxi, long long ld,
+                                 const double* __restrict__ lam, double scale,
+                                 double* __restrict__ part) {
+  const int chunk = blockIdx.x;
+  const int r0 = chunk * RES_ROWS, r1 = min(n, r0 + RES_ROWS);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double l = lam[j];
+    double num = 0.0, den = 0.0;
+    for (int i = r0; i < r1; ++i) {
+      double br = bxr[i * ld + j], ar = axr[i * ld + j];
+      if (axi) {
+        double bi = bxi[i * ld + j], ai = axi[i * ld + j];
+        num += hypot(ar - l * br, ai - l * bi);
+        den += hypot(scale * br, scale * bi);
+      } else {
+        num += fabs(ar - l * br);
+        den += fabs(scale * br);
+      }
+    }
+    part[((size_t)chunk * m + j) * 2] = num;
+    part[((size_t)chunk * m + j) * 2 + 1] = den;
+  }
+}
+
+__global__ void residual_final(int chunks, int m, const double* __restrict__ part,
+                               double* __restrict__ res) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double num = 0.0, den = 0.0;
+  for (int c = 0; c < chunks; ++c) {
+    num += part[((size_t)c * m + j) * 2];
+    den += part[((size_t)c * m + j) * 2 + 1];
+  }
+  res[j] = den > 0.0 ? num / den : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// interleaved complex (n x m, ld in complex elements) <-> planar (ldp)
+__global__ void pack_kernel(int n, int m, const double* __restrict__ z, long long ldz,
+                            double* __restrict__ re, double* __restrict__ im, long long ldp,
+                            int to_planar) {
+  long long total = (long long)n * m;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(e / m), j = (int)(e % m);
+    if (to_planar) {
+      double2 v = reinterpret_cast<const double2*>(z)[i * ldz + j];
+      re[i * ldp + j] = v.x;
+      if (im) im[i * ldp + j] = v.y;
+    } else {
+      double2 v;
+      v.x = re[i * ldp + j];
+      v.y = im ? im[i * ldp + j] : 0.0;
+      reinterpret_cast<double2*>(const_cast<double*>(z))[i * ldz + j] = v;
+    }
+  }
+}
+
+int grid_for(long long total, int threads = 256) {
+  long long b = (total + threads - 1) / threads;
+  if (b > 16 * kSMs) b = 16 * kSMs;
+  return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+cudaError_t splitmix_launch(unsigned long long seed, long long off_re, long long off_im, int n, int m,
+                            double* re, double* im, long long ld, cudaStream_t st) {
+  if (n <= 0 || m <= 0) return cudaSuccess;
+  splitmix_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(seed, off_re, off_im, n, m, re, im, ld);
+  return cudaGetLastError();
+}
+
+cudaError_t accumulate_launch(int mode, int n, int m, const double* xr, const double* xi,
+                              long long ldx, double* qr, double* qi, long long ldq, double h,
+                              double cr, double ci, cudaStream_t st) {
+  if (n <= 0 || m <= 0) return cudaSuccess;
+  accumulate_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(mode, n, m, xr, xi, ldx, qr, qi, ldq,
+                                                                h, cr, ci);
+  return cudaGetLastError();
+}
+
+cudaError_t symmetrize_launch(int m, double* re, double* im, long long ld, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  symmetrize_kernel<<<grid_for((long long)m * m), 256, 0, st>>>(m, re, im, ld);
+  return cudaGetLastError();
+}
+
+size_t residual_scratch_bytes(int n, int m) {
+  return sizeof(double) * 2 * (size_t)ceil_div(n, RES_ROWS) * m;
+}
+
+cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, const double* bxr,
+                            const double* bxi, long long ld, const double* lam, double scale,
+                            double* res, double* scratch, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  int chunks = ceil_div(n, RES_ROWS);
+  residual_partial<<<chunks, 128, 0, st>>>(n, m, axr, axi, bxr, bxi, ld, lam, scale, scratch);
+  residual_final<<<ceil_div(m, 128), 128, 0, st>>>(chunks, m, scratch, res);
+  return cudaGetLastError();
+}
+
+cudaError_t pack_launch(int n, int m, const double* z, long long ldz, double* re, double* im,
+                        long long ldp, int to_planar, cudaStream_t st) {
+  if (n <= 0 || m <= 0) return cudaSuccess;
+  pack_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(n, m, z, ldz, re, im, ldp, to_planar);
+  return cudaGetLastError();
+}
+
+}  // namespace fb

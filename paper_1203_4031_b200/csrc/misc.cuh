@@ -1,0 +1,29 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fb {
+
+cudaError_t splitmix_launch(unsigned long long seed, long long off_re, long long off_im, int n, int m,
+                            double* re, double* im, long long ld, cudaStream_t st);
+cudaError_t accumulate_launch(int mode, int n, int m, const double* xr, const double* xi,
+                              long long ldx, double* qr, double* qi, long long ldq, double h,
+                              double cr, double ci, cudaStream_t st);
+cudaError_t symmetrize_launch(int m, double* re, double* im, long long ld, cudaStream_t st);
+size_t residual_scratch_bytes(int n, int m);
+cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, const double* bxr,
+                            const double* bxi, long long ld, const double* lam, double scale,
+                            double* res, double* scratch, cudaStream_t st);
+cudaError_t pack_launch(int n, int m, const double* z, long long ldz, double* re, double* im,
+                        long long ldp, int to_planar, cudaStream_t st);
+
+// reduced eigensolver (reduced.cu)
+size_t reduced_scratch_bytes(int m);
+cudaError_t chol_check_launch(int m, const double* bre, const double* bim, long long ld, int* fail,
+                              double* scratch, cudaStream_t st);
+cudaError_t reduced_eig_launch(int m, const double* are, const double* aim, const double* bre,
+                               const double* bim, long long ld, double* eps, double* phre,
+                               double* phim, long long ldphi, int* status, double* scratch,
+                               cudaStream_t st);
+
+}  // namespace fb

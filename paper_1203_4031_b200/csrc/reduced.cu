@@ -1,0 +1,567 @@
+// Reduced (M0 x M0) generalized Hermitian eigensolver, on the GPU.
+//
+// Restates reduced.py:22-218 step for step so the Ritz values follow the
+// reference algorithm:
+//   spd_factor (Cholesky with 1-based failing-pivot index)       reduced.py:22-40
+//   C = L^-1 A L^-H, then C <- (C + C^H)/2                        reduced.py:209-212
+//   Householder tridiagonalisation with accumulated V             reduced.py:65-114
+//   complex phase folding of the subdiagonal into V               reduced.py:102-113
+//   implicit QL with Wilkinson shifts, <= 30 sweeps / eigenvalue  reduced.py:117-172
+//   stable ascending sort, Phi = L^-H Y                           reduced.py:180-185, 213-218
+//
+// One CTA does the whole solve (M0 <= 512 here): every O(M0^3) stage is
+// parallel across the CTA's threads, the O(M0^2) QL recurrences run on one
+// thread with the rotation sequence applied by all threads.  Working arrays
+// live in a global scratch (L2-resident for M0 <= 512).
+#include "common.cuh"
+#include "misc.cuh"
+
+namespace fb {
+
+namespace {
+
+constexpr int RT = 512;  // threads
+
+struct Red {
+  double v[RT / 32];
+};
+
+__device__ double block_sum(double x, double* sh) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+struct RArgs {
+  int m;
+  const double *are, *aim, *bre, *bim;
+  long long ld;
+  double* eps;
+  double *phre, *phim;
+  long long ldphi;
+  int* status;
+  double* ws;
+  int check_only;
+};
+
+// complex helpers
+__device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double& cr, double& ci) {
+  cr = ar * br - ai * bi;
+  ci = ar * bi + ai * br;
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
+  const int m = a.m, tid = threadIdx.x;
+  const size_t mm = (size_t)m * m;
+  double* Lr = a.ws;
+  double* Li = Lr + mm;
+  double* Cr = Li + mm;  // working matrix (row-major)
+  double* Ci = Cr + mm;
+  double* Tr = Ci + mm;  // transposes / V^T
+  double* Ti = Tr + mm;
+  double* Vr = Ti + mm;  // V^T: Vr[c*m + r] = V[r][c]
+  double* Vi = Vr + mm;
+  double* ur = Vi + mm;
+  double* ui = ur + m;
+  double* pr = ui + m;
+  double* pi = pr + m;
+  double* wr = pi + m;
+  double* wi = wr + m;
+  extern __shared__ double shd[];
+  double* d = shd;           // [m]
+  double* ee = d + m;        // [m]
+  double* rc = ee + m;       // rotation cosines [m]
+  double* rs = rc + m;       // rotation sines [m]
+  double* sh = rs + m;       // reduction scratch [40]
+  __shared__ int s_int[4];
+  __shared__ double s_dbl[8];
+
+  // finiteness (reduced.py:203-204)
+  if (!a.check_only) {
+    int bad = 0;
+    for (size_t e = tid; e < mm; e += RT) {
+      size_t i = e / m, j = e % m;
+      double x = a.are[i * a.ld + j] + a.bre[i * a.ld + j];
+      if (CPLX) x += a.aim[i * a.ld + j] + a.bim[i * a.ld + j];
+      if (!isfinite(x)) bad = 1;
+    }
+    if (__syncthreads_or(bad)) {
+      if (tid == 0) *a.status = -2;
+      return;
+    }
+  }
+  if (m == 1 && !a.check_only) {  // reduced.py:205-210
+    if (tid == 0) {
+      double b00 = a.bre[0];
+      if (b00 <= 0) {
+        *a.status = -2;
+      } else {
+        a.eps[0] = a.are[0] / b00;
+        a.phre[0] = 1.0 / sqrt(b00);
+        if (CPLX) a.phim[0] = 0.0;
+        *a.status = 0;
+      }
+    }
+    return;
+  }
+
+  // 1. Cholesky L L^H = B (reduced.py:22-40)
+  for (int j = 0; j < m; ++j) {
+    double part = 0.0;
+    for (int k = tid; k < j; k += RT) {
+      double xr = Lr[(size_t)j * m + k], xi = CPLX ? Li[(size_t)j * m + k] : 0.0;
+      part += xr * xr + xi * xi;
+    }
+    double s = block_sum(part, sh);
+    double dj = a.bre[(size_t)j * a.ld + j] - s;
+    if (!(dj > 0.0) || !isfinite(dj)) {
+      if (tid == 0) *a.status = j + 1;
+      return;
+    }
+    double ljj = sqrt(dj);
+    for (int i = j + 1 + tid; i < m; i += RT) {
+      double sr = 0.0, si = 0.0;
+      for (int k = 0; k < j; ++k) {
+        double xr = Lr[(size_t)i * m + k], yr = Lr[(size_t)j * m + k];
+        if (CPLX) {
+          double xi = Li[(size_t)i * m + k], yi = -Li[(size_t)j * m + k];
+          sr += xr * yr - xi * yi;
+          si += xr * yi + xi * yr;
+        } else {
+          sr += xr * yr;
+        }
+      }
+      Lr[(size_t)i * m + j] = (a.bre[(size_t)i * a.ld + j] - sr) / ljj;
+      if (CPLX) Li[(size_t)i * m + j] = (a.bim[(size_t)i * a.ld + j] - si) / ljj;
+    }
+    if (tid == 0) {
+      Lr[(size_t)j * m + j] = ljj;
+      if (CPLX) Li[(size_t)j * m + j] = 0.0;
+    }
+    for (int k = j + 1 + tid; k < m; k += RT) {  // strictly upper part of L is zero
+      Lr[(size_t)j * m + k] = 0.0;
+      if (CPLX) Li[(size_t)j * m + k] = 0.0;
+    }
+    __syncthreads();
+  }
+  if (a.check_only) {
+    if (tid == 0) *a.status = 0;
+    return;
+  }
+
+  // 2. W = L^-1 A (column-parallel forward substitution) -> C
+  for (int c = tid; c < m; c += RT) {
+    for (int i = 0; i < m; ++i) {
+      double sr = a.are[(size_t)i * a.ld + c], si = CPLX ? a.aim[(size_t)i * a.ld + c] : 0.0;
+      for (int k = 0; k < i; ++k) {
+        double lr = Lr[(size_t)i * m + k], xr = Cr[(size_t)k * m + c];
+        if (CPLX) {
+          double li = Li[(size_t)i * m + k], xi = Ci[(size_t)k * m + c];
+          sr -= lr * xr - li * xi;
+          si -= lr * xi + li * xr;
+        } else {
+          sr -= lr * xr;
+        }
+      }
+      double dr = Lr[(size_t)i * m + i];
+      Cr[(size_t)i * m + c] = sr / dr;
+      if (CPLX) Ci[(size_t)i * m + c] = si / dr;
+    }
+  }
+  __syncthreads();
+  // T = W^H
+  for (size_t e = tid; e < mm; e += RT) {
+    size_t i = e / m, j = e % m;
+    Tr[j * m + i] = Cr[i * m + j];
+    if (CPLX) Ti[j * m + i] = -Ci[i * m + j];
+  }
+  __syncthreads();
+  // X = L^-1 T -> C (then C <- X^H)
+  for (int c = tid; c < m; c += RT) {
+    for (int i = 0; i < m; ++i) {
+      double sr = Tr[(size_t)i * m + c], si = CPLX ? Ti[(size_t)i * m + c] : 0.0;
+      for (int k = 0; k < i; ++k) {
+        double lr = Lr[(size_t)i * m + k], xr = Cr[(size_t)k * m + c];
+        if (CPLX) {
+          double li = Li[(size_t)i * m + k], xi = Ci[(size_t)k * m + c];
+          sr -= lr * xr - li * xi;
+          si -= lr * xi + li * xr;
+        } else {
+          sr -= lr * xr;
+        }
+      }
+      double dr = Lr[(size_t)i * m + i];
+      Cr[(size_t)i * m + c] = sr / dr;
+      if (CPLX) Ci[(size_t)i * m + c] = si / dr;
+    }
+  }
+  __syncthreads();
+  // C <- X^H, then (C + C^H)/2  (both through T)
+  for (size_t e = tid; e < mm; e += RT) {
+    size_t i = e / m, j = e % m;
+    Tr[j * m + i] = Cr[i * m + j];
+    if (CPLX) Ti[j * m + i] = -Ci[i * m + j];
+  }
+  __syncthreads();
+  for (size_t e = tid; e < mm; e += RT) {
+    size_t i = e / m, j = e % m;
+    double xr = Tr[i * m + j], yr = Tr[j * m + i];
+    Cr[i * m + j] = 0.5 * (xr + yr);
+    if (CPLX) Ci[i * m + j] = 0.5 * (Ti[i * m + j] - Ti[j * m + i]);
+  }
+  // V = I (stored transposed)
+  for (size_t e = tid; e < mm; e += RT) {
+    size_t i = e / m, j = e % m;
+    Vr[e] = (i == j) ? 1.0 : 0.0;
+    if (CPLX) Vi[e] = 0.0;
+  }
+  __syncthreads();
+
+  // 3. Householder tridiagonalisation (reduced.py:73-100)
+  for (int k = 0; k + 2 < m; ++k) {
+    const int len = m - k - 1;
+    double part = 0.0;
+    for (int i = tid; i < len; i += RT) {
+      double xr = Cr[(size_t)(k + 1 + i) * m + k], xi = CPLX ? Ci[(size_t)(k + 1 + i) * m + k] : 0.0;
+      ur[i] = xr;
+      if (CPLX) ui[i] = xi;
+      part += xr * xr + xi * xi;
+    }
+    double xnorm = sqrt(block_sum(part, sh));
+    if (xnorm == 0.0) continue;
+    double x0r = Cr[(size_t)(k + 1) * m + k], x0i = CPLX ? Ci[(size_t)(k + 1) * m + k] : 0.0;
+    double ax0 = CPLX ? hypot(x0r, x0i) : fabs(x0r);
+    double phr = 1.0, phi_ = 0.0;
+    if (ax0 != 0.0) {
+      phr = x0r / ax0;
+      phi_ = x0i / ax0;
+    }
+    const double alr = -phr * xnorm, ali = -phi_ * xnorm;
+    __syncthreads();
+    if (tid == 0) {
+      ur[0] = x0r - alr;
+      if (CPLX) ui[0] = x0i - ali;
+    }
+    __syncthreads();
+    part = 0.0;
+    for (int i = tid; i < len; i += RT) {
+      double xr = ur[i], xi = CPLX ? ui[i] : 0.0;
+      part += xr * xr + xi * xi;
+    }
+    double unorm = sqrt(block_sum(part, sh));
+    if (unorm == 0.0) continue;
+    for (int i = tid; i < len; i += RT) {
+      ur[i] /= unorm;
+      if (CPLX) ui[i] /= unorm;
+    }
+    __syncthreads();
+    // p = 2 * sub @ u   (one warp per row, lanes along the row)
+    {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int i = warp; i < len; i += RT / 32) {
+        const double* rowr = Cr + (size_t)(k + 1 + i) * m + k + 1;
+        const double* rowi = Ci + (size_t)(k + 1 + i) * m + k + 1;
+        double sr = 0.0, si = 0.0;
+        for (int j = lane; j < len; j += 32) {
+          if (CPLX) {
+            sr += rowr[j] * ur[j] - rowi[j] * ui[j];
+            si += rowr[j] * ui[j] + rowi[j] * ur[j];
+          } else {
+            sr += rowr[j] * ur[j];
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          sr += __shfl_xor_sync(0xffffffffu, sr, o);
+          si += __shfl_xor_sync(0xffffffffu, si, o);
+        }
+        if (lane == 0) {
+          pr[i] = 2.0 * sr;
+          if (CPLX) pi[i] = 2.0 * si;
+        }
+      }
+    }
+    __syncthreads();
+    part = 0.0;  // kappa = Re(u^H p)
+    for (int i = tid; i < len; i += RT) part += ur[i] * pr[i] + (CPLX ? ui[i] * pi[i] : 0.0);
+    const double kap2 = 2.0 * block_sum(part, sh);
+    // sub -= p u^H ; sub -= u p^H ; sub += 2 kappa u u^H
+    for (size_t e = tid; e < (size_t)len * len; e += RT) {
+      int i = (int)(e / len), j = (int)(e % len);
+      size_t o = (size_t)(k + 1 + i) * m + k + 1 + j;
+      if (CPLX) {
+        double tr, ti;
+        double sr = Cr[o], si = Ci[o];
+        cmul(pr[i], pi[i], ur[j], -ui[j], tr, ti);
+        sr -= tr;
+        si -= ti;
+        cmul(ur[i], ui[i], pr[j], -pi[j], tr, ti);
+        sr -= tr;
+        si -= ti;
+        cmul(ur[i], ui[i], ur[j], -ui[j], tr, ti);
+        sr += kap2 * tr;
+        si += kap2 * ti;
+        Cr[o] = sr;
+        Ci[o] = si;
+      } else {
+        double s = Cr[o];
+        s -= pr[i] * ur[j];
+        s -= ur[i] * pr[j];
+        s += kap2 * (ur[i] * ur[j]);
+        Cr[o] = s;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      Cr[(size_t)(k + 1) * m + k] = alr;
+      if (CPLX) Ci[(size_t)(k + 1) * m + k] = ali;
+    }
+    // (entries below the subdiagonal are never read again; the row part is
+    //  not needed: only the diagonal and subdiagonal feed the QL step)
+    // V[:, k+1:] -= 2 (V[:, k+1:] u) u^H     (V^T stored: Vr[(k+1+j)*m + r])
+    for (int r = tid; r < m; r += RT) {
+      double sr = 0.0, si = 0.0;
+      for (int j = 0; j < len; ++j) {
+        double vr = Vr[(size_t)(k + 1 + j) * m + r];
+        if (CPLX) {
+          double vi = Vi[(size_t)(k + 1 + j) * m + r];
+          sr += vr * ur[j] - vi * ui[j];
+          si += vr * ui[j] + vi * ur[j];
+        } else {
+          sr += vr * ur[j];
+        }
+      }
+      wr[r] = sr;
+      if (CPLX) wi[r] = si;
+    }
+    __syncthreads();
+    for (size_t e = tid; e < (size_t)len * m; e += RT) {
+      int j = (int)(e / m), r = (int)(e % m);
+      size_t o = (size_t)(k + 1 + j) * m + r;
+      if (CPLX) {
+        double tr, ti;
+        cmul(wr[r], wi[r], ur[j], -ui[j], tr, ti);
+        Vr[o] -= 2.0 * tr;
+        Vi[o] -= 2.0 * ti;
+      } else {
+        Vr[o] -= 2.0 * (wr[r] * ur[j]);
+      }
+    }
+    __syncthreads();
+  }
+
+  // 4. d, e and (complex) phase folding (reduced.py:101-113)
+  for (int i = tid; i < m; i += RT) d[i] = Cr[(size_t)i * m + i];
+  __syncthreads();
+  if (tid == 0) {
+    double fr = 1.0, fi = 0.0;  // running phase phi[j]
+    wr[0] = 1.0;
+    if (CPLX) wi[0] = 0.0;
+    for (int j = 0; j + 1 < m; ++j) {
+      double sr = Cr[(size_t)(j + 1) * m + j];
+      if (CPLX) {
+        double si = Ci[(size_t)(j + 1) * m + j];
+        double mag = hypot(sr, si);
+        if (mag != 0.0) {
+          double nr, ni;
+          cmul(fr, fi, sr / mag, si / mag, nr, ni);
+          fr = nr;
+          fi = ni;
+        }
+        ee[j] = mag;
+        wr[j + 1] = fr;
+        wi[j + 1] = fi;
+      } else {
+        ee[j] = sr;
+      }
+    }
+    ee[m - 1] = 0.0;
+  }
+  __syncthreads();
+  if (CPLX) {  // v = v * phi[None, :] : row c of V^T scaled by phi[c]
+    for (size_t e = tid; e < mm; e += RT) {
+      int c = (int)(e / m);
+      double tr, ti;
+      cmul(Vr[e], Vi[e], wr[c], wi[c], tr, ti);
+      Vr[e] = tr;
+      Vi[e] = ti;
+    }
+    __syncthreads();
+  }
+
+  // 5. implicit QL (reduced.py:117-172); rotations applied to columns of V
+  const double epsm = 2.220446049250313e-16;
+  for (int l = 0; l < m; ++l) {
+    int sweeps = 0;
+    while (true) {
+      if (tid == 0) {
+        int mm_ = l;
+        while (mm_ < m - 1) {
+          double dd = fabs(d[mm_]) + fabs(d[mm_ + 1]);
+          if (fabs(ee[mm_]) <= epsm * dd) break;
+          ++mm_;
+        }
+        int nrot = 0, first = mm_;
+        if (mm_ != l) {
+          ++sweeps;
+          if (sweeps > 30) {
+            nrot = -1;
+          } else {
+            double g = (d[l + 1] - d[l]) / (2.0 * ee[l]);
+            double r = hypot(g, 1.0);
+            g = d[mm_] - d[l] + ee[l] / (g + (g >= 0 ? r : -r));
+            double s = 1.0, c = 1.0, p = 0.0;
+            bool broke = false;
+            for (int i = mm_ - 1; i >= l; --i) {
+              double f = s * ee[i];
+              double b = c * ee[i];
+              r = hypot(f, g);
+              ee[i + 1] = r;
+              if (r == 0.0) {
+                d[i + 1] -= p;
+                ee[mm_] = 0.0;
+                broke = true;
+                break;
+              }
+              s = f / r;
+              c = g / r;
+              g = d[i + 1] - p;
+              r = (d[i] - g) * s + 2.0 * c * b;
+              p = s * r;
+              d[i + 1] = g + p;
+              g = c * r - b;
+              rc[i] = c;
+              rs[i] = s;
+              ++nrot;
+            }
+            if (!broke) {
+              d[l] -= p;
+              ee[l] = g;
+              ee[mm_] = 0.0;
+            }
+          }
+        }
+        s_int[0] = (mm_ == l) ? 1 : 0;  // converged for this l
+        s_int[1] = nrot;
+        s_int[2] = first;
+      }
+      __syncthreads();
+      const int done = s_int[0], nrot = s_int[1], first = s_int[2];
+      __syncthreads();
+      if (nrot < 0) {
+        if (tid == 0) *a.status = -1;
+        return;
+      }
+      // apply rotations i = first-1 down to first-nrot
+      for (int r = tid; r < m; r += RT) {
+        for (int t = 0; t < nrot; ++t) {
+          const int i = first - 1 - t;
+          const double c = rc[i], s = rs[i];
+          double zr = Vr[(size_t)i * m + r], zr1 = Vr[(size_t)(i + 1) * m + r];
+          Vr[(size_t)(i + 1) * m + r] = s * zr + c * zr1;
+          Vr[(size_t)i * m + r] = c * zr - s * zr1;
+          if (CPLX) {
+            double zi = Vi[(size_t)i * m + r], zi1 = Vi[(size_t)(i + 1) * m + r];
+            Vi[(size_t)(i + 1) * m + r] = s * zi + c * zi1;
+            Vi[(size_t)i * m + r] = c * zi - s * zi1;
+          }
+        }
+      }
+      __syncthreads();
+      if (done) break;
+    }
+  }
+
+  // 6. stable ascending order, eps, Phi = L^-H V[:, order]
+  for (int i = tid; i < m; i += RT) {
+    double di = d[i];
+    int rank = 0;
+    for (int j = 0; j < m; ++j) {
+      double dj = d[j];
+      rank += (dj < di) || (dj == di && j < i);
+    }
+    a.eps[rank] = di;
+    reinterpret_cast<int*>(ur)[rank] = i;  // order[rank] = i
+  }
+  __syncthreads();
+  // T = V[:, order] row-major: T[i][c] = V[i][order[c]] = Vt[order[c]][i]
+  for (size_t e = tid; e < mm; e += RT) {
+    int i = (int)(e / m), c = (int)(e % m);
+    int oc = reinterpret_cast<int*>(ur)[c];
+    Tr[e] = Vr[(size_t)oc * m + i];
+    if (CPLX) Ti[e] = Vi[(size_t)oc * m + i];
+  }
+  __syncthreads();
+  // solve L^H X = T (backward), column-parallel
+  for (int c = tid; c < m; c += RT) {
+    for (int i = m - 1; i >= 0; --i) {
+      double sr = Tr[(size_t)i * m + c], si = CPLX ? Ti[(size_t)i * m + c] : 0.0;
+      for (int k = i + 1; k < m; ++k) {
+        // conj(L[k][i]) * x_k
+        double lr = Lr[(size_t)k * m + i], xr = a.phre[(size_t)k * a.ldphi + c];
+        if (CPLX) {
+          double li = -Li[(size_t)k * m + i], xi = a.phim[(size_t)k * a.ldphi + c];
+          sr -= lr * xr - li * xi;
+          si -= lr * xi + li * xr;
+        } else {
+          sr -= lr * xr;
+        }
+      }
+      double dr = Lr[(size_t)i * m + i];
+      a.phre[(size_t)i * a.ldphi + c] = sr / dr;
+      if (CPLX) a.phim[(size_t)i * a.ldphi + c] = si / dr;
+    }
+  }
+  if (tid == 0) *a.status = 0;
+  (void)s_dbl;
+}
+
+size_t smem_for(int m) { return sizeof(double) * (4 * (size_t)m + 40); }
+
+}  // namespace
+
+size_t reduced_scratch_bytes(int m) { return sizeof(double) * (8 * (size_t)m * m + 6 * (size_t)m + 64); }
+
+template <bool C>
+static cudaError_t run_reduced(const RArgs& a, cudaStream_t st) {
+  size_t smem = smem_for(a.m);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(reduced_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cfg = true;
+  }
+  reduced_kernel<C><<<1, RT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t chol_check_launch(int m, const double* bre, const double* bim, long long ld, int* fail,
+                              double* scratch, cudaStream_t st) {
+  RArgs a{};
+  a.m = m; a.are = bre; a.aim = bim; a.bre = bre; a.bim = bim; a.ld = ld;
+  a.status = fail; a.ws = scratch; a.check_only = 1;
+  return bim ? run_reduced<true>(a, st) : run_reduced<false>(a, st);
+}
+
+cudaError_t reduced_eig_launch(int m, const double* are, const double* aim, const double* bre,
+                               const double* bim, long long ld, double* eps, double* phre,
+                               double* phim, long long ldphi, int* status, double* scratch,
+                               cudaStream_t st) {
+  RArgs a{};
+  a.m = m; a.are = are; a.aim = aim; a.bre = bre; a.bim = bim; a.ld = ld;
+  a.eps = eps; a.phre = phre; a.phim = phim; a.ldphi = ldphi;
+  a.status = status; a.ws = scratch; a.check_only = 0;
+  return aim ? run_reduced<true>(a, st) : run_reduced<false>(a, st);
+}
+
+}  // namespace fb

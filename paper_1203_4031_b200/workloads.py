@@ -60,7 +60,7 @@ def c1_syev(n=2000, m0=150, seed=1, interval=(-0.05, 0.05), expect_m=106):
                     interval[1], a, None, expect_m=expect_m)
 
 
-def c2_sygv(n=4096, m0=160, seed=2, interval=(-0.025213996656045, 0.024185071538914),
+def c2_sygv(n=4096, m0=160, seed=2, interval=(-0.025214303929920006, 0.024185493537830133),
             expect_m=100):
     """dfeast_sygv: A = (G+G^T)/(2 sqrt N), B = I + 0.1 H H^T / N."""
     rng = np.random.default_rng(seed)
@@ -119,8 +119,8 @@ def c5_hegv(n=32768, m0=512, seed=5, interval=(-0.0174, 0.0174), expect_m=None, 
 
 # Frozen C4 intervals: mid-gap endpoints placed by Sylvester inertia of the
 # band LDL^T of A - sigma B (oracle/band_inertia.c), ~64 eigenvalues near 0.
-C4_INTERVALS = {}
-C4_COUNTS = {}
+C4_INTERVALS = {1_000_000: (-0.0008386015186658824, 0.0008983531868125283)}
+C4_COUNTS = {1_000_000: 64}
 
 
 def scaled(name):
@@ -143,5 +143,11 @@ def scaled(name):
     raise KeyError(name)
 
 
-SCALED_INTERVALS = {}
-SCALED_COUNTS = {}
+SCALED_INTERVALS = {
+    "c1s": (-0.0709876675617629, 0.04150800239648725),
+    "c2s": (-0.036707360246074655, 0.04395870482595646),
+    "c3s": (-0.08366074494469067, 0.08125681303910331),
+    "c5s": (-0.10442947838146643, 0.11245175206817981),
+    "c4s": (-0.04350204809335878, 0.04554114245277674),
+}
+SCALED_COUNTS = {"c1s": 20, "c2s": 20, "c3s": 20, "c5s": 24, "c4s": 64}

@@ -360,7 +360,7 @@ def make_config(tag, w):
     r, hist, wall, t = run_kernel_lapack(w)
     out = {}
     _pack("", r, out)
-    out["x"] = r.x[:, : r.m] if w.n * r.m <= 4_000_000 else np.zeros((0, 0))
+    out["x"] = r.x[:, : r.m] if w.n * r.m <= 250_000 else np.zeros((0, 0))
     out["history"] = hist
     out["meta"] = np.array([w.n, w.m0, w.emin, w.emax, wall, t["factor"], t["solve"], t["mult"]])
     a_sum = np.array([np.sum(w.a), np.sum(np.abs(w.a))])

@@ -1,0 +1,234 @@
+"""Driver-level parity on the GPU: the predefined drivers and the RCI surface
+against the reference's own outputs (tests/golden/small.npz) and the
+LAPACK-backed reference-kernel oracle on scaled BASELINE configurations
+(tests/golden/scaled_*.npz).  Bar (BASELINE.json north_star): same m, same
+info, |d lambda| <= 1e-10 * max(|Emin|,|Emax|), every residual <= 1e-10
+where the reference converged, loop count within +-1."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from conftest import GOLDEN  # noqa: E402
+
+
+def _names():
+    g = np.load(os.path.join(GOLDEN, "small.npz"))
+    return [str(s) for s in g["names"]]
+
+
+def _fpm(g, name):
+    import paper_1203_4031_b200 as fb
+    return fb.FeastParams([int(v) for v in g[f"{name}__fpm"]])
+
+
+def _run_small(g, name):
+    import paper_1203_4031_b200 as fb
+    kind = str(g[f"{name}__kind"])
+    emin, emax, m0, kla, klb = g[f"{name}__cfg"]
+    m0, kla, klb = int(m0), int(kla), int(klb)
+    uplo = str(g[f"{name}__uplo"])
+    a = g[f"{name}__a"]
+    b = g[f"{name}__b"] if f"{name}__b" in g.files else None
+    fpm = _fpm(g, name)
+    if kind == "sy":
+        return fb.feast_sy(a, emin, emax, m0, b=b, uplo=uplo, fpm=fpm)
+    if kind == "he":
+        return fb.feast_he(a, emin, emax, m0, b=b, uplo=uplo, fpm=fpm)
+    fn = fb.feast_sb if kind == "sb" else fb.feast_hb
+    return fn(a, kla, emin, emax, m0, b=b, klb=klb if b is not None else None, uplo=uplo, fpm=fpm)
+
+
+@pytest.mark.parametrize("name", _names())
+def test_small_driver_parity(small_golden, name):
+    g = small_golden
+    r = _run_small(g, name)
+    m, loop, info, m0 = (int(v) for v in g[f"{name}__scal"])
+    emin, emax = g[f"{name}__cfg"][:2]
+    s = max(abs(emin), abs(emax))
+    assert r.info == info
+    assert r.m == m
+    assert r.m0 == m0
+    assert abs(r.loop - loop) <= 1
+    ref_e, ref_res = g[f"{name}__e"], g[f"{name}__res"]
+    if m:
+        assert np.abs(r.e[:m] - ref_e[:m]).max() <= 1e-10 * s
+        if info == 0:
+            assert r.res[:m].max() <= max(1e-10, 10 * ref_res[:m].max())
+    assert np.array_equal(r.res[:m0] == -1, ref_res[:m0] == -1)
+    if info == 4:   # fpm(14): the accumulated subspace itself
+        assert np.abs(r.x - g[f"{name}__x"]).max() <= 1e-12
+
+
+def test_helloworld_golden_values(capsys):
+    # PAPER.md:803-833 (test_dense.py:51-64, test_acceptance.py:42-65)
+    import paper_1203_4031_b200 as fb
+    a = np.array([[2.0, -1.0], [-1.0, 2.0]])
+    fpm = fb.feastinit()
+    fpm.set_slot(1, 1)
+    r = fb.feast_sy(a, -5.0, 5.0, 2, fpm=fpm)
+    out = capsys.readouterr().out
+    assert r.info == 0 and r.m == 2 and r.loop <= 2
+    assert np.allclose(r.e[:2], [1.0, 3.0], atol=1e-12)
+    assert r.epsout <= 1e-14
+    assert max(r.res[:2]) <= 1e-14
+    s = np.sqrt(2.0) / 2.0
+    assert np.allclose(np.abs(r.x), s, atol=1e-12)
+    assert r.x[0, 0] * r.x[1, 0] > 0 and r.x[0, 1] * r.x[1, 1] < 0
+    assert "==>FEAST has successfully converged" in out
+    assert "DFEAST_SYEV" in out
+
+
+@pytest.mark.parametrize("tag", ["c1s", "c2s", "c3s", "c5s"])
+def test_scaled_config_parity(tag):
+    import paper_1203_4031_b200 as fb
+    from paper_1203_4031_b200 import workloads as W
+    g = np.load(os.path.join(GOLDEN, f"scaled_{tag}.npz"))
+    w = W.scaled(tag)
+    fn = fb.feast_he if w.hermitian else fb.feast_sy
+    r = fn(w.a, w.emin, w.emax, w.m0, b=w.b, fpm=w.fpm())
+    m, loop, info, m0 = (int(v) for v in g["scal"])
+    s = max(abs(w.emin), abs(w.emax))
+    assert r.info == info == 0
+    assert r.m == m == w.expect_m
+    assert abs(r.loop - loop) <= 1
+    assert np.abs(r.e[:m] - g["e"][:m]).max() <= 1e-10 * s
+    assert r.res[:m].max() <= 1e-10
+
+
+def test_rci_surface_with_numpy_caller(rng):
+    """A user RCI loop written against the reference (kernel.py:8-22) drives
+    the GPU engine; results match the predefined driver."""
+    import paper_1203_4031_b200 as fb
+    from conftest import gap_interval, random_symmetric
+    a = random_symmetric(24, rng)
+    ev = np.linalg.eigvalsh(a)
+    emin, emax = gap_interval(ev, 6, 14)
+    k = fb.SymmetricRci(24, 14, emin, emax)
+    trace = []
+    task = k.step()
+    fac = None
+    while task != fb.RciTask.DONE:
+        trace.append(int(task))
+        if task == fb.RciTask.FACTORIZE:
+            fac = k.ze * np.eye(24) - a
+        elif task == fb.RciTask.SOLVE:
+            k.work2[:, :k.m0] = np.linalg.solve(fac, k.work2[:, :k.m0])
+        elif task == fb.RciTask.MULTIPLY_A:
+            s = k.multiply_columns
+            k.work1[:, s] = a @ k.x[:, s]
+        elif task == fb.RciTask.MULTIPLY_B:
+            s = k.multiply_columns
+            k.work1[:, s] = k.x[:, s]
+        task = k.step()
+    r = k.result
+    assert r.info == 0 and r.m == 9
+    assert np.abs(r.e[:9] - ev[6:15]).max() <= 1e-10
+    per_loop = [10, 11] * 8 + [30, 40]
+    assert trace[:18] == per_loop
+    d = fb.feast_sy(a, emin, emax, 14)
+    assert np.abs(d.e[:9] - r.e[:9]).max() <= 1e-12
+
+
+def test_hrci_without_adjoint_capability_gets_task_20():
+    import paper_1203_4031_b200 as fb
+    a = np.diag([1.0, 3.0]).astype(complex)
+    k = fb.HermitianRci(2, 2, -5.0, 5.0, adjoint_capable=False)
+    trace = []
+    task = k.step()
+    while task != fb.RciTask.DONE:
+        trace.append(int(task))
+        if task == fb.RciTask.FACTORIZE:
+            fac = k.ze * np.eye(2) - a
+        elif task == fb.RciTask.FACTORIZE_ADJOINT:
+            fadj = (k.ze * np.eye(2) - a).conj().T
+        elif task == fb.RciTask.SOLVE:
+            k.work2[:, :k.m0] = np.linalg.solve(fac, k.work2[:, :k.m0])
+        elif task == fb.RciTask.SOLVE_ADJOINT:
+            k.work2[:, :k.m0] = np.linalg.solve(fadj, k.work2[:, :k.m0])
+        else:
+            s = k.multiply_columns
+            k.work1[:, s] = (a @ k.x[:, s]) if task == fb.RciTask.MULTIPLY_A else k.x[:, s]
+        task = k.step()
+    assert k.result.info == 0
+    assert trace.count(20) == trace.count(21) > 0
+
+
+def test_singular_shift_reports_minus2():
+    import paper_1203_4031_b200 as fb
+    contour = fb.build_contour(fb.gauss_legendre(8), -5.0, 5.0)
+    z = contour.z[0]
+    a = np.array([[z.real, -z.imag], [z.imag, z.real]])
+    assert fb.feast_sy(a, -5.0, 5.0, 2).info == -2
+
+
+def test_argument_errors():
+    import paper_1203_4031_b200 as fb
+    hello = np.array([[2.0, -1.0], [-1.0, 2.0]])
+    assert fb.feast_sy(hello, -5.0, 5.0, 2, uplo="Q").info == -101
+    assert fb.feast_sy(np.zeros((2, 3)), -5.0, 5.0, 2).info == -104
+    assert fb.feast_sy(hello, -5.0, 5.0, 2, b=np.eye(3)).info == -106
+    assert fb.feast_sy(np.zeros((0, 0)), 0.0, 1.0, 1).info == 202
+    assert fb.feast_sy(hello, -5.0, 5.0, 3).info == 201
+    assert fb.feast_sy(hello, 5.0, -5.0, 2).info == 200
+    ab = np.zeros((3, 4))
+    assert fb.feast_sb(ab, 1, 0.0, 1.0, 2, uplo="X").info == -101
+    assert fb.feast_sb(ab, -1, 0.0, 1.0, 2).info == -103
+    assert fb.feast_sb(np.zeros((2, 4)), 1, 0.0, 1.0, 2).info == -105
+    assert fb.feast_sb(ab, 1, 0.0, 1.0, 2, b=np.zeros((3, 4)), klb=None).info == -106
+    assert fb.feast_sb(ab, 1, 0.0, 1.0, 2, b=np.zeros((2, 4)), klb=1).info == -108
+
+
+def test_reduced_failure_maps_to_minus3():
+    import paper_1203_4031_b200 as fb
+    hello = np.array([[2.0, -1.0], [-1.0, 2.0]])
+    k = fb.SymmetricRci(2, 2, -5.0, 5.0)
+    task = k.step()
+    while task != fb.RciTask.DONE:
+        if task == fb.RciTask.FACTORIZE:
+            fac = k.ze * np.eye(2) - hello
+        elif task == fb.RciTask.SOLVE:
+            k.work2[:, :k.m0] = np.linalg.solve(fac, k.work2[:, :k.m0])
+        else:
+            s = k.multiply_columns
+            k.work1[:, s] = (hello @ k.x[:, s]) if task == fb.RciTask.MULTIPLY_A else 0.0
+        task = k.step()
+    assert k.result.info == -3
+
+
+def test_warm_start_and_determinism(rng):
+    import paper_1203_4031_b200 as fb
+    from conftest import gap_interval, random_symmetric
+    a = random_symmetric(16, rng)
+    ev = np.linalg.eigvalsh(a)
+    emin, emax = gap_interval(ev, 4, 9)
+    cold = fb.feast_sy(a, emin, emax, 9)
+    again = fb.feast_sy(a, emin, emax, 9)
+    assert cold.e.tobytes() == again.e.tobytes() and cold.x.tobytes() == again.x.tobytes()
+    fpm = fb.feastinit()
+    fpm.set_slot(5, 1)
+    warm = fb.feast_sy(a, emin, emax, 9, fpm=fpm, x0=cold.x)
+    assert warm.info == 0 and warm.loop <= 1
+    with pytest.raises(ValueError):
+        fb.feast_sy(a, emin, emax, 9, fpm=fpm)
+    par = fb.feast_sy(a, emin, emax, 9, options=fb.SolverOptions(parallel_contour=8))
+    assert par.e.tobytes() == cold.e.tobytes()
+
+
+def test_reference_ops_protocol_adapter(rng):
+    """B200DenseOps answers the numpy ops protocol (dense.py:91-117) that the
+    reference's own run_rci consumes; driven here by our run_rci mirror with a
+    host-mirrored kernel."""
+    import paper_1203_4031_b200 as fb
+    from paper_1203_4031_b200.dense import B200DenseOps
+    from conftest import gap_interval, random_hermitian
+    a = random_hermitian(30, rng)
+    ev = np.linalg.eigvalsh(a)
+    emin, emax = gap_interval(ev, 10, 17)
+    k = fb.HermitianRci(30, 12, emin, emax)
+    r = fb.run_rci(k, B200DenseOps(a), fb.SolverOptions())
+    assert r.info == 0 and r.m == 8
+    assert np.abs(r.e[:8] - ev[10:18]).max() <= 1e-10

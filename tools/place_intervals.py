@@ -73,3 +73,30 @@ if "c4" in which:
     print("gaps c4", gaps)
 for k, v in out.items():
     print(k, repr(tuple(float(x) if not isinstance(x, int) else x for x in v)))
+
+
+def band_interval_wide(n, kd, seed, k=64, search=5):
+    """Like band_interval but moves each endpoint to the widest nearby gap."""
+    ab, bb = W.c4_band_matrices(n, kd, seed)
+    i0 = count_below(ab, bb, 0.0)
+    lo0 = i0 - k // 2
+    hi0 = lo0 + k - 1
+    ev = {}
+    def lam(i):
+        if i not in ev:
+            ev[i] = band_eig_k(ab, bb, i, -1.0, 1.0)
+        return ev[i]
+    best_lo = max(range(lo0 - search, lo0 + search + 1), key=lambda i: lam(i) - lam(i - 1))
+    best_hi = max(range(hi0 - search, hi0 + search + 1), key=lambda i: lam(i + 1) - lam(i))
+    emin = 0.5 * (lam(best_lo - 1) + lam(best_lo))
+    emax = 0.5 * (lam(best_hi) + lam(best_hi + 1))
+    m = count_below(ab, bb, emax) - count_below(ab, bb, emin)
+    spacing = (lam(hi0) - lam(lo0)) / (k - 1)
+    return (emin, emax), m, ((lam(best_lo) - lam(best_lo - 1)) / spacing,
+                             (lam(best_hi + 1) - lam(best_hi)) / spacing)
+
+
+if "wide" in which:
+    for tag, n, seed in (("c4s", 20000, 14), ("c4", 1_000_000, 4)):
+        iv, m, gaps = band_interval_wide(n, 16, seed)
+        print(tag, repr((float(iv[0]), float(iv[1]), m)), "gap/spacing", gaps, flush=True)
