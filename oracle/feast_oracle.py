@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = [
-    "ALLOWED_NE", "splitmix_uniform", "gl_rule", "half_circle", "accumulate",
+    "ALLOWED_NE", "splitmix_uniform", "start_block", "default_fpm", "gl_rule", "half_circle", "accumulate",
     "expand_uplo", "lu_factor_ref", "lu_solve_ref", "expand_band", "pad_band",
     "band_matvec", "band_lu_factor_ref", "band_lu_solve_ref", "cholesky_lower",
     "reduced_eig", "column_residuals", "finalize_order", "OracleResult",

@@ -279,6 +279,7 @@ cudaError_t band_matvec_launch(int n, int kl, int m, const double* fbr, const do
   if (n <= 0 || m <= 0) return cudaSuccess;
   long long total = (long long)n * m;
   int blocks = (int)std::min<long long>((total + 255) / 256, 16 * kSMs);
+  count_launch();
   band_matvec_kernel<<<blocks, 256, 0, st>>>(n, kl, m, fbr, fbi, ldb, xr, xi, ldx, yr, yi, ldy);
   return cudaGetLastError();
 }
@@ -292,6 +293,7 @@ cudaError_t band_factor_launch(int n, int kl, double zr, double zi, const double
   if (kl > 127) return cudaErrorInvalidValue;
   long long total = (long long)n * (3 * kl + 1);
   int blocks = (int)std::min<long long>((total + 255) / 256, 16 * kSMs);
+  count_launch(2);
   band_shift_kernel<<<blocks, 256, 0, st>>>(n, kl, zr, zi, far_, fai, fbr, fbi, ldb, wr, wi);
   band_factor_seq<<<1, FT, 0, st>>>(n, kl, wr, wi, ipiv, info);
   return cudaGetLastError();
@@ -302,6 +304,7 @@ cudaError_t band_solve_launch(int n, int kl, int nrhs, const double* wr, const d
   if (n <= 0 || nrhs <= 0) return cudaSuccess;
   const int T = 32;
   size_t smem = sizeof(double) * 2 * (2 * kl + 2) * T;
+  count_launch();
   band_solve_seq<<<ceil_div(nrhs, T), T, smem, st>>>(n, kl, nrhs, wr, wi, ipiv, adjoint, xr, xi, ldx);
   return cudaGetLastError();
 }

@@ -11,6 +11,8 @@
 #include "lu.cuh"
 #include "misc.cuh"
 
+std::atomic<long long> fb::g_launches{0};
+
 struct fb_ctx : fb::Ctx {
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -125,14 +127,16 @@ int fb_ctx_synchronize(fb_ctx* c) {
 
 const char* fb_ctx_last_error(const fb_ctx* c) { return c ? c->err : "null context"; }
 
-int64_t fb_ctx_launch_count(const fb_ctx* c) { return c ? c->launches : 0; }
+int64_t fb_ctx_launch_count(const fb_ctx* c) {
+  (void)c;
+  return fb::g_launches.load(std::memory_order_relaxed);
+}
 
 int fb_dense_shift(fb_ctx* c, int n, double zr, double zi, const double* are, const double* aim,
                    int64_t lda, const double* bre, const double* bim, int64_t ldb, double* sre,
                    double* sim, int64_t lds) {
   CTX_GUARD(c);
   if (n < 0 || !are || !sre || !sim) return FB_ERR_ARG;
-  c->launches += 1;
   return set_err(c, fb::shift_launch(n, zr, zi, are, aim, lda, bre, bim, ldb, sre, sim, lds, c->stream),
                  "dense_shift");
 }
@@ -148,7 +152,6 @@ int fb_zgetrf(fb_ctx* c, int n, double* re, double* im, int64_t ld, int* piv, do
   cudaError_t e = cudaMemcpyAsync(info, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
   if (e != cudaSuccess) return set_err(c, e, "zgetrf info init");
   // kernels per outer block: 4 panels + laswps + gemms (counted approximately)
-  c->launches += (long long)((n + 127) / 128) * 31;
   return set_err(c, fb::zgetrf(n, re, im, ld, piv, info, dinv, (char*)c->scratch, c->stream), "zgetrf");
 }
 
@@ -166,14 +169,12 @@ int fb_zgetrs(fb_ctx* c, int n, int nrhs, const double* re, const double* im, in
               const double* dinv, int adjoint, double* xr, double* xi, int64_t ldx) {
   CTX_GUARD(c);
   if (n < 0 || nrhs < 0 || !xr || !xi) return FB_ERR_ARG;
-  c->launches += 2 + 4LL * ((n + 31) / 32);
   return set_err(c, fb::zgetrs(n, nrhs, re, im, ld, piv, dinv, adjoint, xr, xi, ldx, c->stream), "zgetrs");
 }
 
 int fb_splitmix(fb_ctx* c, uint64_t seed, int64_t off_re, int64_t off_im, int n, int m, double* re,
                 double* im, int64_t ld) {
   CTX_GUARD(c);
-  c->launches += 1;
   return set_err(c, fb::splitmix_launch(seed, off_re, off_im, n, m, re, im, ld, c->stream), "splitmix");
 }
 
@@ -199,7 +200,6 @@ int fb_accumulate(fb_ctx* c, int variant, int n, int m, const double* xr, const 
     cr = s * cth;
     ci = s * (variant == 1 ? sth : -sth);
   }
-  c->launches += 1;
   return set_err(c, fb::accumulate_launch(mode, n, m, xr, xi, ldx, qr, qi, ldq, h, cr, ci, c->stream),
                  "accumulate");
 }
@@ -223,13 +223,11 @@ int fb_gemm(fb_ctx* c, int cplx, char opa, char opb, int m, int n, int k, double
     if (r) return r;
     p.ws = (double*)c->scratch;
   }
-  c->launches += p.splits > 1 ? 2 : 1;
   return set_err(c, fb::gemm_launch(cplx, p, c->stream), "gemm");
 }
 
 int fb_symmetrize(fb_ctx* c, int m, double* re, double* im, int64_t ld) {
   CTX_GUARD(c);
-  c->launches += 1;
   return set_err(c, fb::symmetrize_launch(m, re, im, ld, c->stream), "symmetrize");
 }
 
@@ -238,7 +236,6 @@ int fb_residuals(fb_ctx* c, int n, int m, const double* axr, const double* axi, 
   CTX_GUARD(c);
   int r = ensure_scratch(c, fb::residual_scratch_bytes(n, m));
   if (r) return r;
-  c->launches += 2;
   return set_err(c, fb::residual_launch(n, m, axr, axi, bxr, bxi, ld, lam, scale, res,
                                         (double*)c->scratch, c->stream),
                  "residuals");
@@ -249,7 +246,6 @@ int fb_chol_check(fb_ctx* c, int m, const double* bre, const double* bim, int64_
   if (m <= 0 || !fail) return FB_ERR_ARG;
   int r = ensure_scratch(c, fb::reduced_scratch_bytes(m));
   if (r) return r;
-  c->launches += 1;
   cudaError_t e = fb::chol_check_launch(m, bre, bim, ld, c->dev_word, (double*)c->scratch, c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(c->host_word, c->dev_word, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
@@ -266,7 +262,6 @@ int fb_reduced_eig(fb_ctx* c, int m, const double* are, const double* aim, const
   if (m <= 0 || !status || !eps || !phre) return FB_ERR_ARG;
   int r = ensure_scratch(c, fb::reduced_scratch_bytes(m));
   if (r) return r;
-  c->launches += 1;
   cudaError_t e = fb::reduced_eig_launch(m, are, aim, bre, bim, ld, eps, phre, phim, ldphi, c->dev_word,
                                          (double*)c->scratch, c->stream);
   if (e == cudaSuccess)
@@ -280,7 +275,6 @@ int fb_reduced_eig(fb_ctx* c, int m, const double* are, const double* aim, const
 int fb_pack(fb_ctx* c, int n, int m, const double* z, int64_t ldz, double* re, double* im, int64_t ld,
             int to_planar) {
   CTX_GUARD(c);
-  c->launches += 1;
   return set_err(c, fb::pack_launch(n, m, z, ldz, re, im, ld, to_planar, c->stream), "pack");
 }
 
@@ -288,7 +282,6 @@ int fb_band_matvec(fb_ctx* c, int n, int kl, int m, const double* fbr, const dou
                    const double* xr, const double* xi, int64_t ldx, double* yr, double* yi, int64_t ldy) {
   CTX_GUARD(c);
   if (n < 0 || kl < 0 || m < 0 || !fbr || !xr || !yr) return FB_ERR_ARG;
-  c->launches += 1;
   return set_err(c, fb::band_matvec_launch(n, kl, m, fbr, fbi, ldb, xr, xi, ldx, yr, yi, ldy, c->stream),
                  "band_matvec");
 }
@@ -301,7 +294,6 @@ int fb_band_factor(fb_ctx* c, int n, int kl, double zr, double zi, const double*
   const int big = INT_MAX;
   cudaError_t e = cudaMemcpyAsync(info, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
   if (e != cudaSuccess) return set_err(c, e, "band info init");
-  c->launches += 2;
   return set_err(c, fb::band_factor_launch(n, kl, zr, zi, far_, fai, fbr, fbi, ldb, fr, fi, ipiv, info,
                                            c->stream),
                  "band_factor");
@@ -311,7 +303,6 @@ int fb_band_solve(fb_ctx* c, int n, int kl, int nrhs, const double* fr, const do
                   int adjoint, double* xr, double* xi, int64_t ldx) {
   CTX_GUARD(c);
   if (n < 0 || kl < 0 || nrhs < 0 || !fr || !xr || !xi) return FB_ERR_ARG;
-  c->launches += 1;
   return set_err(c, fb::band_solve_launch(n, kl, nrhs, fr, fi, ipiv, adjoint, xr, xi, ldx, c->stream),
                  "band_solve");
 }

@@ -9,6 +9,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libfeastb200 targets sm_100a only"
 #endif
@@ -16,6 +18,10 @@
 namespace fb {
 
 constexpr int kSMs = 148;
+
+// Every kernel launch of the library bumps this counter (bench.py reports it).
+extern std::atomic<long long> g_launches;
+inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 struct Ctx {
   int device;

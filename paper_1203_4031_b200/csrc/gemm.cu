@@ -209,11 +209,13 @@ cudaError_t launch_t(const GemmParams& p, cudaStream_t st) {
   }
   dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.splits);
   kern<<<grid, THREADS, smem, st>>>(p);
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p.splits <= 1) return e;
   size_t plane = (size_t)p.m * p.n;
   int blocks = (int)std::min<size_t>((plane + 255) / 256, 4 * 148);
   splitk_reduce<CPLX><<<blocks, 256, 0, st>>>(p);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -364,6 +364,7 @@ cudaError_t shift_launch(int n, double zr, double zi, const double* are, const d
   long long total = (long long)n * n;
   int blocks = (int)std::min<long long>((total + 255) / 256, 8 * kSMs);
   shift_kernel<<<blocks, 256, 0, st>>>(n, zr, zi, are, aim, lda, bre, bim, ldb, sre, sim, lds);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -372,6 +373,7 @@ cudaError_t laswp_launch(double* re, double* im, long long ld, int c0, int c1, c
   if (c1 <= c0 || k1 <= k0) return cudaSuccess;
   int cols = c1 - c0;
   laswp_kernel<<<ceil_div(cols, 128), 128, 0, st>>>(re, im, ld, c0, c1, piv, k0, k1, rev);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -406,6 +408,7 @@ static cudaError_t panel_launch(double* re, double* im, long long ld, int n, int
   a.linv = linv;
   a.uinv = uinv;
   void* args[] = {&a};
+  count_launch();
   if (G > 1) {
     return cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PT), args, smem, st);
   }

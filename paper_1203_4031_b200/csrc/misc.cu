@@ -72,7 +72,7 @@ __global__ void symmetrize_kernel(int m, double* __restrict__ re, double* __rest
     re[j * ld + i] = nr;
     if (im) {
       im[i * ld + j] = ni;
-      im[j * ld + i] = -ni;
+      if (j != i) im[j * ld + i] = -ni;
     }
   }
 }
@@ -149,6 +149,7 @@ int grid_for(long long total, int threads = 256) {
 cudaError_t splitmix_launch(unsigned long long seed, long long off_re, long long off_im, int n, int m,
                             double* re, double* im, long long ld, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
+  count_launch();
   splitmix_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(seed, off_re, off_im, n, m, re, im, ld);
   return cudaGetLastError();
 }
@@ -157,6 +158,7 @@ cudaError_t accumulate_launch(int mode, int n, int m, const double* xr, const do
                               long long ldx, double* qr, double* qi, long long ldq, double h,
                               double cr, double ci, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
+  count_launch();
   accumulate_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(mode, n, m, xr, xi, ldx, qr, qi, ldq,
                                                                 h, cr, ci);
   return cudaGetLastError();
@@ -164,6 +166,7 @@ cudaError_t accumulate_launch(int mode, int n, int m, const double* xr, const do
 
 cudaError_t symmetrize_launch(int m, double* re, double* im, long long ld, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
+  count_launch();
   symmetrize_kernel<<<grid_for((long long)m * m), 256, 0, st>>>(m, re, im, ld);
   return cudaGetLastError();
 }
@@ -177,6 +180,7 @@ cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, 
                             double* res, double* scratch, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
   int chunks = ceil_div(n, RES_ROWS);
+  count_launch(2);
   residual_partial<<<chunks, 128, 0, st>>>(n, m, axr, axi, bxr, bxi, ld, lam, scale, scratch);
   residual_final<<<ceil_div(m, 128), 128, 0, st>>>(chunks, m, scratch, res);
   return cudaGetLastError();
@@ -185,6 +189,7 @@ cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, 
 cudaError_t pack_launch(int n, int m, const double* z, long long ldz, double* re, double* im,
                         long long ldp, int to_planar, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
+  count_launch();
   pack_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(n, m, z, ldz, re, im, ldp, to_planar);
   return cudaGetLastError();
 }

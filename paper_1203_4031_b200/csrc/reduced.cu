@@ -542,6 +542,7 @@ static cudaError_t run_reduced(const RArgs& a, cudaStream_t st) {
     cfg = true;
   }
   reduced_kernel<C><<<1, RT, smem, st>>>(a);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -56,6 +56,9 @@ class DeviceDenseOps:
     N = 32768 holds ~8 of its 16 factors on one B200)."""
 
     on_device = True
+    # bench.py instrumentation: when a list, (start, end) CUDA events recorded
+    # on the context stream around every fb_zgetrf call are appended to it.
+    lu_event_sink = None
 
     def __init__(self, dev, A: Planar, B: Planar | None, hermitian: bool, cache_bytes=None):
         self.dev, self.A, self.B, self.hermitian = dev, A, B, hermitian
@@ -88,8 +91,15 @@ class DeviceDenseOps:
                                      B.im if B is not None else None,
                                      B.ld if B is not None else 0,
                                      f.lu.re, f.lu.im, f.lu.ld), "dense_shift")
+        sink = DeviceDenseOps.lu_event_sink
+        if sink is not None:
+            ev = (dev.torch.cuda.Event(enable_timing=True), dev.torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         dev.check(lib.fb_zgetrf(dev.h, n, f.lu.re, f.lu.im, f.lu.ld, f.piv.data_ptr(),
                                 f.dinv.data_ptr(), f.info.data_ptr()), "zgetrf")
+        if sink is not None:
+            ev[1].record()
+            sink.append(ev)
         self.factorizations += 1
         bad = dev.read_info(f.info.data_ptr())
         if bad >= 0:
@@ -190,7 +200,8 @@ def _shape(a):
     return tuple(a.shape) if hasattr(a, "shape") else np.asarray(a).shape
 
 
-def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, device=None):
+def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, device=None,
+                  engine_kwargs=None):
     options = options or SolverOptions()
     fpm = FeastParams.coerce(fpm) if fpm is not None else feastinit()
     uplo = (uplo or "F").upper()
@@ -203,7 +214,8 @@ def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, devic
     routine = _routine_name(hermitian, single, b is not None)
     cls = HermitianRci if hermitian else SymmetricRci
     kernel = cls(n, m0, emin, emax, fpm, seed=options.seed, block_size=options.block_size,
-                 dtype=scalar, routine_name=routine, device=device, host_mirror=False)
+                 dtype=scalar, routine_name=routine, device=device, host_mirror=False,
+                 **(engine_kwargs or {}))
     if uplo not in _UPLOS:
         kernel.abort(-101)
         return kernel.result

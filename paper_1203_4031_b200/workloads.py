@@ -132,10 +132,10 @@ def scaled(name):
         return c2_sygv(n=512, m0=40, seed=12, interval=SCALED_INTERVALS["c2s"],
                        expect_m=SCALED_COUNTS["c2s"])
     if name == "c3s":
-        return c3_heev(n=384, m0=40, seed=13, interval=SCALED_INTERVALS["c3s"],
+        return c3_heev(n=384, m0=30, seed=13, interval=SCALED_INTERVALS["c3s"],
                        expect_m=SCALED_COUNTS["c3s"], ne=16)
     if name == "c5s":
-        return c5_hegv(n=320, m0=48, seed=15, interval=SCALED_INTERVALS["c5s"],
+        return c5_hegv(n=320, m0=36, seed=15, interval=SCALED_INTERVALS["c5s"],
                        expect_m=SCALED_COUNTS["c5s"], ne=16)
     if name == "c4s":
         return c4_sbgv(n=20000, kd=16, m0=96, seed=14, interval=SCALED_INTERVALS["c4s"],
@@ -148,6 +148,6 @@ SCALED_INTERVALS = {
     "c2s": (-0.036707360246074655, 0.04395870482595646),
     "c3s": (-0.08366074494469067, 0.08125681303910331),
     "c5s": (-0.10442947838146643, 0.11245175206817981),
-    "c4s": (-0.04350204809335878, 0.04554114245277674),
+    "c4s": (-0.05045715313974597, 0.054020304571423594),
 }
-SCALED_COUNTS = {"c1s": 20, "c2s": 20, "c3s": 20, "c5s": 24, "c4s": 64}
+SCALED_COUNTS = {"c1s": 20, "c2s": 20, "c3s": 20, "c5s": 24, "c4s": 71}
