@@ -169,7 +169,11 @@ int fb_zgetrs(fb_ctx* c, int n, int nrhs, const double* re, const double* im, in
               const double* dinv, int adjoint, double* xr, double* xi, int64_t ldx) {
   CTX_GUARD(c);
   if (n < 0 || nrhs < 0 || !xr || !xi) return FB_ERR_ARG;
-  return set_err(c, fb::zgetrs(n, nrhs, re, im, ld, piv, dinv, adjoint, xr, xi, ldx, c->stream), "zgetrs");
+  int r = ensure_scratch(c, sizeof(double) * 2 * (size_t)n * (size_t)nrhs);
+  if (r) return r;
+  return set_err(c, fb::zgetrs(n, nrhs, re, im, ld, piv, dinv, adjoint, xr, xi, ldx, (double*)c->scratch,
+                               c->stream),
+                 "zgetrs");
 }
 
 int fb_splitmix(fb_ctx* c, uint64_t seed, int64_t off_re, int64_t off_im, int n, int m, double* re,
