@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "lu.cuh"
+#include "trsm.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -492,15 +493,20 @@ size_t zgetrf_scratch_bytes(int n) {
 
 // Factor side storage, in doubles: [nblk][4][PW][PW] diagonal inverses (L re/im,
 // U re/im), then perm[n] ints, then nblk swap lists.
+// ... then the per-block sweep operators G (trsm.cu) of the fused solves.
+static size_t lists_doubles(int n) { return ((size_t)ceil_div(n, PW) * LIST + 1) / 2 + 2; }
 size_t dinv_doubles(int n) {
   size_t nblk = ceil_div(n, PW);
-  return nblk * 4 * PW * PW + ceil_div(n, 2) + (nblk * LIST + 1) / 2 + 2;
+  return nblk * 4 * PW * PW + ceil_div(n, 2) + lists_doubles(n) + gmat_doubles(n);
 }
 const int* factor_perm(const double* dinv, int n) {
   return reinterpret_cast<const int*>(dinv + (size_t)ceil_div(n, PW) * 4 * PW * PW);
 }
 static int* factor_lists(double* dinv, int n) {
   return reinterpret_cast<int*>(dinv + (size_t)ceil_div(n, PW) * 4 * PW * PW + ceil_div(n, 2));
+}
+const double* factor_gmat(const double* dinv, int n) {
+  return dinv + (size_t)ceil_div(n, PW) * 4 * PW * PW + ceil_div(n, 2) + lists_doubles(n);
 }
 
 cudaError_t shift_launch(int n, double zr, double zi, const double* are, const double* aim,
@@ -681,7 +687,8 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
   if (psmem > 200 * 1024) return cudaErrorInvalidValue;
   perm_kernel<<<1, 256, psmem, st>>>(n, lists, const_cast<int*>(factor_perm(dinv, n)));
   count_launch();
-  return cudaGetLastError();
+  if ((e = cudaGetLastError())) return e;
+  return gmat_launch(n, re, im, ld, dinv, const_cast<double*>(factor_gmat(dinv, n)), st);
 }
 
 // Solve op(A) X = B in place for X (n x nrhs planar, ldx) from zgetrf output.
@@ -700,6 +707,22 @@ cudaError_t zgetrs(int n, int nrhs, const double* re, const double* im, long lon
   auto L = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW; };
   auto U = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW + 2 * PW * PW; };
   auto row = [&](const double* p, int r, int c) { return p + (long long)r * ld + c; };
+  static const bool blocked = getenv("FB_SOLVE_BLOCKED") != nullptr;  // A/B switch for tests
+  if (!blocked) {
+    const double* gm = factor_gmat(dinv, n);
+    if (!adjoint) {
+      if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
+      if ((e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
+      if ((e = permute_rows_launch(n, nrhs, perm, 1, tr, ti, nrhs, xr, xi, ldx, st))) return e;
+      if ((e = sweep_launch(0, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st))) return e;
+      return sweep_launch(1, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st);
+    }
+    if ((e = sweep_launch(2, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st))) return e;
+    if ((e = sweep_launch(3, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st))) return e;
+    if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
+    if ((e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
+    return permute_rows_launch(n, nrhs, perm, 0, tr, ti, nrhs, xr, xi, ldx, st);
+  }
   if (!adjoint) {
     // X <- P X (one gather through the scratch copy)
     if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
