@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "lu.cuh"
+#include "panel.cuh"
 #include "trsm.cuh"
 
 namespace cg = cooperative_groups;
@@ -35,10 +36,6 @@ namespace {
 
 constexpr int PW = 32;         // sub-panel width (= diagonal block size of dinv)
 constexpr int NB = 128;        // outer block (trailing-update K)
-constexpr int PT = 128;        // threads per panel CTA
-constexpr int SP = PW + 1;     // smem pitch of panel rows (conflict-free per-row access)
-constexpr int RPC_CLUSTER = 384;  // max panel rows per CTA in cluster mode (~203 KB smem)
-constexpr int MAX_CLUSTER = 16;
 constexpr int LIST = 1 + 2 * 2 * PW;  // per-block swap list: cnt, dst[2PW], src[2PW]
 
 // ---------------------------------------------------------------------------
@@ -149,346 +146,11 @@ __global__ void permute_rows_kernel(int n, int m, const int* __restrict__ perm, 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Sub-panel factorization.
-// ---------------------------------------------------------------------------
-struct PanelArgs {
-  double* re;
-  double* im;
-  long long ld;
-  int n, c0, pw, rpc;
-  int* piv;
-  int* info;
-  double* xrec;   // GRID mode: [2][G][2 + 2*PW] (val, row, data), in L2
-  double* xrowr;  // GRID mode: [2][2*PW] copy of row rj
-  double* linv;   // [2 planes][PW][PW] inverse of unit-lower diagonal block
-  double* uinv;   // [2 planes][PW][PW] inverse of upper diagonal block
-  int* list;      // [LIST] swap list of this sub-panel
-};
-
-struct Best {
-  double v;
-  int r;
-};
-__device__ __forceinline__ Best better(Best a, Best b) {
-  if (b.v > a.v || (b.v == a.v && b.r < a.r)) return b;
-  return a;
-}
-__device__ __forceinline__ Best warp_best(Best b) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    Best t;
-    t.v = __shfl_xor_sync(0xffffffffu, b.v, o);
-    t.r = __shfl_xor_sync(0xffffffffu, b.r, o);
-    b = better(b, t);
-  }
-  return b;
-}
-
-__device__ Best block_best(Best b, Best* red) {
-  b = warp_best(b);
-  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = b;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    Best t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : Best{-1.0, 0x7fffffff};
-    t = warp_best(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  return red[0];
-}
-
-enum { MODE_GRID = 0, MODE_CLUSTER = 1 };
-
-template <int MODE>
-__global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
-  extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x;
-  int G, g;
-  if (MODE == MODE_CLUSTER) {
-    G = (int)cg::this_cluster().num_blocks();
-    g = (int)cg::this_cluster().block_rank();
-  } else {
-    G = gridDim.x;
-    g = blockIdx.x;
-  }
-  const int rbeg = a.c0 + g * a.rpc;
-  const int rend = min(a.n, rbeg + a.rpc);
-  const int cnt = max(0, rend - rbeg);
-  constexpr int REC = 2 + 2 * PW;
-  double* sre = sm;                       // [rpc][SP]
-  double* sim = sm + a.rpc * SP;          // [rpc][SP]
-  double* prow = sim + a.rpc * SP;        // [2*PW] pivot row
-  double* rrow = prow + 2 * PW;           // [2*PW] old row rj
-  double* lrec = rrow + 2 * PW;           // CLUSTER: [2][REC] own record
-  double* lrj = lrec + 2 * REC;           // CLUSTER: [2][2*PW] own copy of row rj
-  __shared__ Best red[PT / 32];
-  __shared__ int s_gw;
-  __shared__ int s_piv[PW];
-
-  for (int e = tid; e < cnt * PW; e += PT) {
-    int lr = e / PW, c = e % PW;
-    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
-    bool ok = c < a.pw;
-    sre[lr * SP + c] = ok ? a.re[off] : 0.0;
-    sim[lr * SP + c] = ok ? a.im[off] : 0.0;
-  }
-  __syncthreads();
-  const int owner_rows = a.rpc;
-
-  for (int j = 0; j < a.pw; ++j) {
-    const int rj = a.c0 + j;
-    const int par = j & 1;
-    // 1. local argmax of |a[r, j]| over own rows r >= rj
-    Best b{-1.0, 0x7fffffff};
-    for (int lr = tid; lr < cnt; lr += PT) {
-      int gr = rbeg + lr;
-      if (gr >= rj) b = better(b, Best{cabs_(sre[lr * SP + j], sim[lr * SP + j]), gr});
-    }
-    b = block_best(b, red);
-    const bool own_best = b.v >= 0.0 && b.r >= rbeg && b.r < rend;
-    const bool own_rj = rj >= rbeg && rj < rend;
-    // 2. publish the record (and the owner's copy of row rj), 3. barrier
-    if (MODE == MODE_CLUSTER) {
-      double* rec = lrec + par * REC;
-      if (tid == 0) {
-        rec[0] = b.v;
-        rec[1] = (double)b.r;
-      }
-      if (own_best) {
-        int lr = b.r - rbeg;
-        for (int c = tid; c < PW; c += PT) {
-          rec[2 + c] = sre[lr * SP + c];
-          rec[2 + PW + c] = sim[lr * SP + c];
-        }
-      }
-      if (own_rj) {
-        int lr = rj - rbeg;
-        for (int c = tid; c < PW; c += PT) {
-          lrj[par * 2 * PW + c] = sre[lr * SP + c];
-          lrj[par * 2 * PW + PW + c] = sim[lr * SP + c];
-        }
-      }
-      cg::this_cluster().sync();
-    } else {
-      double* rec = a.xrec + ((size_t)par * G + g) * REC;
-      if (tid == 0) {
-        __stcg(rec, b.v);
-        __stcg(rec + 1, (double)b.r);
-      }
-      if (own_best) {
-        int lr = b.r - rbeg;
-        for (int c = tid; c < PW; c += PT) {
-          __stcg(rec + 2 + c, sre[lr * SP + c]);
-          __stcg(rec + 2 + PW + c, sim[lr * SP + c]);
-        }
-      }
-      if (own_rj) {
-        int lr = rj - rbeg;
-        for (int c = tid; c < PW; c += PT) {
-          __stcg(a.xrowr + par * 2 * PW + c, sre[lr * SP + c]);
-          __stcg(a.xrowr + par * 2 * PW + PW + c, sim[lr * SP + c]);
-        }
-      }
-      if (G > 1) {
-        __threadfence();
-        cg::this_grid().sync();
-      } else {
-        __syncthreads();
-      }
-    }
-    // 4. global winner
-    Best w{-1.0, 0x7fffffff};
-    int wg = 0;
-    for (int q = tid; q < G; q += PT) {
-      Best t;
-      if (MODE == MODE_CLUSTER) {
-        const double* rr = cg::this_cluster().map_shared_rank(lrec + par * REC, q);
-        t = Best{rr[0], (int)rr[1]};
-      } else {
-        const double* rr = a.xrec + ((size_t)par * G + q) * REC;
-        t = Best{__ldcg(rr), (int)__ldcg(rr + 1)};
-      }
-      Best nb = better(w, t);
-      if (nb.r != w.r || nb.v != w.v) wg = q;
-      w = nb;
-    }
-    Best wb = block_best(w, red);
-    if (w.v == wb.v && w.r == wb.r && w.v >= 0.0) s_gw = wg;  // unique row -> unique writer
-    const int rj_owner = (rj - a.c0) / owner_rows;
-    for (int c = tid; c < 2 * PW; c += PT) {
-      if (MODE == MODE_CLUSTER)
-        rrow[c] = cg::this_cluster().map_shared_rank(lrj + par * 2 * PW, rj_owner)[c];
-      else
-        rrow[c] = __ldcg(a.xrowr + par * 2 * PW + c);
-    }
-    __syncthreads();
-    const int gw = s_gw;
-    for (int c = tid; c < 2 * PW; c += PT) {
-      if (MODE == MODE_CLUSTER)
-        prow[c] = cg::this_cluster().map_shared_rank(lrec + par * REC, gw)[2 + c];
-      else
-        prow[c] = __ldcg(a.xrec + ((size_t)par * G + gw) * REC + 2 + c);
-    }
-    int p = wb.r;
-    const bool zero = !(wb.v > 0.0);
-    if (zero) {
-      p = rj;
-      if (g == 0 && tid == 0) atomicMin(a.info, rj + 1);
-    }
-    if (tid == 0) s_piv[j] = p;
-    if (g == 0 && tid == 0) a.piv[rj] = p;
-    __syncthreads();
-    // 5. swap rows p <-> rj (full panel width), then scale and rank-1 update
-    if (p != rj) {
-      if (p >= rbeg && p < rend) {
-        int lr = p - rbeg;
-        for (int c = tid; c < PW; c += PT) {
-          sre[lr * SP + c] = rrow[c];
-          sim[lr * SP + c] = rrow[PW + c];
-        }
-      }
-      if (own_rj) {
-        int lr = rj - rbeg;
-        for (int c = tid; c < PW; c += PT) {
-          sre[lr * SP + c] = prow[c];
-          sim[lr * SP + c] = prow[PW + c];
-        }
-      }
-      __syncthreads();
-    }
-    if (!zero) {
-      const double pr = prow[j], pi = prow[PW + j];
-      const double den = pr * pr + pi * pi;
-      const double ir = pr / den, ii = -pi / den;
-      for (int lr = tid; lr < cnt; lr += PT) {
-        if (rbeg + lr <= rj) continue;
-        double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
-        double lr_ = xr * ir - xi * ii, li = xr * ii + xi * ir;
-        sre[lr * SP + j] = lr_;
-        sim[lr * SP + j] = li;
-        for (int c = j + 1; c < a.pw; ++c) {
-          double ur = prow[c], ui = prow[PW + c];
-          sre[lr * SP + c] -= lr_ * ur - li * ui;
-          sim[lr * SP + c] -= lr_ * ui + li * ur;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (MODE == MODE_CLUSTER) cg::this_cluster().sync();  // remote readers done before exit
-
-  // write back
-  for (int e = tid; e < cnt * a.pw; e += PT) {
-    int lr = e / a.pw, c = e % a.pw;
-    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
-    a.re[off] = sre[lr * SP + c];
-    a.im[off] = sim[lr * SP + c];
-  }
-  if (g != 0) return;
-  // swap list of this sub-panel (dst row <- content of src row)
-  if (tid < 32) {
-    const int t = tid;
-    const int bend = a.c0 + a.pw;
-    const int pt = t < a.pw ? s_piv[t] : -1;
-    const bool extra = t < a.pw && pt >= bend;
-    int first = t;
-    if (extra)
-      for (int q = 0; q < t; ++q)
-        if (s_piv[q] == pt) { first = q; break; }
-    const unsigned repmask = __ballot_sync(0xffffffffu, extra && first == t);
-    const int nextra = __popc(repmask);
-    const int slot = __popc(repmask & ((1u << first) - 1u));
-    __shared__ int s_pos[PW], s_row[2 * PW], s_content[2 * PW];
-    if (t < a.pw) s_pos[t] = extra ? a.pw + slot : pt - a.c0;
-    if (t < a.pw) s_row[t] = a.c0 + t;
-    if (extra && first == t) s_row[a.pw + slot] = pt;
-    __syncwarp();
-    const int total = a.pw + nextra;
-    for (int q = t; q < total; q += 32) s_content[q] = s_row[q];
-    __syncwarp();
-    if (t == 0) {
-      for (int q = 0; q < a.pw; ++q) {
-        int x = s_content[q];
-        s_content[q] = s_content[s_pos[q]];
-        s_content[s_pos[q]] = x;
-      }
-      a.list[0] = total;
-    }
-    __syncwarp();
-    for (int q = t; q < total; q += 32) {
-      a.list[1 + q] = s_row[q];
-      a.list[1 + 2 * PW + q] = s_content[q];
-    }
-  }
-  // diagonal-block inverses
-  if (tid < PW) {
-    const int c = tid;
-    double xr[PW], xi[PW];
-#pragma unroll
-    for (int i = 0; i < PW; ++i) {
-      double sr = (i == c) ? 1.0 : 0.0, si = 0.0;
-      if (i < a.pw) {
-#pragma unroll
-        for (int k = 0; k < PW; ++k) {
-          if (k < i) {
-            double lr_ = sre[i * SP + k], li = sim[i * SP + k];
-            sr -= lr_ * xr[k] - li * xi[k];
-            si -= lr_ * xi[k] + li * xr[k];
-          }
-        }
-      }
-      xr[i] = sr;
-      xi[i] = si;
-    }
-#pragma unroll
-    for (int i = 0; i < PW; ++i) {
-      a.linv[i * PW + c] = xr[i];
-      a.linv[PW * PW + i * PW + c] = xi[i];
-    }
-#pragma unroll
-    for (int i = PW - 1; i >= 0; --i) {
-      double sr = (i == c) ? 1.0 : 0.0, si = 0.0;
-      if (i < a.pw) {
-#pragma unroll
-        for (int k = 0; k < PW; ++k) {
-          if (k > i && k < a.pw) {
-            double ur = sre[i * SP + k], ui = sim[i * SP + k];
-            sr -= ur * xr[k] - ui * xi[k];
-            si -= ur * xi[k] + ui * xr[k];
-          }
-        }
-        double dr = sre[i * SP + i], di = sim[i * SP + i];
-        double den = dr * dr + di * di;
-        double qr = (sr * dr + si * di) / den, qi = (si * dr - sr * di) / den;
-        sr = qr;
-        si = qi;
-      }
-      xr[i] = sr;
-      xi[i] = si;
-    }
-#pragma unroll
-    for (int i = 0; i < PW; ++i) {
-      a.uinv[i * PW + c] = xr[i];
-      a.uinv[PW * PW + i * PW + c] = xi[i];
-    }
-  }
-}
-
-int g_grid_max_blocks = 0;
-bool g_cluster_ok = false;
-bool g_cluster_probed = false;
-
-size_t panel_smem(int rpc) { return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * (2 + 2 * PW) + 4 * PW); }
-
 }  // namespace
 
 size_t zgetrf_scratch_bytes(int n) {
   (void)n;
-  const int Gmax = 4 * kSMs;
-  return sizeof(double) * (2 * (size_t)Gmax * (2 + 2 * PW) + 2 * 2 * PW) + 256;
+  return panel_scratch_bytes();
 }
 
 // Factor side storage, in doubles: [nblk][4][PW][PW] diagonal inverses (L re/im,
@@ -530,82 +192,6 @@ cudaError_t permute_rows_launch(int n, int m, const int* perm, int gather, const
   return cudaGetLastError();
 }
 
-static cudaError_t panel_launch(double* re, double* im, long long ld, int n, int c0, int pw, int* piv,
-                                int* info, char* scratch, double* linv, double* uinv, int* list,
-                                cudaStream_t st) {
-  const int rows = n - c0;
-  const int smem_cap = 210 * 1024;
-  PanelArgs a;
-  a.re = re; a.im = im; a.ld = ld; a.n = n; a.c0 = c0; a.pw = pw;
-  a.piv = piv; a.info = info; a.linv = linv; a.uinv = uinv; a.list = list;
-  double* d = reinterpret_cast<double*>(scratch);
-  const int Gmax = 4 * kSMs;
-  a.xrec = d;
-  a.xrowr = d + 2 * (size_t)Gmax * (2 + 2 * PW);
-  if (!g_cluster_probed) {
-    g_cluster_probed = true;
-    cudaFuncSetAttribute(panel_kernel<MODE_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
-    cudaFuncSetAttribute(panel_kernel<MODE_CLUSTER>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(panel_kernel<MODE_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = MAX_CLUSTER;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(MAX_CLUSTER);
-    cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = panel_smem(RPC_CLUSTER);
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int clusters = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, panel_kernel<MODE_CLUSTER>, &cfg);
-    g_cluster_ok = (e == cudaSuccess && clusters >= 1);
-    cudaGetLastError();
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, panel_kernel<MODE_GRID>, PT, panel_smem(128));
-    g_grid_max_blocks = std::max(1, nb);
-  }
-  count_launch();
-  if (rows <= RPC_CLUSTER || (g_cluster_ok && rows <= MAX_CLUSTER * RPC_CLUSTER)) {
-    int G = std::max(1, std::min(MAX_CLUSTER, ceil_div(rows, RPC_CLUSTER)));
-    // keep CTA 0 holding the whole diagonal block, and use more CTAs for tall panels
-    if (rows > 2 * PW) G = std::max(G, std::min(MAX_CLUSTER, ceil_div(rows, 256)));
-    G = std::max(1, std::min(G, rows / PW));
-    int rpc = ceil_div(rows, G);
-    G = ceil_div(rows, rpc);
-    a.rpc = rpc;
-    size_t smem = panel_smem(rpc);
-    if (G == 1) {
-      panel_kernel<MODE_GRID><<<1, PT, smem, st>>>(a);
-      return cudaGetLastError();
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = G;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, panel_kernel<MODE_CLUSTER>, a);
-  }
-  int G = ceil_div(rows, 128);
-  G = std::max(1, std::min(G, rows / PW));
-  G = std::min(G, g_grid_max_blocks * kSMs);
-  int rpc = ceil_div(rows, G);
-  G = ceil_div(rows, rpc);
-  a.rpc = rpc;
-  size_t smem = panel_smem(rpc);
-  if ((int)smem > smem_cap) return cudaErrorInvalidConfiguration;
-  void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)panel_kernel<MODE_GRID>, dim3(G), dim3(PT), args, smem, st);
-}
-
 static cudaError_t swap_list_launch(double* re, double* im, long long ld, int n, int c0, int pw,
                                     const int* list, cudaStream_t st) {
   int ncols = n - pw;
@@ -629,7 +215,10 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
     for (int s = 0; s < nb; s += PW) {
       const int c0 = k + s, pw = std::min(PW, nb - s), blk = c0 / PW;
       int* list = lists + (size_t)blk * LIST;
-      e = panel_launch(re, im, ld, n, c0, pw, piv, info, scratch, L(blk), U(blk), list, st);
+      PanelArgs pa{};
+      pa.re = re; pa.im = im; pa.ld = ld; pa.n = n; pa.c0 = c0; pa.pw = pw;
+      pa.piv = piv; pa.info = info; pa.linv = L(blk); pa.uinv = U(blk); pa.list = list;
+      e = panel_launch(pa, scratch, st);
       if (e != cudaSuccess) return e;
       if ((e = swap_list_launch(re, im, ld, n, c0, pw, list, st))) return e;
       const int rest = k + nb - (c0 + pw);

@@ -1,0 +1,428 @@
+// Sub-panel factorization of the blocked shifted LU (restates dense.py:40-49
+// for PW = 32 columns at a time).
+//
+// The panel rows [c0, n) x [c0, c0+pw) live in shared memory, split across the
+// CTAs of a thread-block cluster (<= 16 CTAs, records exchanged through DSMEM,
+// one barrier.cluster per column) or, for panels taller than the cluster's
+// shared memory, across a cooperative grid (records through L2, one grid
+// barrier per column).  Per column j:
+//   1. every thread scans its rows for max |a(r, j)| (np.abs = hypot; first
+//      index wins ties, as np.argmax, dense.py:41); warp shuffles + one
+//      barrier give the CTA candidate, whose full panel row is published
+//      together with the current row rj (owner only);
+//   2. barrier.cluster / grid barrier;
+//   3. warp 0 reduces the <= 16 (or G) candidates and fetches the pivot row and
+//      the old row rj (DSMEM / L2);
+//   4. each row thread scales its multiplier l = a(r, j) / pivot (rows p and rj
+//      take their swapped contents first);
+//   5. all threads apply the rank-1 update over the flattened (row, column)
+//      space of the remaining panel columns.
+// At the end CTA 0 emits the inverses of the 32x32 unit-lower and upper
+// diagonal blocks and the (dst, src) list of the panel's row interchanges.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "panel.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fb {
+
+namespace {
+
+constexpr int PW = PANEL_W;
+constexpr int PT = 256;          // threads per panel CTA (8 warps)
+constexpr int NW = PT / 32;
+constexpr int SP = PW + 1;       // row pitch of the panel in smem (conflict-free per-row access)
+constexpr int REC = 2 + 2 * PW;  // exchange record: |pivot|, row, row data (re, im)
+
+struct Best {
+  double v;
+  int r;
+};
+__device__ __forceinline__ Best better(Best a, Best b) {
+  if (b.v > a.v || (b.v == a.v && b.r < a.r)) return b;
+  return a;
+}
+__device__ __forceinline__ Best warp_best(Best b) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    Best t;
+    t.v = __shfl_xor_sync(0xffffffffu, b.v, o);
+    t.r = __shfl_xor_sync(0xffffffffu, b.r, o);
+    b = better(b, t);
+  }
+  return b;
+}
+
+// Column `c` of the inverse of the unit-lower (LOWER) or upper diagonal block
+// held in rows 0..pw-1 of the CTA's panel (two partial sums break the FMA chain).
+template <bool LOWER>
+__device__ void tri_inverse(const PanelArgs& a, const double* sre, const double* sim, int c) {
+  double xr[PW], xi[PW];
+#pragma unroll
+  for (int s = 0; s < PW; ++s) {
+    const int i = LOWER ? s : PW - 1 - s;
+    double sr0 = (i == c) ? 1.0 : 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
+    if (i < a.pw) {
+#pragma unroll
+      for (int k = 0; k < PW; k += 2) {
+        const bool in0 = LOWER ? (k < i) : (k > i && k < a.pw);
+        const bool in1 = LOWER ? (k + 1 < i) : (k + 1 > i && k + 1 < a.pw);
+        if (in0) {
+          double ur = sre[i * SP + k], ui = sim[i * SP + k];
+          sr0 -= ur * xr[k] - ui * xi[k];
+          si0 -= ur * xi[k] + ui * xr[k];
+        }
+        if (in1) {
+          double ur = sre[i * SP + k + 1], ui = sim[i * SP + k + 1];
+          sr1 -= ur * xr[k + 1] - ui * xi[k + 1];
+          si1 -= ur * xi[k + 1] + ui * xr[k + 1];
+        }
+      }
+    }
+    double sr = sr0 + sr1, si = si0 + si1;
+    if (!LOWER && i < a.pw) {
+      double dr = sre[i * SP + i], di = sim[i * SP + i];
+      double den = dr * dr + di * di;
+      double qr = (sr * dr + si * di) / den, qi = (si * dr - sr * di) / den;
+      sr = qr;
+      si = qi;
+    }
+    xr[i] = sr;
+    xi[i] = si;
+  }
+  double* out = LOWER ? a.linv : a.uinv;
+#pragma unroll
+  for (int i = 0; i < PW; ++i) {
+    out[i * PW + c] = xr[i];
+    out[PW * PW + i * PW + c] = xi[i];
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int G, g;
+  if (MODE == PANEL_CLUSTER) {
+    G = (int)cg::this_cluster().num_blocks();
+    g = (int)cg::this_cluster().block_rank();
+  } else {
+    G = gridDim.x;
+    g = blockIdx.x;
+  }
+  const int rbeg = a.c0 + g * a.rpc;
+  const int rend = min(a.n, rbeg + a.rpc);
+  const int cnt = max(0, rend - rbeg);
+  double* sre = sm;                       // [rpc][SP]
+  double* sim = sm + a.rpc * SP;          // [rpc][SP]
+  double* prow = sim + a.rpc * SP;        // [2*PW] pivot row
+  double* rrow = prow + 2 * PW;           // [2*PW] old row rj
+  double* lrec = rrow + 2 * PW;           // CLUSTER: [2][REC] own record
+  double* lrj = lrec + 2 * REC;           // CLUSTER: [2][2*PW] own copy of row rj
+  __shared__ Best red[NW];
+  __shared__ Best s_best;
+  __shared__ int s_p, s_zero;
+  __shared__ int s_piv[PW];
+
+  for (int e = tid; e < cnt * PW; e += PT) {
+    int lr = e / PW, c = e % PW;
+    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
+    bool ok = c < a.pw;
+    sre[lr * SP + c] = ok ? a.re[off] : 0.0;
+    sim[lr * SP + c] = ok ? a.im[off] : 0.0;
+  }
+  __syncthreads();
+
+  for (int j = 0; j < a.pw; ++j) {
+    const int rj = a.c0 + j;
+    const int par = j & 1;
+    const bool own_rj = rj >= rbeg && rj < rend;
+    // 1. local argmax of |a[r, j]| over own rows r >= rj
+    Best b{-1.0, 0x7fffffff};
+    for (int lr = max(0, rj - rbeg) + tid; lr < cnt; lr += PT)
+      b = better(b, Best{cabs_(sre[lr * SP + j], sim[lr * SP + j]), rbeg + lr});
+    b = warp_best(b);
+    if (lane == 0) red[warp] = b;
+    __syncthreads();
+    if (warp == 0) {
+      Best t = lane < NW ? red[lane] : Best{-1.0, 0x7fffffff};
+      t = warp_best(t);
+      if (lane == 0) s_best = t;
+      const bool own_best = t.v >= 0.0 && t.r >= rbeg && t.r < rend;
+      double* rec = MODE == PANEL_CLUSTER ? lrec + par * REC : a.xrec + ((size_t)par * G + g) * REC;
+      if (MODE == PANEL_CLUSTER) {
+        if (lane == 0) {
+          rec[0] = t.v;
+          rec[1] = (double)t.r;
+        }
+        if (own_best) {
+          rec[2 + lane] = sre[(t.r - rbeg) * SP + lane];
+          rec[2 + PW + lane] = sim[(t.r - rbeg) * SP + lane];
+        }
+      } else {
+        if (lane == 0) {
+          __stcg(rec, t.v);
+          __stcg(rec + 1, (double)t.r);
+        }
+        if (own_best) {
+          __stcg(rec + 2 + lane, sre[(t.r - rbeg) * SP + lane]);
+          __stcg(rec + 2 + PW + lane, sim[(t.r - rbeg) * SP + lane]);
+        }
+      }
+    } else if (warp == 1 && own_rj) {
+      double* dst = MODE == PANEL_CLUSTER ? lrj + par * 2 * PW : a.xrowr + par * 2 * PW;
+      const double vr = sre[(rj - rbeg) * SP + lane], vi = sim[(rj - rbeg) * SP + lane];
+      if (MODE == PANEL_CLUSTER) {
+        dst[lane] = vr;
+        dst[PW + lane] = vi;
+      } else {
+        __stcg(dst + lane, vr);
+        __stcg(dst + PW + lane, vi);
+      }
+    }
+    // 2. exchange barrier
+    if (MODE == PANEL_CLUSTER) {
+      cg::this_cluster().sync();
+    } else if (G > 1) {
+      __threadfence();
+      cg::this_grid().sync();
+    } else {
+      __syncthreads();
+    }
+    // 3. winner, pivot row and old row rj (warp 0)
+    if (warp == 0) {
+      Best w{-1.0, 0x7fffffff};
+      int wg = 0;
+      for (int q = lane; q < G; q += 32) {
+        Best t;
+        if (MODE == PANEL_CLUSTER) {
+          const double* rr = cg::this_cluster().map_shared_rank(lrec + par * REC, q);
+          t = Best{rr[0], (int)rr[1]};
+        } else {
+          const double* rr = a.xrec + ((size_t)par * G + q) * REC;
+          t = Best{__ldcg(rr), (int)__ldcg(rr + 1)};
+        }
+        Best nb = better(w, t);
+        if (nb.r != w.r || nb.v != w.v) wg = q;
+        w = nb;
+      }
+      Best wb = warp_best(w);
+      const unsigned m = __ballot_sync(0xffffffffu, w.r == wb.r && w.v == wb.v && w.v >= 0.0);
+      const int gw = __shfl_sync(0xffffffffu, wg, m ? __ffs(m) - 1 : 0);
+      const int rj_owner = (rj - a.c0) / a.rpc;
+      if (MODE == PANEL_CLUSTER) {
+        const double* src = cg::this_cluster().map_shared_rank(lrec + par * REC, gw);
+        prow[lane] = src[2 + lane];
+        prow[PW + lane] = src[2 + PW + lane];
+        const double* rsrc = cg::this_cluster().map_shared_rank(lrj + par * 2 * PW, rj_owner);
+        rrow[lane] = rsrc[lane];
+        rrow[PW + lane] = rsrc[PW + lane];
+      } else {
+        const double* src = a.xrec + ((size_t)par * G + gw) * REC;
+        prow[lane] = __ldcg(src + 2 + lane);
+        prow[PW + lane] = __ldcg(src + 2 + PW + lane);
+        rrow[lane] = __ldcg(a.xrowr + par * 2 * PW + lane);
+        rrow[PW + lane] = __ldcg(a.xrowr + par * 2 * PW + PW + lane);
+      }
+      if (lane == 0) {
+        const bool zero = !(wb.v > 0.0);
+        const int p = zero ? rj : wb.r;
+        s_p = p;
+        s_zero = zero;
+        s_piv[j] = p;
+        if (g == 0) {
+          a.piv[rj] = p;
+          if (zero) atomicMin(a.info, rj + 1);
+        }
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const bool zero = s_zero;
+    // 4. swapped rows take their new contents; multipliers l = a(r, j) / pivot
+    double ir = 0.0, ii = 0.0;
+    if (!zero) {
+      const double pr = prow[j], pi = prow[PW + j];
+      const double den = pr * pr + pi * pi;
+      ir = pr / den;
+      ii = -pi / den;
+    }
+    for (int lr = tid; lr < cnt; lr += PT) {
+      const int gr = rbeg + lr;
+      if (gr == rj) {
+        if (p != rj) {
+          for (int c = 0; c < PW; ++c) {
+            sre[lr * SP + c] = prow[c];
+            sim[lr * SP + c] = prow[PW + c];
+          }
+        }
+      } else if (gr > rj) {
+        if (gr == p) {
+          for (int c = 0; c < PW; ++c) {
+            sre[lr * SP + c] = rrow[c];
+            sim[lr * SP + c] = rrow[PW + c];
+          }
+        }
+        if (!zero) {
+          const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
+          sre[lr * SP + j] = xr * ir - xi * ii;
+          sim[lr * SP + j] = xr * ii + xi * ir;
+        }
+      }
+    }
+    __syncthreads();
+    // 5. rank-1 update of columns j+1 .. pw-1 on rows below rj
+    const int width = a.pw - j - 1;
+    const int lr0 = max(0, rj + 1 - rbeg);
+    if (!zero && width > 0) {
+      const int nrow = cnt - lr0;
+      for (int e = tid; e < nrow * width; e += PT) {
+        const int lr = lr0 + e / width, c = j + 1 + e % width;
+        const double lrv = sre[lr * SP + j], liv = sim[lr * SP + j];
+        const double ur = prow[c], ui = prow[PW + c];
+        sre[lr * SP + c] -= lrv * ur - liv * ui;
+        sim[lr * SP + c] -= lrv * ui + liv * ur;
+      }
+    }
+    __syncthreads();
+  }
+  if (MODE == PANEL_CLUSTER) cg::this_cluster().sync();  // remote readers done before exit
+
+  for (int e = tid; e < cnt * a.pw; e += PT) {
+    int lr = e / a.pw, c = e % a.pw;
+    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
+    a.re[off] = sre[lr * SP + c];
+    a.im[off] = sim[lr * SP + c];
+  }
+  if (g != 0) return;
+  if (warp == 0) {
+    // (dst, src) list of the panel's interchanges (dst row <- content of src row)
+    const int t = lane;
+    const int bend = a.c0 + a.pw;
+    const int pt = t < a.pw ? s_piv[t] : -1;
+    const bool extra = t < a.pw && pt >= bend;
+    int first = t;
+    if (extra)
+      for (int q = 0; q < t; ++q)
+        if (s_piv[q] == pt) { first = q; break; }
+    const unsigned repmask = __ballot_sync(0xffffffffu, extra && first == t);
+    const int nextra = __popc(repmask);
+    const int slot = __popc(repmask & ((1u << first) - 1u));
+    __shared__ int s_pos[PW], s_row[2 * PW], s_content[2 * PW];
+    if (t < a.pw) s_pos[t] = extra ? a.pw + slot : pt - a.c0;
+    if (t < a.pw) s_row[t] = a.c0 + t;
+    if (extra && first == t) s_row[a.pw + slot] = pt;
+    __syncwarp();
+    const int total = a.pw + nextra;
+    for (int q = t; q < total; q += 32) s_content[q] = s_row[q];
+    __syncwarp();
+    if (t == 0) {
+      for (int q = 0; q < a.pw; ++q) {
+        int x = s_content[q];
+        s_content[q] = s_content[s_pos[q]];
+        s_content[s_pos[q]] = x;
+      }
+      a.list[0] = total;
+    }
+    __syncwarp();
+    for (int q = t; q < total; q += 32) {
+      a.list[1 + q] = s_row[q];
+      a.list[1 + 2 * PW + q] = s_content[q];
+    }
+  } else if (warp == 1) {
+    tri_inverse<true>(a, sre, sim, lane);
+  } else if (warp == 2) {
+    tri_inverse<false>(a, sre, sim, lane);
+  }
+}
+
+int g_grid_max_blocks = 0;
+bool g_cluster_ok = false;
+bool g_probed = false;
+
+size_t panel_smem(int rpc) {
+  return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * REC + 4 * PW);
+}
+
+}  // namespace
+
+size_t panel_scratch_bytes() {
+  const int Gmax = 4 * kSMs;
+  return sizeof(double) * (2 * (size_t)Gmax * REC + 2 * 2 * PW) + 256;
+}
+
+cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
+  const int rows = a.n - a.c0;
+  const int smem_cap = 210 * 1024;
+  const int rpc_cluster = 384;
+  const int max_cluster = 16;
+  double* d = reinterpret_cast<double*>(scratch);
+  const int Gmax = 4 * kSMs;
+  a.xrec = d;
+  a.xrowr = d + 2 * (size_t)Gmax * REC;
+  if (!g_probed) {
+    g_probed = true;
+    cudaFuncSetAttribute(panel_kernel<PANEL_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
+    cudaFuncSetAttribute(panel_kernel<PANEL_CLUSTER>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = max_cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(max_cluster);
+    cfg.blockDim = dim3(PT);
+    cfg.dynamicSmemBytes = panel_smem(rpc_cluster);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, panel_kernel<PANEL_CLUSTER>, &cfg);
+    g_cluster_ok = (e == cudaSuccess && clusters >= 1);
+    cudaGetLastError();
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, panel_kernel<PANEL_GRID>, PT, panel_smem(128));
+    g_grid_max_blocks = std::max(1, nb);
+  }
+  count_launch();
+  if (rows <= rpc_cluster || (g_cluster_ok && rows <= max_cluster * rpc_cluster)) {
+    int G = std::max(1, std::min(max_cluster, ceil_div(rows, rpc_cluster)));
+    if (rows > 2 * PW) G = std::max(G, std::min(max_cluster, ceil_div(rows, 192)));
+    G = std::max(1, std::min(G, rows / PW));
+    int rpc = ceil_div(rows, G);
+    G = ceil_div(rows, rpc);
+    a.rpc = rpc;
+    size_t smem = panel_smem(rpc);
+    if (G == 1) {
+      panel_kernel<PANEL_GRID><<<1, PT, smem, st>>>(a);
+      return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(PT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, panel_kernel<PANEL_CLUSTER>, a);
+  }
+  int G = ceil_div(rows, 128);
+  G = std::max(1, std::min(G, rows / PW));
+  G = std::min(G, g_grid_max_blocks * kSMs);
+  int rpc = ceil_div(rows, G);
+  G = ceil_div(rows, rpc);
+  a.rpc = rpc;
+  size_t smem = panel_smem(rpc);
+  if ((int)smem > smem_cap) return cudaErrorInvalidConfiguration;
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((void*)panel_kernel<PANEL_GRID>, dim3(G), dim3(PT), args, smem, st);
+}
+
+}  // namespace fb

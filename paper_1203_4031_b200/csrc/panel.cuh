@@ -1,0 +1,27 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace fb {
+
+constexpr int PANEL_W = 32;
+enum { PANEL_GRID = 0, PANEL_CLUSTER = 1 };
+
+struct PanelArgs {
+  double* re;
+  double* im;
+  long long ld;
+  int n, c0, pw, rpc;
+  int* piv;
+  int* info;
+  double* xrec;   // GRID mode exchange records (set by panel_launch)
+  double* xrowr;  // GRID mode copy of row rj
+  double* linv;   // [2 planes][PW][PW] inverse of the unit-lower diagonal block
+  double* uinv;   // [2 planes][PW][PW] inverse of the upper diagonal block
+  int* list;      // [1 + 4*PW] (dst, src) row-interchange list of this panel
+};
+
+size_t panel_scratch_bytes();
+cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st);
+
+}  // namespace fb
