@@ -11,6 +11,10 @@
 #include "lu.cuh"
 #include "misc.cuh"
 
+namespace fb {
+void panel_profile_read(unsigned long long* out);
+}
+
 std::atomic<long long> fb::g_launches{0};
 
 struct fb_ctx : fb::Ctx {
@@ -309,6 +313,12 @@ int fb_band_solve(fb_ctx* c, int n, int kl, int nrhs, const double* fr, const do
   if (n < 0 || kl < 0 || nrhs < 0 || !fr || !xr || !xi) return FB_ERR_ARG;
   return set_err(c, fb::band_solve_launch(n, kl, nrhs, fr, fi, ipiv, adjoint, xr, xi, ldx, c->stream),
                  "band_solve");
+}
+
+// Debug only (not part of the ABI header): cycles per panel phase, CTA 0 / thread 0.
+int fb_debug_panel_profile(unsigned long long* out8) {
+  fb::panel_profile_read(out8);
+  return FB_OK;
 }
 
 }  // extern "C"

@@ -100,6 +100,18 @@ __device__ void tri_inverse(const PanelArgs& a, const double* sre, const double*
   }
 }
 
+// Phase timers of CTA 0 / thread 0 (read with fb_debug_panel_profile; tools/).
+__device__ unsigned long long g_panel_prof[8];
+#define PROBE_START long long _t_last = clock64()
+#define PROBE(k)                                          \
+  do {                                                    \
+    if (g == 0 && tid == 0) {                             \
+      long long _now = clock64();                         \
+      atomicAdd(&g_panel_prof[k], (unsigned long long)(_now - _t_last)); \
+      _t_last = _now;                                     \
+    }                                                     \
+  } while (0)
+
 template <int MODE>
 __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double sm[];
@@ -136,6 +148,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   __syncthreads();
 
   for (int j = 0; j < a.pw; ++j) {
+    PROBE_START;
     const int rj = a.c0 + j;
     const int par = j & 1;
     const bool own_rj = rj >= rbeg && rj < rend;
@@ -146,6 +159,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
     b = warp_best(b);
     if (lane == 0) red[warp] = b;
     __syncthreads();
+    PROBE(0);
     if (warp == 0) {
       Best t = lane < NW ? red[lane] : Best{-1.0, 0x7fffffff};
       t = warp_best(t);
@@ -182,6 +196,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
         __stcg(dst + PW + lane, vi);
       }
     }
+    PROBE(1);
     // 2. exchange barrier
     if (MODE == PANEL_CLUSTER) {
       cg::this_cluster().sync();
@@ -191,6 +206,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
     } else {
       __syncthreads();
     }
+    PROBE(2);
     // 3. winner, pivot row and old row rj (warp 0)
     if (warp == 0) {
       Best w{-1.0, 0x7fffffff};
@@ -239,6 +255,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       }
     }
     __syncthreads();
+    PROBE(3);
     const int p = s_p;
     const bool zero = s_zero;
     // 4. swapped rows take their new contents; multipliers l = a(r, j) / pivot
@@ -273,6 +290,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       }
     }
     __syncthreads();
+    PROBE(4);
     // 5. rank-1 update of columns j+1 .. pw-1 on rows below rj
     const int width = a.pw - j - 1;
     const int lr0 = max(0, rj + 1 - rbeg);
@@ -287,6 +305,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       }
     }
     __syncthreads();
+    PROBE(5);
   }
   if (MODE == PANEL_CLUSTER) cg::this_cluster().sync();  // remote readers done before exit
 
@@ -347,6 +366,12 @@ size_t panel_smem(int rpc) {
 }
 
 }  // namespace
+
+void panel_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_panel_prof, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_panel_prof, z, sizeof(z));
+}
 
 size_t panel_scratch_bytes() {
   const int Gmax = 4 * kSMs;

@@ -48,3 +48,15 @@ for r in range(reps):
           f"({8 / 3 * n**3 / lu_ms / 1e9:.2f} TF, host issue {1e3 * (t1 - t0):.1f} ms), "
           f"zgetrs {e[2].elapsed_time(e[3]):.3f} ms ({8 * n * n * nrhs / e[2].elapsed_time(e[3]) / 1e9:.2f} TF), "
           f"adjoint {e[3].elapsed_time(e[4]):.3f} ms, launches {dev.launches()}", flush=True)
+if os.environ.get("PANEL_PROF"):
+    buf = (ctypes.c_ulonglong * 8)()
+    dev.lib.fb_debug_panel_profile(buf)   # reset
+    dev.check(dev.lib.fb_dense_shift(dev.h, n, 0.01, 0.02, P(A.re), None, A.ld, None, None, 0,
+                                     P(lu.re), P(lu.im), lu.ld), "shift")
+    dev.check(dev.lib.fb_zgetrf(dev.h, n, P(lu.re), P(lu.im), lu.ld, P(piv.data_ptr()),
+                                P(dinv.data_ptr()), P(info.data_ptr())), "zgetrf")
+    torch.cuda.synchronize()
+    dev.lib.fb_debug_panel_profile(buf)
+    names = ["argmax", "publish", "barrier", "winner", "swap+scale", "update"]
+    cols = n
+    print("panel phase cycles per column:", {k: round(buf[i] / cols) for i, k in enumerate(names)})
