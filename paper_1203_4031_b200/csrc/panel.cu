@@ -35,6 +35,7 @@ constexpr int PT = 256;          // threads per panel CTA (8 warps)
 constexpr int NW = PT / 32;
 constexpr int SP = PW + 1;       // row pitch of the panel in smem (conflict-free per-row access)
 constexpr int REC = 2 + 2 * PW;  // exchange record: |pivot|, row, row data (re, im)
+constexpr int SB = 8;            // sub-block width: per-column updates stay inside it
 
 struct Best {
   double v;
@@ -134,7 +135,6 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   double* lrec = rrow + 2 * PW;           // CLUSTER: [2][REC] own record
   double* lrj = lrec + 2 * REC;           // CLUSTER: [2][2*PW] own copy of row rj
   __shared__ Best red[NW];
-  __shared__ Best s_best;
   __shared__ int s_p, s_zero;
   __shared__ int s_piv[PW];
 
@@ -147,10 +147,13 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   }
   __syncthreads();
 
+  __shared__ double s_inv[2];
+  double* ubuf = lrj + 2 * 2 * PW;        // [2][SB][PW] U rows of the finished sub-block
   for (int j = 0; j < a.pw; ++j) {
     PROBE_START;
     const int rj = a.c0 + j;
     const int par = j & 1;
+    const int sb0 = (j / SB) * SB, sb_end = min(a.pw, sb0 + SB);
     const bool own_rj = rj >= rbeg && rj < rend;
     // 1. local argmax of |a[r, j]| over own rows r >= rj
     Best b{-1.0, 0x7fffffff};
@@ -160,29 +163,26 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
     if (lane == 0) red[warp] = b;
     __syncthreads();
     PROBE(0);
+    // 2. publish the CTA candidate (warp 0) and the current row rj (warp 1, owner)
     if (warp == 0) {
       Best t = lane < NW ? red[lane] : Best{-1.0, 0x7fffffff};
       t = warp_best(t);
-      if (lane == 0) s_best = t;
       const bool own_best = t.v >= 0.0 && t.r >= rbeg && t.r < rend;
       double* rec = MODE == PANEL_CLUSTER ? lrec + par * REC : a.xrec + ((size_t)par * G + g) * REC;
+      const double d0 = lane == 0 ? t.v : (double)t.r;
+      const double vr = own_best ? sre[(t.r - rbeg) * SP + lane] : 0.0;
+      const double vi = own_best ? sim[(t.r - rbeg) * SP + lane] : 0.0;
       if (MODE == PANEL_CLUSTER) {
-        if (lane == 0) {
-          rec[0] = t.v;
-          rec[1] = (double)t.r;
-        }
+        if (lane < 2) rec[lane] = d0;
         if (own_best) {
-          rec[2 + lane] = sre[(t.r - rbeg) * SP + lane];
-          rec[2 + PW + lane] = sim[(t.r - rbeg) * SP + lane];
+          rec[2 + lane] = vr;
+          rec[2 + PW + lane] = vi;
         }
       } else {
-        if (lane == 0) {
-          __stcg(rec, t.v);
-          __stcg(rec + 1, (double)t.r);
-        }
+        if (lane < 2) __stcg(rec + lane, d0);
         if (own_best) {
-          __stcg(rec + 2 + lane, sre[(t.r - rbeg) * SP + lane]);
-          __stcg(rec + 2 + PW + lane, sim[(t.r - rbeg) * SP + lane]);
+          __stcg(rec + 2 + lane, vr);
+          __stcg(rec + 2 + PW + lane, vi);
         }
       }
     } else if (warp == 1 && own_rj) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       }
     }
     PROBE(1);
-    // 2. exchange barrier
+    // 3. exchange barrier
     if (MODE == PANEL_CLUSTER) {
       cg::this_cluster().sync();
     } else if (G > 1) {
@@ -207,8 +207,18 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       __syncthreads();
     }
     PROBE(2);
-    // 3. winner, pivot row and old row rj (warp 0)
+    // 4. winner, pivot row, old row rj, pivot reciprocal (warp 0)
     if (warp == 0) {
+      const int rj_owner = (rj - a.c0) / a.rpc;
+      double r0, r1;  // old row rj, fetched while the candidates are reduced
+      if (MODE == PANEL_CLUSTER) {
+        const double* rsrc = cg::this_cluster().map_shared_rank(lrj + par * 2 * PW, rj_owner);
+        r0 = rsrc[lane];
+        r1 = rsrc[PW + lane];
+      } else {
+        r0 = __ldcg(a.xrowr + par * 2 * PW + lane);
+        r1 = __ldcg(a.xrowr + par * 2 * PW + PW + lane);
+      }
       Best w{-1.0, 0x7fffffff};
       int wg = 0;
       for (int q = lane; q < G; q += 32) {
@@ -227,23 +237,27 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       Best wb = warp_best(w);
       const unsigned m = __ballot_sync(0xffffffffu, w.r == wb.r && w.v == wb.v && w.v >= 0.0);
       const int gw = __shfl_sync(0xffffffffu, wg, m ? __ffs(m) - 1 : 0);
-      const int rj_owner = (rj - a.c0) / a.rpc;
+      double p0, p1;
       if (MODE == PANEL_CLUSTER) {
         const double* src = cg::this_cluster().map_shared_rank(lrec + par * REC, gw);
-        prow[lane] = src[2 + lane];
-        prow[PW + lane] = src[2 + PW + lane];
-        const double* rsrc = cg::this_cluster().map_shared_rank(lrj + par * 2 * PW, rj_owner);
-        rrow[lane] = rsrc[lane];
-        rrow[PW + lane] = rsrc[PW + lane];
+        p0 = src[2 + lane];
+        p1 = src[2 + PW + lane];
       } else {
         const double* src = a.xrec + ((size_t)par * G + gw) * REC;
-        prow[lane] = __ldcg(src + 2 + lane);
-        prow[PW + lane] = __ldcg(src + 2 + PW + lane);
-        rrow[lane] = __ldcg(a.xrowr + par * 2 * PW + lane);
-        rrow[PW + lane] = __ldcg(a.xrowr + par * 2 * PW + PW + lane);
+        p0 = __ldcg(src + 2 + lane);
+        p1 = __ldcg(src + 2 + PW + lane);
+      }
+      prow[lane] = p0;
+      prow[PW + lane] = p1;
+      rrow[lane] = r0;
+      rrow[PW + lane] = r1;
+      const bool zero = !(wb.v > 0.0);
+      if (lane == j) {  // lane j holds the pivot value
+        double den = p0 * p0 + p1 * p1;
+        s_inv[0] = zero ? 0.0 : p0 / den;
+        s_inv[1] = zero ? 0.0 : -p1 / den;
       }
       if (lane == 0) {
-        const bool zero = !(wb.v > 0.0);
         const int p = zero ? rj : wb.r;
         s_p = p;
         s_zero = zero;
@@ -258,53 +272,114 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
     PROBE(3);
     const int p = s_p;
     const bool zero = s_zero;
-    // 4. swapped rows take their new contents; multipliers l = a(r, j) / pivot
-    double ir = 0.0, ii = 0.0;
-    if (!zero) {
-      const double pr = prow[j], pi = prow[PW + j];
-      const double den = pr * pr + pi * pi;
-      ir = pr / den;
-      ii = -pi / den;
-    }
-    for (int lr = tid; lr < cnt; lr += PT) {
-      const int gr = rbeg + lr;
-      if (gr == rj) {
-        if (p != rj) {
-          for (int c = 0; c < PW; ++c) {
-            sre[lr * SP + c] = prow[c];
-            sim[lr * SP + c] = prow[PW + c];
-          }
-        }
-      } else if (gr > rj) {
-        if (gr == p) {
-          for (int c = 0; c < PW; ++c) {
-            sre[lr * SP + c] = rrow[c];
-            sim[lr * SP + c] = rrow[PW + c];
-          }
-        }
-        if (!zero) {
-          const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
-          sre[lr * SP + j] = xr * ir - xi * ii;
-          sim[lr * SP + j] = xr * ii + xi * ir;
-        }
+    // 5. full-row swap (one warp per moved row, lanes over columns)
+    if (p != rj) {
+      if (warp == 2 && p >= rbeg && p < rend) {
+        sre[(p - rbeg) * SP + lane] = rrow[lane];
+        sim[(p - rbeg) * SP + lane] = rrow[PW + lane];
+      } else if (warp == 3 && own_rj) {
+        sre[(rj - rbeg) * SP + lane] = prow[lane];
+        sim[(rj - rbeg) * SP + lane] = prow[PW + lane];
       }
+      __syncthreads();
     }
-    __syncthreads();
     PROBE(4);
-    // 5. rank-1 update of columns j+1 .. pw-1 on rows below rj
-    const int width = a.pw - j - 1;
-    const int lr0 = max(0, rj + 1 - rbeg);
-    if (!zero && width > 0) {
-      const int nrow = cnt - lr0;
-      for (int e = tid; e < nrow * width; e += PT) {
-        const int lr = lr0 + e / width, c = j + 1 + e % width;
-        const double lrv = sre[lr * SP + j], liv = sim[lr * SP + j];
-        const double ur = prow[c], ui = prow[PW + c];
-        sre[lr * SP + c] -= lrv * ur - liv * ui;
-        sim[lr * SP + c] -= lrv * ui + liv * ur;
+    // 6. multipliers and the rank-1 update inside the current sub-block only
+    if (!zero) {
+      const double ir = s_inv[0], ii = s_inv[1];
+      for (int lr = max(0, rj + 1 - rbeg) + tid; lr < cnt; lr += PT) {
+        const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
+        const double lre = xr * ir - xi * ii, lim = xr * ii + xi * ir;
+        sre[lr * SP + j] = lre;
+        sim[lr * SP + j] = lim;
+        for (int c = j + 1; c < sb_end; ++c) {
+          const double ur = prow[c], ui = prow[PW + c];
+          sre[lr * SP + c] -= lre * ur - lim * ui;
+          sim[lr * SP + c] -= lre * ui + lim * ur;
+        }
       }
     }
     __syncthreads();
+    // 7. end of a sub-block: U rows of the sub-block for the remaining panel
+    //    columns (CTA 0, forward substitution with the unit-lower block), then
+    //    A[r, rest] -= L[r, sub] U[sub, rest] for every row below the sub-block.
+    if (j == sb_end - 1 && sb_end < a.pw) {
+      const int rest = a.pw - sb_end, nsub = sb_end - sb0;
+      if (g == 0) {
+        if (tid < rest) {
+          const int c = sb_end + tid;
+          for (int i = 1; i < nsub; ++i) {
+            double ar = sre[(sb0 + i) * SP + c], ai = sim[(sb0 + i) * SP + c];
+            for (int k = 0; k < i; ++k) {
+              const double lr_ = sre[(sb0 + i) * SP + sb0 + k], li = sim[(sb0 + i) * SP + sb0 + k];
+              const double ur = sre[(sb0 + k) * SP + c], ui = sim[(sb0 + k) * SP + c];
+              ar -= lr_ * ur - li * ui;
+              ai -= lr_ * ui + li * ur;
+            }
+            sre[(sb0 + i) * SP + c] = ar;
+            sim[(sb0 + i) * SP + c] = ai;
+          }
+        }
+        __syncthreads();
+        double* ub = ubuf + par * 2 * SB * PW;  // [2 planes][SB][PW]
+        for (int e = tid; e < nsub * PW; e += PT) {
+          const int i = e / PW, c = e % PW;
+          const double vr = sre[(sb0 + i) * SP + c], vi = sim[(sb0 + i) * SP + c];
+          if (MODE == PANEL_CLUSTER) {
+            ub[i * PW + c] = vr;
+            ub[SB * PW + i * PW + c] = vi;
+          } else {
+            __stcg(a.xu + par * 2 * SB * PW + i * PW + c, vr);
+            __stcg(a.xu + par * 2 * SB * PW + SB * PW + i * PW + c, vi);
+          }
+        }
+      }
+      if (MODE == PANEL_CLUSTER) {
+        cg::this_cluster().sync();
+      } else if (G > 1) {
+        __threadfence();
+        cg::this_grid().sync();
+      } else {
+        __syncthreads();
+      }
+      // fetch U[sub, rest] into prow/rrow-free scratch (reuse the record area of parity par^1)
+      double* uloc = ubuf + (par ^ 1) * 2 * SB * PW;
+      if (g != 0 || MODE != PANEL_CLUSTER) {
+        for (int e = tid; e < nsub * PW; e += PT) {
+          double vr, vi;
+          if (MODE == PANEL_CLUSTER) {
+            const double* src = cg::this_cluster().map_shared_rank(ubuf + par * 2 * SB * PW, 0);
+            vr = src[e];
+            vi = src[SB * PW + e];
+          } else {
+            vr = __ldcg(a.xu + par * 2 * SB * PW + e);
+            vi = __ldcg(a.xu + par * 2 * SB * PW + SB * PW + e);
+          }
+          uloc[e] = vr;
+          uloc[SB * PW + e] = vi;
+        }
+      } else {
+        for (int e = tid; e < nsub * PW; e += PT) {
+          uloc[e] = ubuf[par * 2 * SB * PW + e];
+          uloc[SB * PW + e] = ubuf[par * 2 * SB * PW + SB * PW + e];
+        }
+      }
+      __syncthreads();
+      for (int lr = max(0, a.c0 + sb_end - rbeg) + tid; lr < cnt; lr += PT) {
+        for (int c = sb_end; c < a.pw; ++c) {
+          double ar = sre[lr * SP + c], ai = sim[lr * SP + c];
+          for (int k = 0; k < nsub; ++k) {
+            const double lr_ = sre[lr * SP + sb0 + k], li = sim[lr * SP + sb0 + k];
+            const double ur = uloc[k * PW + c], ui = uloc[SB * PW + k * PW + c];
+            ar -= lr_ * ur - li * ui;
+            ai -= lr_ * ui + li * ur;
+          }
+          sre[lr * SP + c] = ar;
+          sim[lr * SP + c] = ai;
+        }
+      }
+      __syncthreads();
+    }
     PROBE(5);
   }
   if (MODE == PANEL_CLUSTER) cg::this_cluster().sync();  // remote readers done before exit
@@ -362,7 +437,7 @@ bool g_cluster_ok = false;
 bool g_probed = false;
 
 size_t panel_smem(int rpc) {
-  return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * REC + 4 * PW);
+  return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * REC + 4 * PW + 4 * SB * PW);
 }
 
 }  // namespace
@@ -375,7 +450,7 @@ void panel_profile_read(unsigned long long* out) {
 
 size_t panel_scratch_bytes() {
   const int Gmax = 4 * kSMs;
-  return sizeof(double) * (2 * (size_t)Gmax * REC + 2 * 2 * PW) + 256;
+  return sizeof(double) * (2 * (size_t)Gmax * REC + 2 * 2 * PW + 4 * SB * PW) + 256;
 }
 
 cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
@@ -387,6 +462,7 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
   const int Gmax = 4 * kSMs;
   a.xrec = d;
   a.xrowr = d + 2 * (size_t)Gmax * REC;
+  a.xu = a.xrowr + 2 * 2 * PW;
   if (!g_probed) {
     g_probed = true;
     cudaFuncSetAttribute(panel_kernel<PANEL_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);

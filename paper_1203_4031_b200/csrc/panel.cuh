@@ -16,6 +16,7 @@ struct PanelArgs {
   int* info;
   double* xrec;   // GRID mode exchange records (set by panel_launch)
   double* xrowr;  // GRID mode copy of row rj
+  double* xu;     // GRID mode U rows of a finished sub-block
   double* linv;   // [2 planes][PW][PW] inverse of the unit-lower diagonal block
   double* uinv;   // [2 planes][PW][PW] inverse of the upper diagonal block
   int* list;      // [1 + 4*PW] (dst, src) row-interchange list of this panel
