@@ -23,6 +23,7 @@ struct fb_ctx : fb::Ctx {
   int* dev_word = nullptr;   // small device scratch for status words
   int* host_word = nullptr;  // pinned mirror
   long long launches = 0;
+  fb::LuStreams lu{};        // look-ahead side stream + events of zgetrf
 };
 
 using fb::FB_ERR_ALLOC;
@@ -103,6 +104,16 @@ int fb_ctx_create(int device, void* stream, fb_ctx** out) {
     delete c;
     return FB_ERR_ALLOC;
   }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (!getenv("FB_NO_LOOKAHEAD") &&
+      cudaStreamCreateWithPriority(&c->lu.side, cudaStreamNonBlocking, hi) == cudaSuccess) {
+    cudaEventCreateWithFlags(&c->lu.ev_s, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->lu.ev_p, cudaEventDisableTiming);
+  } else {
+    c->lu.side = nullptr;
+    cudaGetLastError();
+  }
   *out = c;
   return FB_OK;
 }
@@ -111,6 +122,12 @@ int fb_ctx_destroy(fb_ctx* c) {
   if (!c) return FB_OK;
   use_device(c);
   cudaStreamSynchronize(c->stream);
+  if (c->lu.side) {
+    cudaStreamSynchronize(c->lu.side);
+    cudaEventDestroy(c->lu.ev_s);
+    cudaEventDestroy(c->lu.ev_p);
+    cudaStreamDestroy(c->lu.side);
+  }
   if (c->scratch) cudaFree(c->scratch);
   if (c->dev_word) cudaFree(c->dev_word);
   if (c->host_word) cudaFreeHost(c->host_word);
@@ -156,7 +173,7 @@ int fb_zgetrf(fb_ctx* c, int n, double* re, double* im, int64_t ld, int* piv, do
   cudaError_t e = cudaMemcpyAsync(info, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
   if (e != cudaSuccess) return set_err(c, e, "zgetrf info init");
   // kernels per outer block: 4 panels + laswps + gemms (counted approximately)
-  return set_err(c, fb::zgetrf(n, re, im, ld, piv, info, dinv, (char*)c->scratch, c->stream), "zgetrf");
+  return set_err(c, fb::zgetrf(n, re, im, ld, piv, info, dinv, (char*)c->scratch, c->stream, &c->lu), "zgetrf");
 }
 
 int fb_read_info(fb_ctx* c, const int* info, int* bad_col) {

@@ -74,7 +74,7 @@ __global__ void shift_kernel(int n, double zr, double zi, const double* __restri
 // ---------------------------------------------------------------------------
 constexpr int SW_COLS = 32;
 __global__ void __launch_bounds__(256) swap_list_kernel(double* __restrict__ re, double* __restrict__ im,
-                                                        long long ld, int n, int c0, int pw,
+                                                        long long ld, int ca, int cb, int cc, int cd,
                                                         const int* __restrict__ list) {
   __shared__ double sv[2 * PW][SW_COLS][2];
   __shared__ int sdst[2 * PW], ssrc[2 * PW];
@@ -84,12 +84,12 @@ __global__ void __launch_bounds__(256) swap_list_kernel(double* __restrict__ re,
     ssrc[i] = list[1 + 2 * PW + i];
   }
   __syncthreads();
-  const int ncols = n - pw;
+  const int n1 = cb - ca, ncols = n1 + (cd - cc);
   const int j0 = blockIdx.x * SW_COLS;
   for (int e = threadIdx.x; e < cnt * SW_COLS; e += blockDim.x) {
     int i = e / SW_COLS, jj = e % SW_COLS, j = j0 + jj;
     if (j >= ncols) continue;
-    int col = j < c0 ? j : j + pw;
+    int col = j < n1 ? ca + j : cc + (j - n1);
     long long o = (long long)ssrc[i] * ld + col;
     sv[i][jj][0] = re[o];
     sv[i][jj][1] = im[o];
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) swap_list_kernel(double* __restrict__ re,
   for (int e = threadIdx.x; e < cnt * SW_COLS; e += blockDim.x) {
     int i = e / SW_COLS, jj = e % SW_COLS, j = j0 + jj;
     if (j >= ncols) continue;
-    int col = j < c0 ? j : j + pw;
+    int col = j < n1 ? ca + j : cc + (j - n1);
     long long o = (long long)sdst[i] * ld + col;
     re[o] = sv[i][jj][0];
     im[o] = sv[i][jj][1];
@@ -192,11 +192,13 @@ cudaError_t permute_rows_launch(int n, int m, const int* perm, int gather, const
   return cudaGetLastError();
 }
 
-static cudaError_t swap_list_launch(double* re, double* im, long long ld, int n, int c0, int pw,
+// interchanges of one sub-panel on the columns [ca, cb) u [cc, cd)
+static cudaError_t swap_list_launch(double* re, double* im, long long ld, int ca, int cb, int cc, int cd,
                                     const int* list, cudaStream_t st) {
-  int ncols = n - pw;
+  const int ncols = std::max(0, cb - ca) + std::max(0, cd - cc);
   if (ncols <= 0) return cudaSuccess;
-  swap_list_kernel<<<ceil_div(ncols, SW_COLS), 256, 0, st>>>(re, im, ld, n, c0, pw, list);
+  swap_list_kernel<<<ceil_div(ncols, SW_COLS), 256, 0, st>>>(re, im, ld, ca, std::max(ca, cb), cc,
+                                                            std::max(cc, cd), list);
   count_launch();
   return cudaGetLastError();
 }
@@ -204,67 +206,113 @@ static cudaError_t swap_list_launch(double* re, double* im, long long ld, int n,
 // In-place LU of the planar n x n matrix (re, im, ld).  piv[n] (device, 0-based),
 // info (device int, pre-set by caller to INT_MAX: stays INT_MAX on success,
 // else 1 + first zero-pivot column), dinv = dinv_doubles(n) doubles.
+//
+// Look-ahead of depth one over two streams: the high-priority side stream P
+// factors outer block k+1 (four panel launches + in-block updates) while the
+// main stream S applies block k's bulk trailing update.  S finishes block k's
+// next-block columns first and records F_k; P waits F_k, factors block k+1 and
+// records E_{k+1}; S waits E_{k+1} before touching block k+1's results.  Row
+// interchanges of block k outside the block (left L columns and the trailing
+// matrix) are applied on S after its previous update, so P and S never write
+// the same columns concurrently.
 cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* info, double* dinv,
-                   char* scratch, cudaStream_t st) {
+                   char* scratch, cudaStream_t st, const LuStreams* ls) {
   cudaError_t e;
   auto L = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW; };
   auto U = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW + 2 * PW * PW; };
   int* lists = factor_lists(dinv, n);
-  for (int k = 0; k < n; k += NB) {
+  const bool la = ls && ls->side && n > 2 * NB;
+  cudaStream_t P = la ? ls->side : st;
+  auto rec_wait = [&](cudaEvent_t ev, cudaStream_t from, cudaStream_t to) -> cudaError_t {
+    if (from == to) return cudaSuccess;
+    cudaError_t r = cudaEventRecord(ev, from);
+    if (r) return r;
+    return cudaStreamWaitEvent(to, ev, 0);
+  };
+  // factor outer block k on stream q (panels, in-block interchanges and updates)
+  auto block_factor = [&](int k, cudaStream_t q) -> cudaError_t {
     const int nb = std::min(NB, n - k);
+    cudaError_t r;
     for (int s = 0; s < nb; s += PW) {
       const int c0 = k + s, pw = std::min(PW, nb - s), blk = c0 / PW;
       int* list = lists + (size_t)blk * LIST;
       PanelArgs pa{};
       pa.re = re; pa.im = im; pa.ld = ld; pa.n = n; pa.c0 = c0; pa.pw = pw;
       pa.piv = piv; pa.info = info; pa.linv = L(blk); pa.uinv = U(blk); pa.list = list;
-      e = panel_launch(pa, scratch, st);
-      if (e != cudaSuccess) return e;
-      if ((e = swap_list_launch(re, im, ld, n, c0, pw, list, st))) return e;
+      if ((r = panel_launch(pa, scratch, q))) return r;
+      if ((r = swap_list_launch(re, im, ld, k, c0, c0 + pw, k + nb, list, q))) return r;
       const int rest = k + nb - (c0 + pw);
       if (rest > 0) {
         double* br = re + (long long)c0 * ld + c0 + pw;
         double* bi = im + (long long)c0 * ld + c0 + pw;
-        // U row block: A[c0:c0+pw, c0+pw:k+nb] = Linv * A[...]  (in place, M=K=pw <= 64)
-        e = gemm(1, pw, rest, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(br, bi, ld), br, bi, ld,
-                 1.0, 0.0, 0.0, 0.0, st);
-        if (e) return e;
+        r = gemm(1, pw, rest, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(br, bi, ld), br, bi, ld,
+                 1.0, 0.0, 0.0, 0.0, q);
+        if (r) return r;
         const int below = n - (c0 + pw);
         if (below > 0) {
-          e = gemm(1, below, rest, pw,
+          r = gemm(1, below, rest, pw,
                    op_n(re + (long long)(c0 + pw) * ld + c0, im + (long long)(c0 + pw) * ld + c0, ld),
                    op_n(br, bi, ld), re + (long long)(c0 + pw) * ld + c0 + pw,
-                   im + (long long)(c0 + pw) * ld + c0 + pw, ld, -1.0, 0.0, 1.0, 0.0, st);
-          if (e) return e;
+                   im + (long long)(c0 + pw) * ld + c0 + pw, ld, -1.0, 0.0, 1.0, 0.0, q);
+          if (r) return r;
         }
       }
     }
-    const int right = n - (k + nb);
-    if (right <= 0) continue;
-    // U12 = L11^{-1} A12, by 32-row steps with the diagonal inverses
+    return cudaSuccess;
+  };
+  // U12 = L11^{-1} A12 and A22 -= L21 U12 for the columns [c_lo, c_hi) of block k
+  auto block_update = [&](int k, int c_lo, int c_hi, cudaStream_t q) -> cudaError_t {
+    const int nb = std::min(NB, n - k);
+    const int w = c_hi - c_lo;
+    if (w <= 0) return cudaSuccess;
+    cudaError_t r;
     for (int s = 0; s < nb; s += PW) {
       const int r0 = k + s, pw = std::min(PW, nb - s), blk = r0 / PW;
-      double* xr = re + (long long)r0 * ld + k + nb;
-      double* xi = im + (long long)r0 * ld + k + nb;
-      e = gemm(1, pw, right, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(xr, xi, ld), xr, xi, ld,
-               1.0, 0.0, 0.0, 0.0, st);
-      if (e) return e;
+      double* xr = re + (long long)r0 * ld + c_lo;
+      double* xi = im + (long long)r0 * ld + c_lo;
+      r = gemm(1, pw, w, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(xr, xi, ld), xr, xi, ld,
+               1.0, 0.0, 0.0, 0.0, q);
+      if (r) return r;
       const int rem = nb - s - pw;
       if (rem > 0) {
-        e = gemm(1, rem, right, pw,
+        r = gemm(1, rem, w, pw,
                  op_n(re + (long long)(r0 + pw) * ld + r0, im + (long long)(r0 + pw) * ld + r0, ld),
-                 op_n(xr, xi, ld), re + (long long)(r0 + pw) * ld + k + nb,
-                 im + (long long)(r0 + pw) * ld + k + nb, ld, -1.0, 0.0, 1.0, 0.0, st);
-        if (e) return e;
+                 op_n(xr, xi, ld), re + (long long)(r0 + pw) * ld + c_lo,
+                 im + (long long)(r0 + pw) * ld + c_lo, ld, -1.0, 0.0, 1.0, 0.0, q);
+        if (r) return r;
       }
     }
-    // trailing update A22 -= L21 U12 (K = nb)
-    e = gemm(1, right, right, nb,
-             op_n(re + (long long)(k + nb) * ld + k, im + (long long)(k + nb) * ld + k, ld),
-             op_n(re + (long long)k * ld + k + nb, im + (long long)k * ld + k + nb, ld),
-             re + (long long)(k + nb) * ld + k + nb, im + (long long)(k + nb) * ld + k + nb, ld, -1.0,
-             0.0, 1.0, 0.0, st);
-    if (e) return e;
+    const int below = n - (k + nb);
+    return gemm(1, below, w, nb,
+                op_n(re + (long long)(k + nb) * ld + k, im + (long long)(k + nb) * ld + k, ld),
+                op_n(re + (long long)k * ld + c_lo, im + (long long)k * ld + c_lo, ld),
+                re + (long long)(k + nb) * ld + c_lo, im + (long long)(k + nb) * ld + c_lo, ld, -1.0, 0.0,
+                1.0, 0.0, q);
+  };
+
+  if (la && (e = rec_wait(ls->ev_s, st, P))) return e;  // P sees the shifted matrix
+  if ((e = block_factor(0, P))) return e;
+  for (int k = 0; k < n; k += NB) {
+    const int nb = std::min(NB, n - k);
+    if (la && (e = rec_wait(ls->ev_p, P, st))) return e;  // E_k: block k factored
+    // block k's interchanges outside the block (left L columns, trailing matrix)
+    for (int s = 0; s < nb; s += PW) {
+      const int c0 = k + s, pw = std::min(PW, nb - s);
+      (void)pw;
+      const int* list = lists + (size_t)(c0 / PW) * LIST;
+      if ((e = swap_list_launch(re, im, ld, 0, k, k + nb, n, list, st))) return e;
+    }
+    if (k + nb >= n) break;
+    const int next_hi = std::min(n, k + 2 * NB);
+    if ((e = block_update(k, k + nb, next_hi, st))) return e;  // next block's columns first
+    if (la) {
+      if ((e = rec_wait(ls->ev_s, st, P))) return e;  // F_k
+      if ((e = block_factor(k + nb, P))) return e;
+      if ((e = block_update(k, next_hi, n, st))) return e;  // bulk, overlapped with the panel
+    } else {
+      if ((e = block_update(k, next_hi, n, st))) return e;
+      if ((e = block_factor(k + nb, st))) return e;
+    }
   }
   // composed permutation for the solves
   size_t psmem = sizeof(int) * (size_t)n;

@@ -36,6 +36,7 @@ constexpr int NW = PT / 32;
 constexpr int SP = PW + 1;       // row pitch of the panel in smem (conflict-free per-row access)
 constexpr int REC = 2 + 2 * PW;  // exchange record: |pivot|, row, row data (re, im)
 constexpr int SB = 8;            // sub-block width: per-column updates stay inside it
+constexpr int MAXG = 16;         // max cluster size (mailbox slots)
 
 struct Best {
   double v;
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   double* rrow = prow + 2 * PW;           // [2*PW] old row rj
   double* lrec = rrow + 2 * PW;           // CLUSTER: [2][REC] own record
   double* lrj = lrec + 2 * REC;           // CLUSTER: [2][2*PW] own copy of row rj
+  double* mbox = lrj + 2 * 2 * PW + 4 * SB * PW;  // CLUSTER: [2][MAXG][2] pushed candidates
   __shared__ Best red[NW];
   __shared__ int s_p, s_zero;
   __shared__ int s_piv[PW];
@@ -158,7 +160,8 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
     // 1. local argmax of |a[r, j]| over own rows r >= rj
     Best b{-1.0, 0x7fffffff};
     for (int lr = max(0, rj - rbeg) + tid; lr < cnt; lr += PT)
-      b = better(b, Best{cabs_(sre[lr * SP + j], sim[lr * SP + j]), rbeg + lr});
+      b = better(b, Best{sre[lr * SP + j] * sre[lr * SP + j] + sim[lr * SP + j] * sim[lr * SP + j],
+                         rbeg + lr});
     b = warp_best(b);
     if (lane == 0) red[warp] = b;
     __syncthreads();
@@ -173,10 +176,14 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       const double vr = own_best ? sre[(t.r - rbeg) * SP + lane] : 0.0;
       const double vi = own_best ? sim[(t.r - rbeg) * SP + lane] : 0.0;
       if (MODE == PANEL_CLUSTER) {
-        if (lane < 2) rec[lane] = d0;
         if (own_best) {
           rec[2 + lane] = vr;
           rec[2 + PW + lane] = vi;
+        }
+        if (lane < G) {  // push (|pivot|^2, row) into every CTA's mailbox slot g
+          double* box = cg::this_cluster().map_shared_rank(mbox + (par * MAXG + g) * 2, lane);
+          box[0] = t.v;
+          box[1] = (double)t.r;
         }
       } else {
         if (lane < 2) __stcg(rec + lane, d0);
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
       for (int q = lane; q < G; q += 32) {
         Best t;
         if (MODE == PANEL_CLUSTER) {
-          const double* rr = cg::this_cluster().map_shared_rank(lrec + par * REC, q);
+          const double* rr = mbox + (par * MAXG + q) * 2;
           t = Best{rr[0], (int)rr[1]};
         } else {
           const double* rr = a.xrec + ((size_t)par * G + q) * REC;
@@ -437,7 +444,7 @@ bool g_cluster_ok = false;
 bool g_probed = false;
 
 size_t panel_smem(int rpc) {
-  return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * REC + 4 * PW + 4 * SB * PW);
+  return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * REC + 4 * PW + 4 * SB * PW + 4 * MAXG);
 }
 
 }  // namespace
