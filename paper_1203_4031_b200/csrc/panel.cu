@@ -102,6 +102,58 @@ __device__ void tri_inverse(const PanelArgs& a, const double* sre, const double*
   }
 }
 
+// Write the panel back, then (CTA 0) the interchange list and the diagonal-block inverses.
+__device__ void panel_finish(const PanelArgs& a, const double* sre, const double* sim, const int* s_piv,
+                             int g, int rbeg, int cnt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < cnt * a.pw; e += PT) {
+    int lr = e / a.pw, c = e % a.pw;
+    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
+    a.re[off] = sre[lr * SP + c];
+    a.im[off] = sim[lr * SP + c];
+  }
+  if (g != 0) return;
+  if (warp == 0) {
+    // (dst, src) list of the panel's interchanges (dst row <- content of src row)
+    const int t = lane;
+    const int bend = a.c0 + a.pw;
+    const int pt = t < a.pw ? s_piv[t] : -1;
+    const bool extra = t < a.pw && pt >= bend;
+    int first = t;
+    if (extra)
+      for (int q = 0; q < t; ++q)
+        if (s_piv[q] == pt) { first = q; break; }
+    const unsigned repmask = __ballot_sync(0xffffffffu, extra && first == t);
+    const int nextra = __popc(repmask);
+    const int slot = __popc(repmask & ((1u << first) - 1u));
+    __shared__ int s_pos[PW], s_row[2 * PW], s_content[2 * PW];
+    if (t < a.pw) s_pos[t] = extra ? a.pw + slot : pt - a.c0;
+    if (t < a.pw) s_row[t] = a.c0 + t;
+    if (extra && first == t) s_row[a.pw + slot] = pt;
+    __syncwarp();
+    const int total = a.pw + nextra;
+    for (int q = t; q < total; q += 32) s_content[q] = s_row[q];
+    __syncwarp();
+    if (t == 0) {
+      for (int q = 0; q < a.pw; ++q) {
+        int x = s_content[q];
+        s_content[q] = s_content[s_pos[q]];
+        s_content[s_pos[q]] = x;
+      }
+      a.list[0] = total;
+    }
+    __syncwarp();
+    for (int q = t; q < total; q += 32) {
+      a.list[1 + q] = s_row[q];
+      a.list[1 + 2 * PW + q] = s_content[q];
+    }
+  } else if (warp == 1) {
+    tri_inverse<true>(a, sre, sim, lane);
+  } else if (warp == 2) {
+    tri_inverse<false>(a, sre, sim, lane);
+  }
+}
+
 // Phase timers of CTA 0 / thread 0 (read with fb_debug_panel_profile; tools/).
 __device__ unsigned long long g_panel_prof[8];
 #define PROBE_START long long _t_last = clock64()
@@ -391,52 +443,190 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   }
   if (MODE == PANEL_CLUSTER) cg::this_cluster().sync();  // remote readers done before exit
 
-  for (int e = tid; e < cnt * a.pw; e += PT) {
-    int lr = e / a.pw, c = e % a.pw;
+  panel_finish(a, sre, sim, s_piv, g, rbeg, cnt);
+}
+
+// Cluster path: every row of the panel is owned by one thread of one CTA for
+// the whole factorization, and every CTA PUSHES its column candidate (|pivot|^2,
+// row, full panel row) and, if it owns it, the current row rj into the
+// mailboxes of all CTAs before the cluster barrier.  After the barrier each
+// thread reduces the (local) mailbox itself, so a column costs one
+// __syncthreads, one barrier.cluster and no remote reads.
+__global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = (int)cl.num_blocks(), g = (int)cl.block_rank();
+  const int rbeg = a.c0 + g * a.rpc;
+  const int rend = min(a.n, rbeg + a.rpc);
+  const int cnt = max(0, rend - rbeg);
+  double* sre = sm;                                // [rpc][SP]
+  double* sim = sre + a.rpc * SP;                  // [rpc][SP]
+  double* mrec = sim + a.rpc * SP;                 // [2][MAXG][REC] pushed candidates
+  double* mrj = mrec + 2 * MAXG * REC;             // [2][2*PW] pushed row rj
+  double* ubuf = mrj + 2 * 2 * PW;                 // [2*SB*PW] U rows of a finished sub-block
+  __shared__ Best red[NW];
+  __shared__ int s_piv[PW];
+
+  for (int e = tid; e < cnt * PW; e += PT) {
+    int lr = e / PW, c = e % PW;
     long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
-    a.re[off] = sre[lr * SP + c];
-    a.im[off] = sim[lr * SP + c];
+    bool ok = c < a.pw;
+    sre[lr * SP + c] = ok ? a.re[off] : 0.0;
+    sim[lr * SP + c] = ok ? a.im[off] : 0.0;
   }
-  if (g != 0) return;
-  if (warp == 0) {
-    // (dst, src) list of the panel's interchanges (dst row <- content of src row)
-    const int t = lane;
-    const int bend = a.c0 + a.pw;
-    const int pt = t < a.pw ? s_piv[t] : -1;
-    const bool extra = t < a.pw && pt >= bend;
-    int first = t;
-    if (extra)
-      for (int q = 0; q < t; ++q)
-        if (s_piv[q] == pt) { first = q; break; }
-    const unsigned repmask = __ballot_sync(0xffffffffu, extra && first == t);
-    const int nextra = __popc(repmask);
-    const int slot = __popc(repmask & ((1u << first) - 1u));
-    __shared__ int s_pos[PW], s_row[2 * PW], s_content[2 * PW];
-    if (t < a.pw) s_pos[t] = extra ? a.pw + slot : pt - a.c0;
-    if (t < a.pw) s_row[t] = a.c0 + t;
-    if (extra && first == t) s_row[a.pw + slot] = pt;
-    __syncwarp();
-    const int total = a.pw + nextra;
-    for (int q = t; q < total; q += 32) s_content[q] = s_row[q];
-    __syncwarp();
-    if (t == 0) {
-      for (int q = 0; q < a.pw; ++q) {
-        int x = s_content[q];
-        s_content[q] = s_content[s_pos[q]];
-        s_content[s_pos[q]] = x;
+  __syncthreads();
+
+  for (int j = 0; j < a.pw; ++j) {
+    PROBE_START;
+    const int rj = a.c0 + j;
+    const int par = j & 1;
+    const int sb0 = (j / SB) * SB, sb_end = min(a.pw, sb0 + SB);
+    const bool own_rj = rj >= rbeg && rj < rend;
+    // 1. argmax of |a(r, j)|^2 over own rows r >= rj
+    Best b{-1.0, 0x7fffffff};
+    for (int lr = max(0, rj - rbeg) + tid; lr < cnt; lr += PT) {
+      const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
+      b = better(b, Best{xr * xr + xi * xi, rbeg + lr});
+    }
+    b = warp_best(b);
+    if (lane == 0) red[warp] = b;
+    __syncthreads();
+    PROBE(0);
+    // 2. CTA candidate (every warp reduces red[]); warp w pushes to CTAs w, w+NW, ...
+    {
+      Best t = lane < NW ? red[lane] : Best{-1.0, 0x7fffffff};
+      t = warp_best(t);
+      const bool has = t.v >= 0.0;
+      const int lr = has ? t.r - rbeg : 0;
+      const double vr = has ? sre[lr * SP + lane] : 0.0, vi = has ? sim[lr * SP + lane] : 0.0;
+      const double wr = own_rj ? sre[(rj - rbeg) * SP + lane] : 0.0;
+      const double wi = own_rj ? sim[(rj - rbeg) * SP + lane] : 0.0;
+      for (int q = warp; q < G; q += NW) {
+        double* box = cl.map_shared_rank(mrec + (par * MAXG + g) * REC, q);
+        if (lane == 0) {
+          box[0] = t.v;
+          box[1] = (double)t.r;
+        }
+        box[2 + lane] = vr;
+        box[2 + PW + lane] = vi;
+        if (own_rj) {
+          double* rb = cl.map_shared_rank(mrj + par * 2 * PW, q);
+          rb[lane] = wr;
+          rb[PW + lane] = wi;
+        }
       }
-      a.list[0] = total;
     }
-    __syncwarp();
-    for (int q = t; q < total; q += 32) {
-      a.list[1 + q] = s_row[q];
-      a.list[1 + 2 * PW + q] = s_content[q];
+    PROBE(1);
+    cl.sync();
+    PROBE(2);
+    // 3. winner from the local mailbox (every warp, redundantly)
+    const double* rec = mrec + par * MAXG * REC;
+    Best w = lane < G ? Best{rec[lane * REC], (int)rec[lane * REC + 1]} : Best{-1.0, 0x7fffffff};
+    const Best wb = warp_best(w);
+    const unsigned m = __ballot_sync(0xffffffffu, lane < G && w.r == wb.r && w.v == wb.v);
+    const int gw = m ? __ffs(m) - 1 : 0;
+    const bool zero = !(wb.v > 0.0);
+    const int p = zero ? rj : wb.r;
+    const double* prow = rec + gw * REC + 2;     // pivot row (re[PW], im[PW])
+    const double* rrow = mrj + par * 2 * PW;      // old row rj
+    if (tid == 0) {
+      s_piv[j] = p;
+      if (g == 0) {
+        a.piv[rj] = p;
+        if (zero) atomicMin(a.info, rj + 1);
+      }
     }
-  } else if (warp == 1) {
-    tri_inverse<true>(a, sre, sim, lane);
-  } else if (warp == 2) {
-    tri_inverse<false>(a, sre, sim, lane);
+    double ir = 0.0, ii = 0.0;
+    if (!zero) {
+      const double pr = prow[j], pi = prow[PW + j];
+      const double den = pr * pr + pi * pi;
+      ir = pr / den;
+      ii = -pi / den;
+    }
+    PROBE(3);
+    // 4. own rows: swap, multiplier, rank-1 update inside the sub-block
+    for (int lr = tid; lr < cnt; lr += PT) {
+      const int gr = rbeg + lr;
+      if (gr < rj) continue;
+      if (gr == rj) {
+        if (p != rj)
+          for (int c = 0; c < PW; ++c) {
+            sre[lr * SP + c] = prow[c];
+            sim[lr * SP + c] = prow[PW + c];
+          }
+        continue;
+      }
+      if (gr == p)
+        for (int c = 0; c < PW; ++c) {
+          sre[lr * SP + c] = rrow[c];
+          sim[lr * SP + c] = rrow[PW + c];
+        }
+      if (zero) continue;
+      const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
+      const double lre = xr * ir - xi * ii, lim = xr * ii + xi * ir;
+      sre[lr * SP + j] = lre;
+      sim[lr * SP + j] = lim;
+      for (int c = j + 1; c < sb_end; ++c) {
+        const double ur = prow[c], ui = prow[PW + c];
+        sre[lr * SP + c] -= lre * ur - lim * ui;
+        sim[lr * SP + c] -= lre * ui + lim * ur;
+      }
+    }
+    PROBE(4);
+    // 5. end of a sub-block: U rows (CTA 0, forward substitution), pushed to all
+    //    CTAs; then A[r, rest] -= L[r, sub] U[sub, rest] on the rows below.
+    if (j == sb_end - 1 && sb_end < a.pw) {
+      const int rest = a.pw - sb_end, nsub = sb_end - sb0;
+      __syncthreads();
+      if (g == 0) {
+        if (tid < rest) {
+          const int c = sb_end + tid;
+          for (int i = 1; i < nsub; ++i) {
+            double ar = sre[(sb0 + i) * SP + c], ai = sim[(sb0 + i) * SP + c];
+            for (int k = 0; k < i; ++k) {
+              const double lr_ = sre[(sb0 + i) * SP + sb0 + k], li = sim[(sb0 + i) * SP + sb0 + k];
+              const double ur = sre[(sb0 + k) * SP + c], ui = sim[(sb0 + k) * SP + c];
+              ar -= lr_ * ur - li * ui;
+              ai -= lr_ * ui + li * ur;
+            }
+            sre[(sb0 + i) * SP + c] = ar;
+            sim[(sb0 + i) * SP + c] = ai;
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < G * nsub * PW; e += PT) {
+          const int q = e / (nsub * PW), f = e % (nsub * PW), i = f / PW, c = f % PW;
+          double* ub = cl.map_shared_rank(ubuf, q);
+          ub[i * PW + c] = sre[(sb0 + i) * SP + c];
+          ub[SB * PW + i * PW + c] = sim[(sb0 + i) * SP + c];
+        }
+      }
+      cl.sync();
+      for (int lr = max(0, a.c0 + sb_end - rbeg) + tid; lr < cnt; lr += PT) {
+        for (int c = sb_end; c < a.pw; ++c) {
+          double ar = sre[lr * SP + c], ai = sim[lr * SP + c];
+          for (int k = 0; k < nsub; ++k) {
+            const double lr_ = sre[lr * SP + sb0 + k], li = sim[lr * SP + sb0 + k];
+            const double ur = ubuf[k * PW + c], ui = ubuf[SB * PW + k * PW + c];
+            ar -= lr_ * ur - li * ui;
+            ai -= lr_ * ui + li * ur;
+          }
+          sre[lr * SP + c] = ar;
+          sim[lr * SP + c] = ai;
+        }
+      }
+      cl.sync();  // ubuf is rewritten by CTA 0 at the next sub-block end
+    }
+    PROBE(5);
   }
+  cl.sync();  // remote writers done before anyone exits
+  __syncthreads();
+  panel_finish(a, sre, sim, s_piv, g, rbeg, cnt);
+}
+
+size_t panel_cluster_smem(int rpc) {
+  return sizeof(double) * (2 * (size_t)rpc * SP + 2 * MAXG * REC + 4 * PW + 2 * SB * PW);
 }
 
 int g_grid_max_blocks = 0;
@@ -472,8 +662,8 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
   a.xu = a.xrowr + 2 * 2 * PW;
   if (!g_probed) {
     g_probed = true;
-    cudaFuncSetAttribute(panel_kernel<PANEL_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
-    cudaFuncSetAttribute(panel_kernel<PANEL_CLUSTER>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
+    cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -483,11 +673,11 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(max_cluster);
     cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = panel_smem(rpc_cluster);
+    cfg.dynamicSmemBytes = panel_cluster_smem(rpc_cluster);
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int clusters = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, panel_kernel<PANEL_CLUSTER>, &cfg);
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, panel_cluster_kernel, &cfg);
     g_cluster_ok = (e == cudaSuccess && clusters >= 1);
     cudaGetLastError();
     int nb = 0;
@@ -515,11 +705,11 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = panel_cluster_smem(rpc);
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, panel_kernel<PANEL_CLUSTER>, a);
+    return cudaLaunchKernelEx(&cfg, panel_cluster_kernel, a);
   }
   int G = ceil_div(rows, 128);
   G = std::max(1, std::min(G, rows / PW));
