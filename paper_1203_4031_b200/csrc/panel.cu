@@ -485,7 +485,8 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
     const bool own_rj = rj >= rbeg && rj < rend;
     // 1. argmax of |a(r, j)|^2 over own rows r >= rj
     Best b{-1.0, 0x7fffffff};
-    for (int lr = max(0, rj - rbeg) + tid; lr < cnt; lr += PT) {
+    for (int lr = tid; lr < cnt; lr += PT) {  // own rows only (no barrier since step 4)
+      if (rbeg + lr < rj) continue;
       const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
       b = better(b, Best{xr * xr + xi * xi, rbeg + lr});
     }
