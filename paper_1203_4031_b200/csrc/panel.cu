@@ -21,6 +21,9 @@
 // diagonal blocks and the (dst, src) list of the panel's row interchanges.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "panel.cuh"
 
@@ -653,7 +656,7 @@ size_t panel_scratch_bytes() {
 
 cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
   const int rows = a.n - a.c0;
-  const int smem_cap = 210 * 1024;
+  const int smem_cap = 227 * 1024;
   const int rpc_cluster = 384;
   const int max_cluster = 16;
   double* d = reinterpret_cast<double*>(scratch);
@@ -680,6 +683,9 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
     int clusters = 0;
     cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, panel_cluster_kernel, &cfg);
     g_cluster_ok = (e == cudaSuccess && clusters >= 1);
+    if (getenv("FB_PANEL_DEBUG"))
+      fprintf(stderr, "[feastb200] panel cluster probe: %s, max active 16-CTA clusters = %d\n",
+              cudaGetErrorString(e), clusters);
     cudaGetLastError();
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, panel_kernel<PANEL_GRID>, PT, panel_smem(128));
