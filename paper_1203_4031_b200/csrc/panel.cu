@@ -215,8 +215,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
     // 1. local argmax of |a[r, j]| over own rows r >= rj
     Best b{-1.0, 0x7fffffff};
     for (int lr = max(0, rj - rbeg) + tid; lr < cnt; lr += PT)
-      b = better(b, Best{sre[lr * SP + j] * sre[lr * SP + j] + sim[lr * SP + j] * sim[lr * SP + j],
-                         rbeg + lr});
+      b = better(b, Best{cabs_(sre[lr * SP + j], sim[lr * SP + j]), rbeg + lr});
     b = warp_best(b);
     if (lane == 0) red[warp] = b;
     __syncthreads();
@@ -490,8 +489,7 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
     Best b{-1.0, 0x7fffffff};
     for (int lr = tid; lr < cnt; lr += PT) {  // own rows only (no barrier since step 4)
       if (rbeg + lr < rj) continue;
-      const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
-      b = better(b, Best{xr * xr + xi * xi, rbeg + lr});
+      b = better(b, Best{cabs_(sre[lr * SP + j], sim[lr * SP + j]), rbeg + lr});
     }
     b = warp_best(b);
     if (lane == 0) red[warp] = b;
@@ -656,7 +654,7 @@ size_t panel_scratch_bytes() {
 
 cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
   const int rows = a.n - a.c0;
-  const int smem_cap = 227 * 1024;
+  const int smem_cap = 226 * 1024;  // 227 KB opt-in minus the kernels' static shared memory
   const int rpc_cluster = 384;
   const int max_cluster = 16;
   double* d = reinterpret_cast<double*>(scratch);
