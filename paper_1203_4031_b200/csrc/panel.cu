@@ -49,15 +49,19 @@ __device__ __forceinline__ Best better(Best a, Best b) {
   if (b.v > a.v || (b.v == a.v && b.r < a.r)) return b;
   return a;
 }
+// Warp argmax of (v, row) with exact double comparison and smallest-row ties,
+// as three 32-bit redux.sync steps (v >= 0 for candidates, v = -1 for none).
 __device__ __forceinline__ Best warp_best(Best b) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    Best t;
-    t.v = __shfl_xor_sync(0xffffffffu, b.v, o);
-    t.r = __shfl_xor_sync(0xffffffffu, b.r, o);
-    b = better(b, t);
-  }
-  return b;
+  const unsigned long long k = b.v >= 0.0 ? (unsigned long long)__double_as_longlong(b.v) : 0ull;
+  const unsigned hi = (unsigned)(k >> 32), lo = (unsigned)k;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool top = hi == mhi && lo == mlo;
+  const unsigned mr = __reduce_min_sync(0xffffffffu, top ? (unsigned)b.r : 0x7fffffffu);
+  Best o;
+  o.r = (int)mr;
+  o.v = (mr == 0x7fffffffu) ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+  return o;
 }
 
 // Column `c` of the inverse of the unit-lower (LOWER) or upper diagonal block
@@ -547,24 +551,22 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
       ii = -pi / den;
     }
     PROBE(3);
-    // 4. own rows: swap, multiplier, rank-1 update inside the sub-block
+    // 4. own rows: swap (by the owning warp, lanes over columns), multiplier,
+    //    rank-1 update inside the sub-block
+    if (p != rj) {
+      if (own_rj && (((rj - rbeg) % PT) >> 5) == warp) {
+        sre[(rj - rbeg) * SP + lane] = prow[lane];
+        sim[(rj - rbeg) * SP + lane] = prow[PW + lane];
+      }
+      if (p >= rbeg && p < rend && (((p - rbeg) % PT) >> 5) == warp) {
+        sre[(p - rbeg) * SP + lane] = rrow[lane];
+        sim[(p - rbeg) * SP + lane] = rrow[PW + lane];
+      }
+      __syncwarp();
+    }
     for (int lr = tid; lr < cnt; lr += PT) {
       const int gr = rbeg + lr;
-      if (gr < rj) continue;
-      if (gr == rj) {
-        if (p != rj)
-          for (int c = 0; c < PW; ++c) {
-            sre[lr * SP + c] = prow[c];
-            sim[lr * SP + c] = prow[PW + c];
-          }
-        continue;
-      }
-      if (gr == p)
-        for (int c = 0; c < PW; ++c) {
-          sre[lr * SP + c] = rrow[c];
-          sim[lr * SP + c] = rrow[PW + c];
-        }
-      if (zero) continue;
+      if (gr <= rj || zero) continue;
       const double xr = sre[lr * SP + j], xi = sim[lr * SP + j];
       const double lre = xr * ir - xi * ii, lim = xr * ii + xi * ir;
       sre[lr * SP + j] = lre;
