@@ -91,9 +91,11 @@ __global__ void __launch_bounds__(256) swap_list_kernel(double* __restrict__ re,
     if (j >= ncols) continue;
     int col = j < n1 ? ca + j : cc + (j - n1);
     long long o = (long long)ssrc[i] * ld + col;
-    sv[i][jj][0] = re[o];
-    sv[i][jj][1] = im[o];
+    cp_async8(&sv[i][jj][0], re + o, true);
+    cp_async8(&sv[i][jj][1], im + o, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   for (int e = threadIdx.x; e < cnt * SW_COLS; e += blockDim.x) {
     int i = e / SW_COLS, jj = e % SW_COLS, j = j0 + jj;

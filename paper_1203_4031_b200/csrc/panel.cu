@@ -199,13 +199,16 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
   __shared__ int s_p, s_zero;
   __shared__ int s_piv[PW];
 
+  // panel rows -> shared memory, all loads in flight at once (cp.async)
   for (int e = tid; e < cnt * PW; e += PT) {
     int lr = e / PW, c = e % PW;
-    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
     bool ok = c < a.pw;
-    sre[lr * SP + c] = ok ? a.re[off] : 0.0;
-    sim[lr * SP + c] = ok ? a.im[off] : 0.0;
+    long long off = ok ? (long long)(rbeg + lr) * a.ld + a.c0 + c : 0;
+    cp_async8(&sre[lr * SP + c], a.re + off, ok);
+    cp_async8(&sim[lr * SP + c], a.im + off, ok);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
   __shared__ double s_inv[2];
@@ -474,13 +477,16 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
   __shared__ Best red[NW];
   __shared__ int s_piv[PW];
 
+  // panel rows -> shared memory, all loads in flight at once (cp.async)
   for (int e = tid; e < cnt * PW; e += PT) {
     int lr = e / PW, c = e % PW;
-    long long off = (long long)(rbeg + lr) * a.ld + a.c0 + c;
     bool ok = c < a.pw;
-    sre[lr * SP + c] = ok ? a.re[off] : 0.0;
-    sim[lr * SP + c] = ok ? a.im[off] : 0.0;
+    long long off = ok ? (long long)(rbeg + lr) * a.ld + a.c0 + c : 0;
+    cp_async8(&sre[lr * SP + c], a.re + off, ok);
+    cp_async8(&sim[lr * SP + c], a.im + off, ok);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
   for (int j = 0; j < a.pw; ++j) {
