@@ -78,3 +78,45 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ double cabs_(double re, double im) { return hypot(re, im); }
 
 }  // namespace fb
+
+namespace fb {
+// ---- DSMEM push + mbarrier transaction-count signalling (sm_90+/sm_100a) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// address of the same shared variable in cluster CTA `rank` (shared::cluster window)
+__device__ __forceinline__ unsigned mapa_u32(unsigned local, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(void* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(void* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// 16-byte remote store into a cluster peer's shared memory, completing 16 tx
+// bytes on that peer's mbarrier (both addresses in the shared::cluster window).
+__device__ __forceinline__ void st_async_v2(unsigned raddr, double x, double y, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
+}  // namespace fb

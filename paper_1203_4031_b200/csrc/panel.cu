@@ -476,6 +476,13 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
   double* ubuf = mrj + 2 * 2 * PW;                 // [2*SB*PW] U rows of a finished sub-block
   __shared__ Best red[NW];
   __shared__ int s_piv[PW];
+  __shared__ __align__(8) unsigned long long mbar[2];  // per-parity mailbox completion
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_fence_init();
+  }
+  cl.sync();  // peers may push only after our mbarriers exist
 
   // panel rows -> shared memory, all loads in flight at once (cp.async)
   for (int e = tid; e < cnt * PW; e += PT) {
@@ -505,32 +512,48 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
     if (lane == 0) red[warp] = b;
     __syncthreads();
     PROBE(0);
-    // 2. CTA candidate (every warp reduces red[]); warp w pushes to CTAs w, w+NW, ...
+    // 2. CTA candidate (every warp reduces red[]); warp w pushes it (st.async)
+    //    into the mailboxes of CTAs w, w+NW, ...; the owner of row rj pushes it too.
+    //    Each CTA expects G records + one row rj per column on mbar[par].
     {
+      if (tid == 0) mbar_arrive_expect_tx(&mbar[par], (unsigned)(G * REC * 8 + 2 * PW * 8));
       Best t = lane < NW ? red[lane] : Best{-1.0, 0x7fffffff};
       t = warp_best(t);
       const bool has = t.v >= 0.0;
       const int lr = has ? t.r - rbeg : 0;
-      const double vr = has ? sre[lr * SP + lane] : 0.0, vi = has ? sim[lr * SP + lane] : 0.0;
-      const double wr = own_rj ? sre[(rj - rbeg) * SP + lane] : 0.0;
-      const double wi = own_rj ? sim[(rj - rbeg) * SP + lane] : 0.0;
+      // pair l of the record: l = 0 -> (|pivot|, row); l = 1..16 -> re[2l-2..]; 17..32 -> im
+      const int rb = 2 * lane;  // this lane's data pair covers columns rb, rb+1 of re (lane<16) or im
+      double x0, x1;
+      if (lane < 16) {
+        x0 = has ? sre[lr * SP + rb] : 0.0;
+        x1 = has ? sre[lr * SP + rb + 1] : 0.0;
+      } else {
+        x0 = has ? sim[lr * SP + rb - PW] : 0.0;
+        x1 = has ? sim[lr * SP + rb - PW + 1] : 0.0;
+      }
+      double w0 = 0.0, w1 = 0.0;
+      if (own_rj) {
+        const int l2 = rj - rbeg;
+        if (lane < 16) {
+          w0 = sre[l2 * SP + rb];
+          w1 = sre[l2 * SP + rb + 1];
+        } else {
+          w0 = sim[l2 * SP + rb - PW];
+          w1 = sim[l2 * SP + rb - PW + 1];
+        }
+      }
+      const unsigned rec_l = smem_u32(mrec + (par * MAXG + g) * REC);
+      const unsigned rj_l = smem_u32(mrj + par * 2 * PW);
+      const unsigned bar_l = smem_u32(&mbar[par]);
       for (int q = warp; q < G; q += NW) {
-        double* box = cl.map_shared_rank(mrec + (par * MAXG + g) * REC, q);
-        if (lane == 0) {
-          box[0] = t.v;
-          box[1] = (double)t.r;
-        }
-        box[2 + lane] = vr;
-        box[2 + PW + lane] = vi;
-        if (own_rj) {
-          double* rb = cl.map_shared_rank(mrj + par * 2 * PW, q);
-          rb[lane] = wr;
-          rb[PW + lane] = wi;
-        }
+        const unsigned rrec = mapa_u32(rec_l, q), rbar = mapa_u32(bar_l, q);
+        st_async_v2(rrec + 16 + 16 * lane, x0, x1, rbar);
+        if (lane == 0) st_async_v2(rrec, t.v, (double)t.r, rbar);
+        if (own_rj) st_async_v2(mapa_u32(rj_l, q) + 16 * lane, w0, w1, rbar);
       }
     }
     PROBE(1);
-    cl.sync();
+    mbar_wait_parity(&mbar[par], (j >> 1) & 1);
     PROBE(2);
     // 3. winner from the local mailbox (every warp, redundantly)
     const double* rec = mrec + par * MAXG * REC;
