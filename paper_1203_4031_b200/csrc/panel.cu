@@ -462,6 +462,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
 // thread reduces the (local) mailbox itself, so a column costs one
 // __syncthreads, one barrier.cluster and no remote reads.
 __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
+  const long long _t_kernel0 = clock64();
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
+  if (g == 0 && tid == 0) atomicAdd(&g_panel_prof[6], (unsigned long long)(clock64() - _t_kernel0));
 
   for (int j = 0; j < a.pw; ++j) {
     PROBE_START;
@@ -655,7 +657,9 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
   }
   cl.sync();  // remote writers done before anyone exits
   __syncthreads();
+  const long long _t_fin0 = clock64();
   panel_finish(a, sre, sim, s_piv, g, rbeg, cnt);
+  if (g == 0 && tid == 0) atomicAdd(&g_panel_prof[7], (unsigned long long)(clock64() - _t_fin0));
 }
 
 size_t panel_cluster_smem(int rpc) {

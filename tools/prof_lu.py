@@ -60,3 +60,5 @@ if os.environ.get("PANEL_PROF"):
     names = ["argmax", "publish", "barrier", "winner", "swap+scale", "update"]
     cols = n
     print("panel phase cycles per column:", {k: round(buf[i] / cols) for i, k in enumerate(names)})
+    npan = (n + 31) // 32
+    print("panel prologue / epilogue cycles per panel:", round(buf[6] / npan), round(buf[7] / npan))
