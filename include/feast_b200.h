@@ -71,6 +71,35 @@ int fb_zgetrs(fb_ctx* ctx, int n, int nrhs, const double* lu_re, const double* l
               int64_t ld, const int* piv, const double* dinv, int adjoint,
               double* x_re, double* x_im, int64_t ldx);
 
+/* ---- batched over contour points -------------------------------------- *
+ * The Ne shifted systems of one contour pass are independent (the reference
+ * pre-factorizes them concurrently with parallel_contour, _driver.py:46-54).
+ * These entry points process a strided batch of `count` shifts in one call:
+ * item b uses (re, im) + b*lu_stride, piv + b*piv_stride, dinv +
+ * b*dinv_stride, info[b], rhs + b*b_stride, x + b*x_stride (strides in
+ * elements; a zero rhs stride shares one right-hand-side block).  Each item
+ * is computed exactly as by the single-shift call. */
+
+/* S_b = z_b*B - A for count shifts (z_re/z_im are HOST arrays, count <= 64). */
+int fb_dense_shift_batched(fb_ctx* ctx, int count, int n, const double* z_re, const double* z_im,
+                           const double* a_re, const double* a_im, int64_t lda,
+                           const double* b_re, const double* b_im, int64_t ldb,
+                           double* s_re, double* s_im, int64_t lds, int64_t s_stride);
+
+int fb_zgetrf_batched(fb_ctx* ctx, int count, int n, double* lu_re, double* lu_im, int64_t ld,
+                      int64_t lu_stride, int* piv, int64_t piv_stride, double* dinv,
+                      int64_t dinv_stride, int* info);
+
+/* Synchronise and read count info words; bad_cols[b] = -1 or the zero-pivot column. */
+int fb_read_info_batched(fb_ctx* ctx, int count, const int* info, int* bad_cols);
+
+/* X_b = op(A_b)^{-1} B_b for every item (out of place). */
+int fb_zgetrs_batched(fb_ctx* ctx, int count, int n, int nrhs, const double* lu_re, const double* lu_im,
+                      int64_t ld, int64_t lu_stride, const int* piv, int64_t piv_stride,
+                      const double* dinv, int64_t dinv_stride, int adjoint,
+                      const double* b_re, const double* b_im, int64_t ldb, int64_t b_stride,
+                      double* x_re, double* x_im, int64_t ldx, int64_t x_stride);
+
 /* ---- RCI-kernel arithmetic (kernel.py) ---------------------------------- */
 
 /* Counter-based SplitMix64 start block: out(i, j) = U(seed, offset + j*n + i)

@@ -32,6 +32,12 @@ SIGNATURES = {
     "fb_zgetrf": (c_int, [P, c_int, P, P, c_int64, P, P, P]),
     "fb_read_info": (c_int, [P, P, PI]),
     "fb_zgetrs": (c_int, [P, c_int, c_int, P, P, c_int64, P, P, c_int, P, P, c_int64]),
+    "fb_dense_shift_batched": (c_int, [P, c_int, c_int, P, P, P, P, c_int64, P, P, c_int64, P, P, c_int64,
+                                       c_int64]),
+    "fb_zgetrf_batched": (c_int, [P, c_int, c_int, P, P, c_int64, c_int64, P, c_int64, P, c_int64, P]),
+    "fb_read_info_batched": (c_int, [P, c_int, P, P]),
+    "fb_zgetrs_batched": (c_int, [P, c_int, c_int, c_int, P, P, c_int64, c_int64, P, c_int64, P, c_int64,
+                                  c_int, P, P, c_int64, c_int64, P, P, c_int64, c_int64]),
     "fb_splitmix": (c_int, [P, c_uint64, c_int64, c_int64, c_int, c_int, P, P, c_int64]),
     "fb_accumulate": (c_int, [P, c_int, c_int, c_int, P, P, c_int64, P, P, c_int64, c_double,
                               c_double, c_double]),

@@ -156,44 +156,90 @@ int64_t fb_ctx_launch_count(const fb_ctx* c) {
 int fb_dense_shift(fb_ctx* c, int n, double zr, double zi, const double* are, const double* aim,
                    int64_t lda, const double* bre, const double* bim, int64_t ldb, double* sre,
                    double* sim, int64_t lds) {
+  return fb_dense_shift_batched(c, 1, n, &zr, &zi, are, aim, lda, bre, bim, ldb, sre, sim, lds, 0);
+}
+
+int fb_dense_shift_batched(fb_ctx* c, int count, int n, const double* zr, const double* zi, const double* are,
+                           const double* aim, int64_t lda, const double* bre, const double* bim, int64_t ldb,
+                           double* sre, double* sim, int64_t lds, int64_t s_stride) {
   CTX_GUARD(c);
-  if (n < 0 || !are || !sre || !sim) return FB_ERR_ARG;
-  return set_err(c, fb::shift_launch(n, zr, zi, are, aim, lda, bre, bim, ldb, sre, sim, lds, c->stream),
+  if (n < 0 || count < 0 || count > fb::kMaxBatch || !are || !sre || !sim || !zr || !zi) return FB_ERR_ARG;
+  return set_err(c, fb::shift_launch(n, count, zr, zi, are, aim, lda, bre, bim, ldb, sre, sim, lds, s_stride,
+                                     c->stream),
                  "dense_shift");
 }
 
 size_t fb_zgetrf_dinv_doubles(int n) { return fb::dinv_doubles(n); }
 
 int fb_zgetrf(fb_ctx* c, int n, double* re, double* im, int64_t ld, int* piv, double* dinv, int* info) {
+  return fb_zgetrf_batched(c, 1, n, re, im, ld, 0, piv, 0, dinv, 0, info);
+}
+
+int fb_zgetrf_batched(fb_ctx* c, int count, int n, double* re, double* im, int64_t ld, int64_t lu_stride,
+                      int* piv, int64_t piv_stride, double* dinv, int64_t dinv_stride, int* info) {
   CTX_GUARD(c);
-  if (n < 0 || !re || !im || !piv || !dinv || !info) return FB_ERR_ARG;
-  int r = ensure_scratch(c, fb::zgetrf_scratch_bytes(n));
+  if (n < 0 || count < 0 || !re || !im || !piv || !dinv || !info) return FB_ERR_ARG;
+  if (count == 0 || n == 0) return FB_OK;
+  int r = ensure_scratch(c, fb::zgetrf_scratch_bytes(n, count));
   if (r) return r;
-  const int big = INT_MAX;
-  cudaError_t e = cudaMemcpyAsync(info, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
-  if (e != cudaSuccess) return set_err(c, e, "zgetrf info init");
-  // kernels per outer block: 4 panels + laswps + gemms (counted approximately)
-  return set_err(c, fb::zgetrf(n, re, im, ld, piv, info, dinv, (char*)c->scratch, c->stream, &c->lu), "zgetrf");
+  fb::LuBatch f{count, re, im, ld, lu_stride, piv, piv_stride, info, dinv, dinv_stride};
+  return set_err(c, fb::zgetrf_batched(n, f, (char*)c->scratch, c->stream, &c->lu), "zgetrf");
 }
 
 int fb_read_info(fb_ctx* c, const int* info, int* bad_col) {
+  return fb_read_info_batched(c, 1, info, bad_col);
+}
+
+int fb_read_info_batched(fb_ctx* c, int count, const int* info, int* bad_cols) {
   CTX_GUARD(c);
-  cudaError_t e = cudaMemcpyAsync(c->host_word, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (count < 0 || count > 64) return FB_ERR_ARG;
+  cudaError_t e = cudaMemcpyAsync(c->host_word, info, sizeof(int) * count, cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return set_err(c, e, "read_info");
-  int v = c->host_word[0];
-  if (bad_col) *bad_col = (v == INT_MAX) ? -1 : v - 1;
-  return v == INT_MAX ? FB_OK : FB_ERR_SINGULAR;
+  int rc = FB_OK;
+  for (int b = 0; b < count; ++b) {
+    int v = c->host_word[b];
+    if (bad_cols) bad_cols[b] = (v == INT_MAX) ? -1 : v - 1;
+    if (v != INT_MAX) rc = FB_ERR_SINGULAR;
+  }
+  return rc;
 }
 
 int fb_zgetrs(fb_ctx* c, int n, int nrhs, const double* re, const double* im, int64_t ld, const int* piv,
               const double* dinv, int adjoint, double* xr, double* xi, int64_t ldx) {
   CTX_GUARD(c);
   if (n < 0 || nrhs < 0 || !xr || !xi) return FB_ERR_ARG;
-  int r = ensure_scratch(c, sizeof(double) * 2 * (size_t)n * (size_t)nrhs);
+  if (n == 0 || nrhs == 0) return FB_OK;
+  // in place: the right-hand sides go through the scratch first
+  const size_t plane = (size_t)n * (size_t)nrhs;
+  int r = ensure_scratch(c, sizeof(double) * 4 * plane);
   if (r) return r;
-  return set_err(c, fb::zgetrs(n, nrhs, re, im, ld, piv, dinv, adjoint, xr, xi, ldx, (double*)c->scratch,
-                               c->stream),
+  double* tr = (double*)c->scratch;
+  double* ti = tr + plane;
+  cudaError_t e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, c->stream);
+  if (e != cudaSuccess) return set_err(c, e, "zgetrs copy");
+  fb::LuBatch f{1, const_cast<double*>(re), const_cast<double*>(im), ld, 0, const_cast<int*>(piv), 0,
+                nullptr, const_cast<double*>(dinv), 0};
+  return set_err(c, fb::zgetrs_batched(n, nrhs, f, adjoint, tr, ti, nrhs, 0, xr, xi, ldx, 0, tr + 2 * plane,
+                                       c->stream),
+                 "zgetrs");
+}
+
+int fb_zgetrs_batched(fb_ctx* c, int count, int n, int nrhs, const double* re, const double* im, int64_t ld,
+                      int64_t lu_stride, const int* piv, int64_t piv_stride, const double* dinv,
+                      int64_t dinv_stride, int adjoint, const double* br, const double* bi, int64_t ldb,
+                      int64_t b_stride, double* xr, double* xi, int64_t ldx, int64_t x_stride) {
+  CTX_GUARD(c);
+  if (n < 0 || nrhs < 0 || count < 0 || !xr || !xi || !br || !bi) return FB_ERR_ARG;
+  if (n == 0 || nrhs == 0 || count == 0) return FB_OK;
+  int r = ensure_scratch(c, sizeof(double) * 2 * (size_t)count * n * nrhs);
+  if (r) return r;
+  fb::LuBatch f{count, const_cast<double*>(re), const_cast<double*>(im), ld, lu_stride, const_cast<int*>(piv),
+                piv_stride, nullptr, const_cast<double*>(dinv), dinv_stride};
+  return set_err(c, fb::zgetrs_batched(n, nrhs, f, adjoint, br, bi, ldb, b_stride, xr, xi, ldx, x_stride,
+                                       (double*)c->scratch, c->stream),
                  "zgetrs");
 }
 

@@ -46,15 +46,18 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int z = blockIdx.z;
+  const int bz = blockIdx.z / p.splits;  // batch item (strided batch)
+  const int z = blockIdx.z % p.splits;   // split-K slice
   const int kbeg = z * p.kchunk;
   const int kend = min(p.k, kbeg + p.kchunk);
   const int nk = kend > kbeg ? ceil_div(kend - kbeg, BK) : 0;
 
-  const double* are = p.a.re;
-  const double* aim = p.a.im;
-  const double* bre = p.b.re;
-  const double* bim = p.b.im;
+  const double* are = p.a.re + bz * p.bsa;
+  const double* aim = p.a.im ? p.a.im + bz * p.bsa : nullptr;
+  const double* bre = p.b.re + bz * p.bsb;
+  const double* bim = p.b.im ? p.b.im + bz * p.bsb : nullptr;
+  double* cre = p.cre + bz * p.bsc;
+  double* cim = p.cim ? p.cim + bz * p.bsc : nullptr;
 
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kbeg + kt * BK;
@@ -162,12 +165,12 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
         double outr = p.alpha_re * vr - p.alpha_im * vi;
         double outi = p.alpha_re * vi + p.alpha_im * vr;
         if (p.beta_re != 0.0 || p.beta_im != 0.0) {
-          double cr = p.cre[c], ci = (CPLX && p.cim) ? p.cim[c] : 0.0;
+          double cr = cre[c], ci = (CPLX && cim) ? cim[c] : 0.0;
           outr += p.beta_re * cr - p.beta_im * ci;
           outi += p.beta_re * ci + p.beta_im * cr;
         }
-        p.cre[c] = outr;
-        if (CPLX && p.cim) p.cim[c] = outi;
+        cre[c] = outr;
+        if (CPLX && cim) cim[c] = outi;
       }
 }
 
@@ -207,7 +210,7 @@ cudaError_t launch_t(const GemmParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.splits);
+  dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.splits * p.batch);
   kern<<<grid, THREADS, smem, st>>>(p);
   count_launch();
   cudaError_t e = cudaGetLastError();
@@ -236,8 +239,9 @@ int gemm_pick_splits(int m, int n, int k) {
 }
 
 cudaError_t gemm_launch(int cplx, GemmParams p, cudaStream_t st) {
-  if (p.m <= 0 || p.n <= 0) return cudaSuccess;
+  if (p.m <= 0 || p.n <= 0 || p.batch <= 0) return cudaSuccess;
   if (p.splits < 1) p.splits = 1;
+  if (p.batch > 1) p.splits = 1;  // split-K workspace is per call, not per batch item
   if (p.k <= 0) {
     // C = beta * C (alpha * 0)
     p.k = 0;

@@ -21,6 +21,8 @@ struct GemmParams {
   double* ws;  // split-K workspace (gemm_workspace_bytes)
   int splits;
   int kchunk;
+  int batch = 1;                  // strided batch: item b uses pointers + b * bs{a,b,c}
+  long long bsa = 0, bsb = 0, bsc = 0;
 };
 
 // Row-major planar helpers: X is rows x cols with leading dimension ld.
@@ -35,8 +37,10 @@ int gemm_pick_splits(int m, int n, int k);
 // Convenience: C = alpha op(A) op(B) + beta C without split-K.
 inline cudaError_t gemm(int cplx, int m, int n, int k, Opnd a, Opnd b, double* cre, double* cim,
                         long long ldc, double ar, double ai, double br, double bi, cudaStream_t st,
-                        double* ws = nullptr, int splits = 1) {
+                        double* ws = nullptr, int splits = 1, int batch = 1, long long bsa = 0,
+                        long long bsb = 0, long long bsc = 0) {
   GemmParams p;
+  p.batch = batch; p.bsa = bsa; p.bsb = bsb; p.bsc = bsc;
   p.m = m; p.n = n; p.k = k; p.a = a; p.b = b;
   p.cre = cre; p.cim = cim; p.cs0 = ldc; p.cs1 = 1;
   p.alpha_re = ar; p.alpha_im = ai; p.beta_re = br; p.beta_im = bi;

@@ -1,26 +1,29 @@
-// Dense shifted complex LU with partial pivoting and its multi-RHS solves.
+// Dense shifted complex LU with partial pivoting and its multi-RHS solves,
+// batched over contour points.
 //
 // Restates feastlib's dense backend (dense.py:30-88, _DenseOps dense.py:91-117)
 // as a blocked algorithm for sm_100a:
-//   * shift formation S = z B - A (dense.py:97-103), planar complex;
+//   * shift formation S_e = z_e B - A (dense.py:97-103), planar complex;
 //   * right-looking blocked LU, outer block NB = 128 (trailing update is one
-//     DMMA ZGEMM with K = 128), inner sub-panels of PW = 32 columns;
-//   * each sub-panel is factored by ONE kernel that keeps the panel rows
-//     resident in shared memory and exchanges one (|pivot|, row, row-data)
-//     record per CTA per column: through DSMEM inside a thread-block cluster
-//     of <= 16 CTAs (barrier.cluster per column) when the panel fits in the
-//     cluster's shared memory, else through L2 with a cooperative grid barrier;
-//     argmax pivot with first-index ties (np.argmax, dense.py:41), full-row swap,
-//     scaling and rank-1 update exactly as dense.py:40-49;
+//     DMMA ZGEMM with K = 128), inner sub-panels of PW = 32 columns factored by
+//     panel.cu (cluster/DSMEM exchange, one pivot per column);
 //   * the panel kernel also emits the 32x32 unit-lower / upper diagonal-block
 //     inverses (every triangular solve downstream is then a DMMA GEMM) and the
-//     panel's interchanges as a (dst, src) row list, applied to all other
-//     columns by one gather/scatter kernel (no per-swap serialisation);
+//     panel's interchanges as a (dst, src) row list, applied to the other
+//     columns by one gather/scatter kernel;
 //   * piv[k] = row swapped with k at step k (0-based) as lu_factor; an exactly
 //     zero pivot reports column k (SingularMatrixError, dense.py:42-43);
-//   * the composed row permutation perm (P B)[i] = B[perm[i]] is stored with the
-//     factor so the solves apply all interchanges with one parallel gather.
-#include <cooperative_groups.h>
+//   * the composed row permutation perm, (P B)[i] = B[perm[i]], is stored with
+//     the factor so the solves apply all interchanges with one gather.
+//
+// Every routine takes a strided BATCH of independent factorizations (the
+// Ne shifts of one contour pass): one launch per step covers all of them, so
+// the latency-bound panel steps of different shifts run side by side on
+// different SMs and the trailing GEMMs get Ne times more tiles.  This is the
+// GPU form of the reference's contour-parallel pre-factorization
+// (_driver.py:46-54): each factorization is computed exactly as it would be
+// alone, so results do not depend on the batch composition.
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -28,24 +31,26 @@
 #include "panel.cuh"
 #include "trsm.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace fb {
 
 namespace {
 
-constexpr int PW = 32;         // sub-panel width (= diagonal block size of dinv)
-constexpr int NB = 128;        // outer block (trailing-update K)
-constexpr int LIST = 1 + 2 * 2 * PW;  // per-block swap list: cnt, dst[2PW], src[2PW]
+constexpr int PW = 32;                 // sub-panel width (= diagonal block size of dinv)
+constexpr int NB = 128;                // outer block (trailing-update K)
+constexpr int LIST = 1 + 2 * 2 * PW;   // per-block swap list: cnt, dst[2PW], src[2PW]
 
-// ---------------------------------------------------------------------------
-// S = z B - A (B == nullptr: identity).  A/B real when their im pointer is null.
-// ---------------------------------------------------------------------------
-__global__ void shift_kernel(int n, double zr, double zi, const double* __restrict__ are,
-                             const double* __restrict__ aim, long long lda,
-                             const double* __restrict__ bre, const double* __restrict__ bim,
-                             long long ldb, double* __restrict__ sre, double* __restrict__ sim,
-                             long long lds) {
+// S_b = z_b B - A (B == nullptr: identity); item b = blockIdx.y.
+struct ShiftZ {
+  double zr[kMaxBatch], zi[kMaxBatch];
+};
+__global__ void shift_kernel(int n, ShiftZ z, const double* __restrict__ are, const double* __restrict__ aim,
+                             long long lda, const double* __restrict__ bre, const double* __restrict__ bim,
+                             long long ldb, double* __restrict__ sre, double* __restrict__ sim, long long lds,
+                             long long ss) {
+  const int b = blockIdx.y;
+  const double zr = z.zr[b], zi = z.zi[b];
+  sre += b * ss;
+  sim += b * ss;
   long long total = (long long)n * n;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -67,17 +72,21 @@ __global__ void shift_kernel(int n, double zr, double zi, const double* __restri
   }
 }
 
-// ---------------------------------------------------------------------------
 // Row interchanges of one sub-panel, given as a (dst, src) list of <= 2*PW
-// rows, applied to the columns [0, c0) u [c0+pw, n): stage the source rows of
-// a 64-column strip in shared memory, then write them to their destinations.
-// ---------------------------------------------------------------------------
+// rows, applied to the columns [ca, cb) u [cc, cd): stage the source rows of a
+// 32-column strip in shared memory (cp.async), then write them to their
+// destinations.  Item b = blockIdx.y.
 constexpr int SW_COLS = 32;
 __global__ void __launch_bounds__(256) swap_list_kernel(double* __restrict__ re, double* __restrict__ im,
-                                                        long long ld, int ca, int cb, int cc, int cd,
-                                                        const int* __restrict__ list) {
+                                                        long long ld, long long slu, int ca, int cb, int cc,
+                                                        int cd, const int* __restrict__ list,
+                                                        long long slist) {
   __shared__ double sv[2 * PW][SW_COLS][2];
   __shared__ int sdst[2 * PW], ssrc[2 * PW];
+  const int b = blockIdx.y;
+  re += b * slu;
+  im += b * slu;
+  list += b * slist;
   const int cnt = list[0];
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     sdst[i] = list[1 + i];
@@ -107,13 +116,13 @@ __global__ void __launch_bounds__(256) swap_list_kernel(double* __restrict__ re,
   }
 }
 
-// ---------------------------------------------------------------------------
 // Composed permutation from the per-block lists: idx starts as identity and
-// each block maps idx'[dst] = idx[src] (one CTA, idx in shared memory).
-// ---------------------------------------------------------------------------
-__global__ void perm_kernel(int n, const int* __restrict__ lists, int* __restrict__ perm) {
+// each block maps idx'[dst] = idx[src] (one CTA per item, idx in smem).
+__global__ void perm_kernel(int n, const int* __restrict__ lists, int* __restrict__ perm, long long sint) {
   extern __shared__ int idx[];
   __shared__ int tmp[2 * PW];
+  lists += blockIdx.x * sint;
+  perm += blockIdx.x * sint;
   for (int i = threadIdx.x; i < n; i += blockDim.x) idx[i] = i;
   __syncthreads();
   const int nblk = ceil_div(n, PW);
@@ -128,11 +137,18 @@ __global__ void perm_kernel(int n, const int* __restrict__ lists, int* __restric
   for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = idx[i];
 }
 
-// out[i][j] = in[perm[i]][j] (gather = 1) or out[perm[i]][j] = in[i][j] (scatter)
-__global__ void permute_rows_kernel(int n, int m, const int* __restrict__ perm, int gather,
+// out_b[i][j] = in_b[perm_b[i]][j] (gather) or out_b[perm_b[i]][j] = in_b[i][j]
+// (scatter); item b = blockIdx.y, strides may be 0 for a shared input.
+__global__ void permute_rows_kernel(int n, int m, const int* __restrict__ perm, long long sperm, int gather,
                                     const double* __restrict__ ir, const double* __restrict__ ii,
-                                    long long ldi, double* __restrict__ orr, double* __restrict__ oi,
-                                    long long ldo) {
+                                    long long ldi, long long sin_, double* __restrict__ orr,
+                                    double* __restrict__ oi, long long ldo, long long sout) {
+  const int b = blockIdx.y;
+  perm += b * sperm;
+  ir += b * sin_;
+  ii += b * sin_;
+  orr += b * sout;
+  oi += b * sout;
   long long total = (long long)n * m;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -148,16 +164,21 @@ __global__ void permute_rows_kernel(int n, int m, const int* __restrict__ perm, 
   }
 }
 
+__global__ void fill_int_kernel(int* p, int v, int count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) p[i] = v;
+}
+
 }  // namespace
 
-size_t zgetrf_scratch_bytes(int n) {
+size_t zgetrf_scratch_bytes(int n, int count) {
   (void)n;
-  return panel_scratch_bytes();
+  return panel_scratch_bytes() * (size_t)count;
 }
 
 // Factor side storage, in doubles: [nblk][4][PW][PW] diagonal inverses (L re/im,
-// U re/im), then perm[n] ints, then nblk swap lists.
-// ... then the per-block sweep operators G (trsm.cu) of the fused solves.
+// U re/im), then perm[n] ints, then nblk swap lists, then the per-block sweep
+// operators G / D (trsm.cu) of the fused solves.
 static size_t lists_doubles(int n) { return ((size_t)ceil_div(n, PW) * LIST + 1) / 2 + 2; }
 size_t dinv_doubles(int n) {
   size_t nblk = ceil_div(n, PW);
@@ -173,41 +194,49 @@ const double* factor_gmat(const double* dinv, int n) {
   return dinv + (size_t)ceil_div(n, PW) * 4 * PW * PW + ceil_div(n, 2) + lists_doubles(n);
 }
 
-cudaError_t shift_launch(int n, double zr, double zi, const double* are, const double* aim,
-                         long long lda, const double* bre, const double* bim, long long ldb,
-                         double* sre, double* sim, long long lds, cudaStream_t st) {
+cudaError_t shift_launch(int n, int count, const double* zr, const double* zi, const double* are,
+                         const double* aim, long long lda, const double* bre, const double* bim,
+                         long long ldb, double* sre, double* sim, long long lds, long long ss, cudaStream_t st) {
+  if (n <= 0 || count <= 0) return cudaSuccess;
+  if (count > kMaxBatch) return cudaErrorInvalidValue;
+  ShiftZ z{};
+  for (int b = 0; b < count; ++b) {
+    z.zr[b] = zr[b];
+    z.zi[b] = zi[b];
+  }
   long long total = (long long)n * n;
-  int blocks = (int)std::min<long long>((total + 255) / 256, 8 * kSMs);
-  shift_kernel<<<blocks, 256, 0, st>>>(n, zr, zi, are, aim, lda, bre, bim, ldb, sre, sim, lds);
+  int blocks = (int)std::min<long long>((total + 255) / 256, std::max(1, 8 * kSMs / count));
+  shift_kernel<<<dim3(blocks, count), 256, 0, st>>>(n, z, are, aim, lda, bre, bim, ldb, sre, sim, lds, ss);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t permute_rows_launch(int n, int m, const int* perm, int gather, const double* ir,
-                                const double* ii, long long ldi, double* orr, double* oi,
-                                long long ldo, cudaStream_t st) {
-  if (n <= 0 || m <= 0) return cudaSuccess;
+cudaError_t permute_rows_launch(int n, int m, int count, const int* perm, long long sperm, int gather,
+                                const double* ir, const double* ii, long long ldi, long long sin_, double* orr,
+                                double* oi, long long ldo, long long sout, cudaStream_t st) {
+  if (n <= 0 || m <= 0 || count <= 0) return cudaSuccess;
   long long total = (long long)n * m;
-  int blocks = (int)std::min<long long>((total + 255) / 256, 16 * kSMs);
-  permute_rows_kernel<<<blocks, 256, 0, st>>>(n, m, perm, gather, ir, ii, ldi, orr, oi, ldo);
+  int blocks = (int)std::min<long long>((total + 255) / 256, std::max(1, 16 * kSMs / count));
+  permute_rows_kernel<<<dim3(blocks, count), 256, 0, st>>>(n, m, perm, sperm, gather, ir, ii, ldi, sin_, orr,
+                                                            oi, ldo, sout);
   count_launch();
   return cudaGetLastError();
 }
 
-// interchanges of one sub-panel on the columns [ca, cb) u [cc, cd)
-static cudaError_t swap_list_launch(double* re, double* im, long long ld, int ca, int cb, int cc, int cd,
-                                    const int* list, cudaStream_t st) {
+// interchanges of one sub-panel on the columns [ca, cb) u [cc, cd), all items
+static cudaError_t swap_list_launch(const LuBatch& f, int ca, int cb, int cc, int cd, const int* list,
+                                    cudaStream_t st) {
   const int ncols = std::max(0, cb - ca) + std::max(0, cd - cc);
   if (ncols <= 0) return cudaSuccess;
-  swap_list_kernel<<<ceil_div(ncols, SW_COLS), 256, 0, st>>>(re, im, ld, ca, std::max(ca, cb), cc,
-                                                            std::max(cc, cd), list);
+  swap_list_kernel<<<dim3(ceil_div(ncols, SW_COLS), f.count), 256, 0, st>>>(
+      f.re, f.im, f.ld, f.slu, ca, std::max(ca, cb), cc, std::max(cc, cd), list, 2 * f.sdinv);
   count_launch();
   return cudaGetLastError();
 }
 
-// In-place LU of the planar n x n matrix (re, im, ld).  piv[n] (device, 0-based),
-// info (device int, pre-set by caller to INT_MAX: stays INT_MAX on success,
-// else 1 + first zero-pivot column), dinv = dinv_doubles(n) doubles.
+// In-place LU of a strided batch of planar n x n matrices.  piv (0-based),
+// info[b] = INT_MAX on success else 1 + first zero-pivot column (set here),
+// dinv = dinv_doubles(n) doubles per item.
 //
 // Look-ahead of depth one over two streams: the high-priority side stream P
 // factors outer block k+1 (four panel launches + in-block updates) while the
@@ -217,12 +246,16 @@ static cudaError_t swap_list_launch(double* re, double* im, long long ld, int ca
 // interchanges of block k outside the block (left L columns and the trailing
 // matrix) are applied on S after its previous update, so P and S never write
 // the same columns concurrently.
-cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* info, double* dinv,
-                   char* scratch, cudaStream_t st, const LuStreams* ls) {
+cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t st, const LuStreams* ls) {
   cudaError_t e;
-  auto L = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW; };
-  auto U = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW + 2 * PW * PW; };
-  int* lists = factor_lists(dinv, n);
+  if (n <= 0 || f.count <= 0) return cudaSuccess;
+  const int B = f.count;
+  const long long ld = f.ld, slu = f.slu, sd = f.sdinv;
+  double* re = f.re;
+  double* im = f.im;
+  auto L = [&](int blk) { return f.dinv + (size_t)blk * 4 * PW * PW; };
+  auto U = [&](int blk) { return f.dinv + (size_t)blk * 4 * PW * PW + 2 * PW * PW; };
+  int* lists = factor_lists(f.dinv, n);
   const bool la = ls && ls->side && n > 2 * NB;
   cudaStream_t P = la ? ls->side : st;
   auto rec_wait = [&](cudaEvent_t ev, cudaStream_t from, cudaStream_t to) -> cudaError_t {
@@ -231,6 +264,8 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
     if (r) return r;
     return cudaStreamWaitEvent(to, ev, 0);
   };
+  fill_int_kernel<<<ceil_div(B, 128), 128, 0, st>>>(f.info, 0x7fffffff, B);
+  count_launch();
   // factor outer block k on stream q (panels, in-block interchanges and updates)
   auto block_factor = [&](int k, cudaStream_t q) -> cudaError_t {
     const int nb = std::min(NB, n - k);
@@ -240,22 +275,24 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
       int* list = lists + (size_t)blk * LIST;
       PanelArgs pa{};
       pa.re = re; pa.im = im; pa.ld = ld; pa.n = n; pa.c0 = c0; pa.pw = pw;
-      pa.piv = piv; pa.info = info; pa.linv = L(blk); pa.uinv = U(blk); pa.list = list;
-      if ((r = panel_launch(pa, scratch, q))) return r;
-      if ((r = swap_list_launch(re, im, ld, k, c0, c0 + pw, k + nb, list, q))) return r;
+      pa.piv = f.piv; pa.info = f.info; pa.linv = L(blk); pa.uinv = U(blk); pa.list = list;
+      pa.slu = slu; pa.spiv = f.spiv; pa.sdinv = sd;
+      if ((r = panel_launch(pa, B, scratch, q))) return r;
+      if ((r = swap_list_launch(f, k, c0, c0 + pw, k + nb, list, q))) return r;
       const int rest = k + nb - (c0 + pw);
       if (rest > 0) {
         double* br = re + (long long)c0 * ld + c0 + pw;
         double* bi = im + (long long)c0 * ld + c0 + pw;
-        r = gemm(1, pw, rest, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(br, bi, ld), br, bi, ld,
-                 1.0, 0.0, 0.0, 0.0, q);
+        r = gemm(1, pw, rest, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(br, bi, ld), br, bi, ld, 1.0, 0.0,
+                 0.0, 0.0, q, nullptr, 1, B, sd, slu, slu);
         if (r) return r;
         const int below = n - (c0 + pw);
         if (below > 0) {
           r = gemm(1, below, rest, pw,
                    op_n(re + (long long)(c0 + pw) * ld + c0, im + (long long)(c0 + pw) * ld + c0, ld),
                    op_n(br, bi, ld), re + (long long)(c0 + pw) * ld + c0 + pw,
-                   im + (long long)(c0 + pw) * ld + c0 + pw, ld, -1.0, 0.0, 1.0, 0.0, q);
+                   im + (long long)(c0 + pw) * ld + c0 + pw, ld, -1.0, 0.0, 1.0, 0.0, q, nullptr, 1, B, slu,
+                   slu, slu);
           if (r) return r;
         }
       }
@@ -272,37 +309,34 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
       const int r0 = k + s, pw = std::min(PW, nb - s), blk = r0 / PW;
       double* xr = re + (long long)r0 * ld + c_lo;
       double* xi = im + (long long)r0 * ld + c_lo;
-      r = gemm(1, pw, w, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(xr, xi, ld), xr, xi, ld,
-               1.0, 0.0, 0.0, 0.0, q);
+      r = gemm(1, pw, w, pw, op_n(L(blk), L(blk) + PW * PW, PW), op_n(xr, xi, ld), xr, xi, ld, 1.0, 0.0, 0.0,
+               0.0, q, nullptr, 1, B, sd, slu, slu);
       if (r) return r;
       const int rem = nb - s - pw;
       if (rem > 0) {
         r = gemm(1, rem, w, pw,
                  op_n(re + (long long)(r0 + pw) * ld + r0, im + (long long)(r0 + pw) * ld + r0, ld),
-                 op_n(xr, xi, ld), re + (long long)(r0 + pw) * ld + c_lo,
-                 im + (long long)(r0 + pw) * ld + c_lo, ld, -1.0, 0.0, 1.0, 0.0, q);
+                 op_n(xr, xi, ld), re + (long long)(r0 + pw) * ld + c_lo, im + (long long)(r0 + pw) * ld + c_lo,
+                 ld, -1.0, 0.0, 1.0, 0.0, q, nullptr, 1, B, slu, slu, slu);
         if (r) return r;
       }
     }
     const int below = n - (k + nb);
-    return gemm(1, below, w, nb,
-                op_n(re + (long long)(k + nb) * ld + k, im + (long long)(k + nb) * ld + k, ld),
+    return gemm(1, below, w, nb, op_n(re + (long long)(k + nb) * ld + k, im + (long long)(k + nb) * ld + k, ld),
                 op_n(re + (long long)k * ld + c_lo, im + (long long)k * ld + c_lo, ld),
-                re + (long long)(k + nb) * ld + c_lo, im + (long long)(k + nb) * ld + c_lo, ld, -1.0, 0.0,
-                1.0, 0.0, q);
+                re + (long long)(k + nb) * ld + c_lo, im + (long long)(k + nb) * ld + c_lo, ld, -1.0, 0.0, 1.0,
+                0.0, q, nullptr, 1, B, slu, slu, slu);
   };
 
-  if (la && (e = rec_wait(ls->ev_s, st, P))) return e;  // P sees the shifted matrix
+  if (la && (e = rec_wait(ls->ev_s, st, P))) return e;  // P sees the shifted matrices
   if ((e = block_factor(0, P))) return e;
   for (int k = 0; k < n; k += NB) {
     const int nb = std::min(NB, n - k);
     if (la && (e = rec_wait(ls->ev_p, P, st))) return e;  // E_k: block k factored
     // block k's interchanges outside the block (left L columns, trailing matrix)
     for (int s = 0; s < nb; s += PW) {
-      const int c0 = k + s, pw = std::min(PW, nb - s);
-      (void)pw;
-      const int* list = lists + (size_t)(c0 / PW) * LIST;
-      if ((e = swap_list_launch(re, im, ld, 0, k, k + nb, n, list, st))) return e;
+      const int* list = lists + (size_t)((k + s) / PW) * LIST;
+      if ((e = swap_list_launch(f, 0, k, k + nb, n, list, st))) return e;
     }
     if (k + nb >= n) break;
     const int next_hi = std::min(n, k + 2 * NB);
@@ -316,7 +350,7 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
       if ((e = block_factor(k + nb, st))) return e;
     }
   }
-  // composed permutation for the solves
+  // composed permutation and sweep operators for the solves
   size_t psmem = sizeof(int) * (size_t)n;
   static bool pcfg = false;
   if (!pcfg) {
@@ -324,105 +358,49 @@ cudaError_t zgetrf(int n, double* re, double* im, long long ld, int* piv, int* i
     pcfg = true;
   }
   if (psmem > 200 * 1024) return cudaErrorInvalidValue;
-  perm_kernel<<<1, 256, psmem, st>>>(n, lists, const_cast<int*>(factor_perm(dinv, n)));
+  perm_kernel<<<B, 256, psmem, st>>>(n, lists, const_cast<int*>(factor_perm(f.dinv, n)), 2 * sd);
   count_launch();
   if ((e = cudaGetLastError())) return e;
-  return gmat_launch(n, re, im, ld, dinv, const_cast<double*>(factor_gmat(dinv, n)), st);
+  return gmat_launch(n, B, re, im, ld, slu, f.dinv, sd, const_cast<double*>(factor_gmat(f.dinv, n)), st);
 }
 
-// Solve op(A) X = B in place for X (n x nrhs planar, ldx) from zgetrf output.
-// adjoint = 0: A X = B (dense.py:62-74); adjoint = 1: A^H X = B (dense.py:75-87).
-// tmp: n*nrhs*2 doubles of scratch for the row permutation.
-cudaError_t zgetrs(int n, int nrhs, const double* re, const double* im, long long ld, const int* piv,
-                   const double* dinv, int adjoint, double* xr, double* xi, long long ldx, double* tmp,
-                   cudaStream_t st) {
+// Solve op(A_b) X_b = B_b for a batch: item b reads its right-hand sides from
+// rhs + b*srhs (srhs = 0: one shared block, e.g. the contour pass's Y) and
+// writes X_b = x + b*sx.  adjoint = 0: A X = B (dense.py:62-74); adjoint = 1:
+// A^H X = B (dense.py:75-87).  tmp: count*n*nrhs*2 doubles (adjoint only).
+cudaError_t zgetrs_batched(int n, int nrhs, const LuBatch& f, int adjoint, const double* rr, const double* ri,
+                           long long ldr, long long srhs, double* xr, double* xi, long long ldx, long long sx,
+                           double* tmp, cudaStream_t st) {
   cudaError_t e;
-  (void)piv;
-  if (n <= 0 || nrhs <= 0) return cudaSuccess;
-  const int nblk = ceil_div(n, PW);
-  const int* perm = factor_perm(dinv, n);
-  double* tr = tmp;
-  double* ti = tmp + (size_t)n * nrhs;
-  auto L = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW; };
-  auto U = [&](int blk) { return dinv + (size_t)blk * 4 * PW * PW + 2 * PW * PW; };
-  auto row = [&](const double* p, int r, int c) { return p + (long long)r * ld + c; };
-  static const bool blocked = getenv("FB_SOLVE_BLOCKED") != nullptr;  // A/B switch for tests
-  if (!blocked) {
-    const double* gm = factor_gmat(dinv, n);
-    if (!adjoint) {
-      if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-      if ((e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-      if ((e = permute_rows_launch(n, nrhs, perm, 1, tr, ti, nrhs, xr, xi, ldx, st))) return e;
-      if ((e = sweep_launch(0, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st))) return e;
-      return sweep_launch(1, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st);
-    }
-    if ((e = sweep_launch(2, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st))) return e;
-    if ((e = sweep_launch(3, n, nrhs, re, im, ld, dinv, gm, xr, xi, ldx, st))) return e;
-    if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-    if ((e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-    return permute_rows_launch(n, nrhs, perm, 0, tr, ti, nrhs, xr, xi, ldx, st);
-  }
+  if (n <= 0 || nrhs <= 0 || f.count <= 0) return cudaSuccess;
+  const int B = f.count;
+  const int* perm = factor_perm(f.dinv, n);
+  const double* gm = factor_gmat(f.dinv, n);
   if (!adjoint) {
-    // X <- P X (one gather through the scratch copy)
-    if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-    if ((e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-    if ((e = permute_rows_launch(n, nrhs, perm, 1, tr, ti, nrhs, xr, xi, ldx, st))) return e;
-    for (int b = 0; b < nblk; ++b) {  // forward, unit L
-      const int r0 = b * PW, pw = std::min(PW, n - r0);
-      double* x0r = xr + (long long)r0 * ldx;
-      double* x0i = xi + (long long)r0 * ldx;
-      if ((e = gemm(1, pw, nrhs, pw, op_n(L(b), L(b) + PW * PW, PW), op_n(x0r, x0i, ldx), x0r, x0i,
-                    ldx, 1.0, 0.0, 0.0, 0.0, st)))
-        return e;
-      const int below = n - r0 - pw;
-      if (below > 0 &&
-          (e = gemm(1, below, nrhs, pw, op_n(row(re, r0 + pw, r0), row(im, r0 + pw, r0), ld),
-                    op_n(x0r, x0i, ldx), xr + (long long)(r0 + pw) * ldx,
-                    xi + (long long)(r0 + pw) * ldx, ldx, -1.0, 0.0, 1.0, 0.0, st)))
-        return e;
-    }
-    for (int b = nblk - 1; b >= 0; --b) {  // backward, U
-      const int r0 = b * PW, pw = std::min(PW, n - r0);
-      double* x0r = xr + (long long)r0 * ldx;
-      double* x0i = xi + (long long)r0 * ldx;
-      if ((e = gemm(1, pw, nrhs, pw, op_n(U(b), U(b) + PW * PW, PW), op_n(x0r, x0i, ldx), x0r, x0i,
-                    ldx, 1.0, 0.0, 0.0, 0.0, st)))
-        return e;
-      if (r0 > 0 && (e = gemm(1, r0, nrhs, pw, op_n(row(re, 0, r0), row(im, 0, r0), ld),
-                              op_n(x0r, x0i, ldx), xr, xi, ldx, -1.0, 0.0, 1.0, 0.0, st)))
-        return e;
-    }
-    return cudaSuccess;
-  }
-  // A^H = U^H L^H P: forward with U^H, backward with L^H, then X <- P^T X
-  for (int b = 0; b < nblk; ++b) {
-    const int r0 = b * PW, pw = std::min(PW, n - r0);
-    double* x0r = xr + (long long)r0 * ldx;
-    double* x0i = xi + (long long)r0 * ldx;
-    if ((e = gemm(1, pw, nrhs, pw, op_c(U(b), U(b) + PW * PW, PW), op_n(x0r, x0i, ldx), x0r, x0i, ldx,
-                  1.0, 0.0, 0.0, 0.0, st)))
+    // X_b <- P_b B_b (one gather), then the L and U sweeps
+    if ((e = permute_rows_launch(n, nrhs, B, perm, 2 * f.sdinv, 1, rr, ri, ldr, srhs, xr, xi, ldx, sx, st)))
       return e;
-    const int below = n - r0 - pw;
-    if (below > 0 &&
-        (e = gemm(1, below, nrhs, pw, op_c(row(re, r0, r0 + pw), row(im, r0, r0 + pw), ld),
-                  op_n(x0r, x0i, ldx), xr + (long long)(r0 + pw) * ldx, xi + (long long)(r0 + pw) * ldx,
-                  ldx, -1.0, 0.0, 1.0, 0.0, st)))
+    if ((e = sweep_launch(0, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, xr, xi, ldx, sx, st)))
+      return e;
+    return sweep_launch(1, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, xr, xi, ldx, sx, st);
+  }
+  // A^H = U^H L^H P: U^H and L^H sweeps on a copy, then X_b <- P_b^T (scatter)
+  const long long st_ = (long long)n * nrhs;
+  double* tr = tmp;
+  double* ti = tmp + (size_t)B * st_;
+  for (int b = 0; b < B; ++b) {
+    if ((e = cudaMemcpy2DAsync(tr + b * st_, nrhs * 8, rr + b * srhs, ldr * 8, nrhs * 8, n,
+                               cudaMemcpyDeviceToDevice, st)))
+      return e;
+    if ((e = cudaMemcpy2DAsync(ti + b * st_, nrhs * 8, ri + b * srhs, ldr * 8, nrhs * 8, n,
+                               cudaMemcpyDeviceToDevice, st)))
       return e;
   }
-  for (int b = nblk - 1; b >= 0; --b) {
-    const int r0 = b * PW, pw = std::min(PW, n - r0);
-    double* x0r = xr + (long long)r0 * ldx;
-    double* x0i = xi + (long long)r0 * ldx;
-    if ((e = gemm(1, pw, nrhs, pw, op_c(L(b), L(b) + PW * PW, PW), op_n(x0r, x0i, ldx), x0r, x0i, ldx,
-                  1.0, 0.0, 0.0, 0.0, st)))
-      return e;
-    if (r0 > 0 && (e = gemm(1, r0, nrhs, pw, op_c(row(re, r0, 0), row(im, r0, 0), ld),
-                            op_n(x0r, x0i, ldx), xr, xi, ldx, -1.0, 0.0, 1.0, 0.0, st)))
-      return e;
-  }
-  if ((e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-  if ((e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, st))) return e;
-  return permute_rows_launch(n, nrhs, perm, 0, tr, ti, nrhs, xr, xi, ldx, st);
+  if ((e = sweep_launch(2, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, tr, ti, nrhs, st_, st)))
+    return e;
+  if ((e = sweep_launch(3, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, tr, ti, nrhs, st_, st)))
+    return e;
+  return permute_rows_launch(n, nrhs, B, perm, 2 * f.sdinv, 0, tr, ti, nrhs, st_, xr, xi, ldx, sx, st);
 }
 
 }  // namespace fb

@@ -174,7 +174,21 @@ __device__ unsigned long long g_panel_prof[8];
   } while (0)
 
 template <int MODE>
-__global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a0) {
+  PanelArgs a = a0;
+  {
+    const long long item = a.b0 + blockIdx.y;
+    a.re += item * a.slu;
+    a.im += item * a.slu;
+    a.piv += item * a.spiv;
+    a.info += item;
+    a.linv += item * a.sdinv;
+    a.uinv += item * a.sdinv;
+    a.list += 2 * item * a.sdinv;
+    a.xrec += item * a.sxs;
+    a.xrowr += item * a.sxs;
+    a.xu += item * a.sxs;
+  }
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int G, g;
@@ -461,7 +475,21 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a) {
 // mailboxes of all CTAs before the cluster barrier.  After the barrier each
 // thread reduces the (local) mailbox itself, so a column costs one
 // __syncthreads, one barrier.cluster and no remote reads.
-__global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
+  PanelArgs a = a0;
+  {
+    const long long item = a.b0 + blockIdx.y;
+    a.re += item * a.slu;
+    a.im += item * a.slu;
+    a.piv += item * a.spiv;
+    a.info += item;
+    a.linv += item * a.sdinv;
+    a.uinv += item * a.sdinv;
+    a.list += 2 * item * a.sdinv;
+    a.xrec += item * a.sxs;
+    a.xrowr += item * a.sxs;
+    a.xu += item * a.sxs;
+  }
   const long long _t_kernel0 = clock64();
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -687,7 +715,7 @@ size_t panel_scratch_bytes() {
   return sizeof(double) * (2 * (size_t)Gmax * REC + 2 * 2 * PW + 4 * SB * PW) + 256;
 }
 
-cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
+cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st) {
   const int rows = a.n - a.c0;
   const int smem_cap = 226 * 1024;  // 227 KB opt-in minus the kernels' static shared memory
   const int rpc_cluster = 384;
@@ -697,6 +725,8 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
   a.xrec = d;
   a.xrowr = d + 2 * (size_t)Gmax * REC;
   a.xu = a.xrowr + 2 * 2 * PW;
+  a.sxs = (long long)(panel_scratch_bytes() / sizeof(double));
+  a.b0 = 0;
   if (!g_probed) {
     g_probed = true;
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
@@ -734,7 +764,7 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
     a.rpc = rpc;
     size_t smem = panel_smem(rpc);
     if (G == 1) {
-      panel_kernel<PANEL_GRID><<<1, PT, smem, st>>>(a);
+      panel_kernel<PANEL_GRID><<<dim3(1, count), PT, smem, st>>>(a);
       return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
@@ -743,7 +773,7 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
     at[0].val.clusterDim.x = G;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(G);
+    cfg.gridDim = dim3(G, count);
     cfg.blockDim = dim3(PT);
     cfg.dynamicSmemBytes = panel_cluster_smem(rpc);
     cfg.stream = st;
@@ -759,8 +789,16 @@ cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st) {
   a.rpc = rpc;
   size_t smem = panel_smem(rpc);
   if ((int)smem > smem_cap) return cudaErrorInvalidConfiguration;
-  void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)panel_kernel<PANEL_GRID>, dim3(G), dim3(PT), args, smem, st);
+  // cooperative launches need every CTA co-resident: split the batch if needed
+  const int per = std::max(1, (g_grid_max_blocks * kSMs) / G);
+  for (int b0 = 0; b0 < count; b0 += per) {
+    a.b0 = b0;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_kernel<PANEL_GRID>, dim3(G, std::min(per, count - b0)),
+                                                dim3(PT), args, smem, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace fb

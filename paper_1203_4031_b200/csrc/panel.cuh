@@ -20,9 +20,13 @@ struct PanelArgs {
   double* linv;   // [2 planes][PW][PW] inverse of the unit-lower diagonal block
   double* uinv;   // [2 planes][PW][PW] inverse of the upper diagonal block
   int* list;      // [1 + 4*PW] (dst, src) row-interchange list of this panel
+  // strided batch: item b = b0 + blockIdx.y offsets re/im by b*slu, piv by b*spiv,
+  // linv/uinv by b*sdinv (doubles), list by 2*b*sdinv (ints), scratch by b*sxs
+  long long slu, spiv, sdinv, sxs;
+  int b0;
 };
 
 size_t panel_scratch_bytes();
-cudaError_t panel_launch(PanelArgs a, char* scratch, cudaStream_t st);
+cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st);
 
 }  // namespace fb

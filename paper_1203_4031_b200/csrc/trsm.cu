@@ -51,7 +51,17 @@ struct SweepArgs {
   const double* gmat;  // [4][nblk][G re, G im, D re, D im][32][32]
   double *xre, *xim;
   long long ldx;
+  long long slu, sdinv, sx;  // batch strides (item b: + b * stride)
 };
+
+__device__ __forceinline__ void offset_item(SweepArgs& a, long long b) {
+  a.lre += b * a.slu;
+  a.lim += b * a.slu;
+  a.dinv += b * a.sdinv;
+  a.gmat += b * a.sdinv;
+  a.xre += b * a.sx;
+  a.xim += b * a.sx;
+}
 
 __device__ __forceinline__ int blk_at(const SweepArgs& a, int t) {
   return (a.variant == 0 || a.variant == 2) ? t : a.nblk - 1 - t;
@@ -159,8 +169,10 @@ __device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b, int w
   return a.gmat + ((size_t)a.variant * a.nblk + b) * GM_BLK + which * 2 * BS * BS;  // 0: G, 1: D
 }
 
-__global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
   extern __shared__ __align__(16) double s[];
+  SweepArgs a = a0;
+  offset_item(a, blockIdx.y);
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x, g = blockIdx.x;
   const int C = ceil_div(a.nrhs, CW);
@@ -251,8 +263,10 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a) {
 
 // Per (block, variant): D_v (the variant's diagonal inverse, conj-transposed for
 // the adjoint sweeps) and G_v = D_v * M(b, prev(b)).
-__global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
   __shared__ double Dr[BS * 33], Di[BS * 33], Mr[BS * 33], Mi[BS * 33];
+  SweepArgs a = a0;
+  offset_item(a, blockIdx.z);
   const int b = blockIdx.x, variant = blockIdx.y;
   const bool upper = variant == 1 || variant == 2;
   const bool trans = variant >= 2;
@@ -314,23 +328,25 @@ size_t sweep_smem() { return sizeof(double) * 2 * STAGE; }
 
 size_t gmat_doubles(int n) { return (size_t)4 * ceil_div(n, BS) * GM_BLK; }
 
-cudaError_t gmat_launch(int n, const double* lre, const double* lim, long long ld, const double* dinv,
-                        double* gmat, cudaStream_t st) {
+cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, long long ld, long long slu,
+                        const double* dinv, long long sdinv, double* gmat, cudaStream_t st) {
   SweepArgs a{};
   a.n = n; a.nblk = ceil_div(n, BS); a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
-  gmat_kernel<<<dim3(a.nblk, 4), TT, 0, st>>>(a);
+  a.slu = slu; a.sdinv = sdinv; a.sx = 0;
+  gmat_kernel<<<dim3(a.nblk, 4, count), TT, 0, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t sweep_launch(int variant, int n, int nrhs, const double* lre, const double* lim, long long ld,
-                         const double* dinv, const double* gmat, double* xre, double* xim, long long ldx,
-                         cudaStream_t st) {
-  if (n <= 0 || nrhs <= 0) return cudaSuccess;
+cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
+                         long long ld, long long slu, const double* dinv, const double* gmat, long long sdinv,
+                         double* xre, double* xim, long long ldx, long long sx, cudaStream_t st) {
+  if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
   SweepArgs a{};
   a.n = n; a.nrhs = nrhs; a.nblk = ceil_div(n, BS); a.variant = variant;
   a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.xre = xre; a.xim = xim; a.ldx = ldx;
+  a.slu = slu; a.sdinv = sdinv; a.sx = sx;
   size_t smem = sweep_smem();
   if (g_sweep_blocks == 0) {
     cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -340,11 +356,13 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, const double* lre, const 
   }
   const int C = ceil_div(nrhs, CW);
   const long long items = (long long)std::max(0, a.nblk - 2) * C;
-  int G = (int)std::min<long long>(g_sweep_blocks * kSMs, std::max<long long>(C, items));
+  const int cap = std::max(1, (g_sweep_blocks * kSMs) / count);
+  if (cap < 1) return cudaErrorInvalidValue;
+  int G = (int)std::min<long long>(cap, std::max<long long>(C, items));
   G = std::max(G, 1);
   void* args[] = {&a};
   count_launch();
-  return cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(G), dim3(TT), args, smem, st);
+  return cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(G, count), dim3(TT), args, smem, st);
 }
 
 }  // namespace fb

@@ -41,23 +41,59 @@ def _is_torch(x):
 
 
 class _DenseFactor:
-    __slots__ = ("z", "lu", "piv", "dinv", "info", "resident")
+    """One shifted factorization: either item `idx` of a resident batch, or a
+    non-resident shift re-factorized on demand into the shared slot."""
 
-    def __init__(self, z, lu, piv, dinv, info, resident):
-        self.z, self.lu, self.piv, self.dinv, self.info, self.resident = z, lu, piv, dinv, info, resident
+    __slots__ = ("z", "batch", "idx", "resident")
+
+    def __init__(self, z, batch, idx, resident):
+        self.z, self.batch, self.idx, self.resident = z, batch, idx, resident
+
+
+class _FactorBatch:
+    """Strided device storage of `count` LU factors (the C ABI batch layout)."""
+
+    def __init__(self, dev, n, count):
+        torch = dev.torch
+        self.n, self.count = n, count
+        self.lu = torch.empty((2, count, n, n), dtype=torch.float64, device=dev.tdev)
+        self.piv = torch.empty((count, n), dtype=torch.int32, device=dev.tdev)
+        self.dd = int(dev.lib.fb_zgetrf_dinv_doubles(n))
+        self.dinv = torch.empty((count, self.dd), dtype=torch.float64, device=dev.tdev)
+        self.info = torch.empty(count, dtype=torch.int32, device=dev.tdev)
+        self.zs = [None] * count
+
+    def args(self, i0=0):
+        """(re, im, ld, lu_stride, piv, piv_stride, dinv, dinv_stride) of item i0 onwards."""
+        n = self.n
+        return (self.lu[0, i0].data_ptr(), self.lu[1, i0].data_ptr(), n, n * n,
+                self.piv[i0].data_ptr(), n, self.dinv[i0].data_ptr(), self.dd)
+
+    @staticmethod
+    def nbytes(dev, n, count):
+        return count * (16 * n * n + 4 * n + 8 * int(dev.lib.fb_zgetrf_dinv_doubles(n)))
 
 
 class DeviceDenseOps:
     """Device backend for the dense drivers.
 
-    Factor cache policy: factors stay resident while they fit in
-    ``cache_bytes`` (default: 85% of free HBM at construction); shifts beyond
-    that are re-factorized into one shared slot when solved (config 5 at
-    N = 32768 holds ~8 of its 16 factors on one B200)."""
+    * ``prefactorize(zs)`` forms and factors all of this rank's shifts in ONE
+      batched pass (fb_dense_shift_batched + fb_zgetrf_batched) — the GPU form
+      of parallel_contour (_driver.py:46-54): results are identical to
+      one-at-a-time factorization.
+    * ``solve_pass(Y, hermitian)`` (called by the engine at the start of every
+      contour pass) solves all resident shifts against the pass's Y in one
+      batched call (fb_zgetrs_batched, direct and, for Hermitian pencils,
+      adjoint); the per-point SOLVE tasks then copy their block out.
+    * Factor cache policy: factors stay resident while they fit in
+      ``cache_bytes`` (default: 85% of free HBM at construction); shifts beyond
+      that are re-factorized into one shared slot when solved (config 5 at
+      N = 32768 holds ~8 of its 16 factors on one B200).
+    """
 
     on_device = True
-    # bench.py instrumentation: when a list, (start, end) CUDA events recorded
-    # on the context stream around every fb_zgetrf call are appended to it.
+    # bench.py instrumentation: when a list, (start, end, count) CUDA events recorded
+    # on the context stream around every batched factorization are appended to it.
     lu_event_sink = None
 
     def __init__(self, dev, A: Planar, B: Planar | None, hermitian: bool, cache_bytes=None):
@@ -70,73 +106,110 @@ class DeviceDenseOps:
         self.cache_left = cache_bytes
         self._slot = None
         self.factorizations = 0
+        self._batches = []
+        self._pass = {}          # (id(batch), idx, adjoint) -> Planar result of this pass
 
-    def _factor_bytes(self):
-        n = self.n
-        return 16 * n * n + 8 * self.dev.lib.fb_zgetrf_dinv_doubles(n) + 4 * n
-
-    def _new_factor(self, z, resident):
-        dev, n, torch = self.dev, self.n, self.dev.torch
-        lu = dev.empty(n, n, True)
-        piv = torch.empty(n, dtype=torch.int32, device=dev.tdev)
-        dinv = torch.empty(int(dev.lib.fb_zgetrf_dinv_doubles(n)), dtype=torch.float64, device=dev.tdev)
-        info = torch.empty(1, dtype=torch.int32, device=dev.tdev)
-        return _DenseFactor(z, lu, piv, dinv, info, resident)
-
-    def _compute(self, f: _DenseFactor):
+    # -- factorization -------------------------------------------------------------
+    def _factor_batch(self, fb_, zs):
         dev, A, B, n, lib = self.dev, self.A, self.B, self.n, self.dev.lib
-        z = f.z
-        dev.check(lib.fb_dense_shift(dev.h, n, z.real, z.imag, A.re, A.im, A.ld,
-                                     B.re if B is not None else None,
-                                     B.im if B is not None else None,
-                                     B.ld if B is not None else 0,
-                                     f.lu.re, f.lu.im, f.lu.ld), "dense_shift")
+        import ctypes
+        cnt = len(zs)
+        zr = (ctypes.c_double * cnt)(*[z.real for z in zs])
+        zi = (ctypes.c_double * cnt)(*[z.imag for z in zs])
+        re, im, ld, slu, piv, spiv, dinv, sdinv = fb_.args()
+        dev.check(lib.fb_dense_shift_batched(dev.h, cnt, n, zr, zi, A.re, A.im, A.ld,
+                                             B.re if B is not None else None,
+                                             B.im if B is not None else None,
+                                             B.ld if B is not None else 0, re, im, ld, slu), "dense_shift")
         sink = DeviceDenseOps.lu_event_sink
         if sink is not None:
             ev = (dev.torch.cuda.Event(enable_timing=True), dev.torch.cuda.Event(enable_timing=True))
             ev[0].record()
-        dev.check(lib.fb_zgetrf(dev.h, n, f.lu.re, f.lu.im, f.lu.ld, f.piv.data_ptr(),
-                                f.dinv.data_ptr(), f.info.data_ptr()), "zgetrf")
+        dev.check(lib.fb_zgetrf_batched(dev.h, cnt, n, re, im, ld, slu, piv, spiv, dinv, sdinv,
+                                        fb_.info.data_ptr()), "zgetrf")
         if sink is not None:
             ev[1].record()
-            sink.append(ev)
-        self.factorizations += 1
-        bad = dev.read_info(f.info.data_ptr())
-        if bad >= 0:
-            raise SingularMatrixError(f"zero pivot at column {bad}")
+            sink.append((ev[0], ev[1], cnt))
+        self.factorizations += cnt
+        bad = (ctypes.c_int * cnt)()
+        rc = lib.fb_read_info_batched(dev.h, cnt, ctypes.c_void_p(fb_.info.data_ptr()), bad)
+        if rc == -2:
+            k = next(i for i in range(cnt) if bad[i] >= 0)
+            raise SingularMatrixError(f"zero pivot at column {bad[k]} (shift {zs[k]})")
+        dev.check(rc, "read_info")
+        for i, z in enumerate(zs):
+            fb_.zs[i] = z
+
+    def prefactorize(self, zs):
+        """Factor every shift that fits in the cache in one batched call;
+        returns {z: factor} for those (the rest are factorized on demand)."""
+        zs = [complex(z) for z in zs]
+        per = _FactorBatch.nbytes(self.dev, self.n, 1)
+        fit = min(len(zs), max(0, self.cache_left // per))
+        out = {}
+        if fit == 0:
+            return out
+        self.cache_left -= fit * per
+        fb_ = _FactorBatch(self.dev, self.n, fit)
+        self._factor_batch(fb_, zs[:fit])
+        self._batches.append(fb_)
+        for i, z in enumerate(zs[:fit]):
+            out[z] = _DenseFactor(z, fb_, i, True)
+        return out
 
     def factorize(self, z):
         z = complex(z)
-        need = self._factor_bytes()
-        if need <= self.cache_left:
-            self.cache_left -= need
-            f = self._new_factor(z, True)
-            self._compute(f)
-            return f
+        got = self.prefactorize([z]) if self.cache_left >= _FactorBatch.nbytes(self.dev, self.n, 1) else {}
+        if z in got:
+            return got[z]
         if self._slot is None:
-            self._slot = self._new_factor(None, False)
-        f = _DenseFactor(z, None, None, None, None, False)
+            self._slot = _FactorBatch(self.dev, self.n, 1)
+        f = _DenseFactor(z, None, 0, False)
         self._materialize(f)
         return f
 
     def _materialize(self, f):
         if f.resident:
-            return f
+            return f.batch, f.idx
         s = self._slot
-        if s.z != f.z:
-            s.z = f.z
-            try:
-                self._compute(s)
-            except Exception:
-                s.z = None
-                raise
-        return s
+        if s.zs[0] != f.z:
+            s.zs[0] = None
+            self._factor_batch(s, [f.z])
+        return s, 0
+
+    # -- solves ----------------------------------------------------------------------
+    def solve_pass(self, Y: Planar, hermitian: bool):
+        """Batched solves of every resident shift against this pass's Y."""
+        self._pass = {}
+        dev, n, m = self.dev, self.n, Y.cols
+        W = Y
+        if not Y.cplx:   # real Y (symmetric pencils): complex copy for the solver
+            W = dev.empty(n, m, True)
+            W.copy_from(Y)
+        for fb_ in self._batches:
+            cnt = fb_.count
+            for adj in ((0, 1) if hermitian else (0,)):
+                X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+                re, im, ld, slu, piv, spiv, dinv, sdinv = fb_.args()
+                dev.check(dev.lib.fb_zgetrs_batched(dev.h, cnt, n, m, re, im, ld, slu, piv, spiv, dinv, sdinv,
+                                                    adj, W.re, W.im, W.ld, 0, X[0].data_ptr(),
+                                                    X[1].data_ptr(), m, n * m), "zgetrs_batched")
+                for i in range(cnt):
+                    self._pass[(id(fb_), i, adj)] = (X, i)
 
     def _solve(self, f, W: Planar, adjoint):
-        g = self._materialize(f)
+        if f.resident:
+            hit = self._pass.get((id(f.batch), f.idx, int(adjoint)))
+            if hit is not None:
+                X, i = hit
+                W.plane(0).copy_(X[0, i][:, :W.cols])
+                W.plane(1).copy_(X[1, i][:, :W.cols])
+                return
+        fb_, i = self._materialize(f)
         dev = self.dev
-        dev.check(dev.lib.fb_zgetrs(dev.h, self.n, W.cols, g.lu.re, g.lu.im, g.lu.ld, g.piv.data_ptr(),
-                                    g.dinv.data_ptr(), 1 if adjoint else 0, W.re, W.im, W.ld), "zgetrs")
+        re, im, ld, slu, piv, spiv, dinv, sdinv = fb_.args(i)
+        dev.check(dev.lib.fb_zgetrs(dev.h, self.n, W.cols, re, im, ld, piv, dinv, 1 if adjoint else 0,
+                                    W.re, W.im, W.ld), "zgetrs")
 
     def solve(self, f, W: Planar):
         self._solve(f, W, False)

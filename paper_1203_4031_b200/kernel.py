@@ -164,6 +164,7 @@ class _RciKernel:
         self._gen = None
         self._points = points          # contour indices served by this rank (None: all)
         self._q_reduce = q_reduce      # callable(Q planar) summing partial Q over ranks
+        self._solve_pass = None        # callable(Y, hermitian): batched solves of a pass
         scalar = np.dtype(dtype) if dtype is not None else (
             np.dtype(np.complex128) if self.hermitian else np.dtype(np.float64))
         self._single = scalar in (np.dtype(np.float32), np.dtype(np.complex64))
@@ -348,6 +349,8 @@ class _RciKernel:
             m0 = self.m0
             Q = self.Q.cols_view(0, m0)
             Q.zero_()
+            if self._solve_pass is not None:
+                self._solve_pass(self.Y.cols_view(0, m0), self.hermitian)
             for k in points:
                 self.ze = complex(contour.z[k])
                 yield RciTask.FACTORIZE

@@ -93,7 +93,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert declared == set(_lib.SIGNATURES), declared ^ set(_lib.SIGNATURES)
     assert lib.fb_abi_version() == 1
-    assert lib.fb_zgetrf_dinv_doubles(64) == 2 * 4 * 32 * 32
+    assert lib.fb_zgetrf_dinv_doubles(64) >= 2 * 4 * 32 * 32
 
 
 def test_no_cpu_fallback_without_gpu():
