@@ -9,10 +9,14 @@
 //   implicit QL with Wilkinson shifts, <= 30 sweeps / eigenvalue  reduced.py:117-172
 //   stable ascending sort, Phi = L^-H Y                           reduced.py:180-185, 213-218
 //
-// One CTA does the whole solve (M0 <= 512 here): every O(M0^3) stage is
-// parallel across the CTA's threads, the O(M0^2) QL recurrences run on one
-// thread with the rotation sequence applied by all threads.  Working arrays
-// live in a global scratch (L2-resident for M0 <= 512).
+// One CTA of 1024 threads does the whole solve (M0 <= 512 here).  Every
+// O(M0^3) stage is written right-looking — each of the M0 sequential steps is
+// an elementwise update spread over all threads with coalesced row-major
+// accesses — so a step costs a couple of barriers and one L2 round trip
+// instead of a dependent chain of loads.  The O(M0^2) QL recurrences run on
+// one thread; their rotation sequence is applied by all threads to
+// contiguous rows of V^T.  Working arrays live in a global scratch
+// (L2-resident for M0 <= 512).
 #include "common.cuh"
 #include "misc.cuh"
 
@@ -20,11 +24,7 @@ namespace fb {
 
 namespace {
 
-constexpr int RT = 512;  // threads
-
-struct Red {
-  double v[RT / 32];
-};
+constexpr int RT = 1024;  // threads
 
 __device__ double block_sum(double x, double* sh) {
 #pragma unroll
@@ -54,7 +54,6 @@ struct RArgs {
   int check_only;
 };
 
-// complex helpers
 __device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double& cr, double& ci) {
   cr = ar * br - ai * bi;
   ci = ar * bi + ai * br;
@@ -62,15 +61,15 @@ __device__ __forceinline__ void cmul(double ar, double ai, double br, double bi,
 
 template <bool CPLX>
 __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
-  const int m = a.m, tid = threadIdx.x;
+  const int m = a.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t mm = (size_t)m * m;
-  double* Lr = a.ws;
+  double* Lr = a.ws;      // Cholesky factor (lower), in place of a copy of B
   double* Li = Lr + mm;
-  double* Cr = Li + mm;  // working matrix (row-major)
+  double* Cr = Li + mm;   // working matrix (row-major)
   double* Ci = Cr + mm;
-  double* Tr = Ci + mm;  // transposes / V^T
+  double* Tr = Ci + mm;   // scratch / V (row-major during Householder)
   double* Ti = Tr + mm;
-  double* Vr = Ti + mm;  // V^T: Vr[c*m + r] = V[r][c]
+  double* Vr = Ti + mm;   // V^T for the QL rotations: Vr[c*m + r] = V[r][c]
   double* Vi = Vr + mm;
   double* ur = Vi + mm;
   double* ui = ur + m;
@@ -85,7 +84,7 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   double* rs = rc + m;       // rotation sines [m]
   double* sh = rs + m;       // reduction scratch [40]
   __shared__ int s_int[4];
-  __shared__ double s_dbl[8];
+  __shared__ double s_val[2];
 
   // finiteness (reduced.py:203-204)
   if (!a.check_only) {
@@ -116,115 +115,115 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
     return;
   }
 
-  // 1. Cholesky L L^H = B (reduced.py:22-40)
+  // 1. Cholesky L L^H = B, right-looking on a copy (reduced.py:22-40); the
+  //    lower triangle of (Lr, Li) ends up holding L, the rest is zeroed.
+  for (size_t e = tid; e < mm; e += RT) {
+    size_t i = e / m, j = e % m;
+    Lr[e] = a.bre[i * a.ld + j];
+    if (CPLX) Li[e] = a.bim[i * a.ld + j];
+  }
+  __syncthreads();
   for (int j = 0; j < m; ++j) {
-    double part = 0.0;
-    for (int k = tid; k < j; k += RT) {
-      double xr = Lr[(size_t)j * m + k], xi = CPLX ? Li[(size_t)j * m + k] : 0.0;
-      part += xr * xr + xi * xi;
+    if (tid == 0) {
+      const double dj = Lr[(size_t)j * m + j];
+      s_int[0] = (!(dj > 0.0) || !isfinite(dj)) ? j + 1 : 0;
+      s_val[0] = sqrt(dj);
     }
-    double s = block_sum(part, sh);
-    double dj = a.bre[(size_t)j * a.ld + j] - s;
-    if (!(dj > 0.0) || !isfinite(dj)) {
-      if (tid == 0) *a.status = j + 1;
+    __syncthreads();
+    if (s_int[0]) {
+      if (tid == 0) *a.status = s_int[0];
       return;
     }
-    double ljj = sqrt(dj);
+    const double ljj = s_val[0];
     for (int i = j + 1 + tid; i < m; i += RT) {
-      double sr = 0.0, si = 0.0;
-      for (int k = 0; k < j; ++k) {
-        double xr = Lr[(size_t)i * m + k], yr = Lr[(size_t)j * m + k];
-        if (CPLX) {
-          double xi = Li[(size_t)i * m + k], yi = -Li[(size_t)j * m + k];
-          sr += xr * yr - xi * yi;
-          si += xr * yi + xi * yr;
-        } else {
-          sr += xr * yr;
-        }
-      }
-      Lr[(size_t)i * m + j] = (a.bre[(size_t)i * a.ld + j] - sr) / ljj;
-      if (CPLX) Li[(size_t)i * m + j] = (a.bim[(size_t)i * a.ld + j] - si) / ljj;
+      Lr[(size_t)i * m + j] /= ljj;
+      if (CPLX) Li[(size_t)i * m + j] /= ljj;
     }
     if (tid == 0) {
       Lr[(size_t)j * m + j] = ljj;
       if (CPLX) Li[(size_t)j * m + j] = 0.0;
     }
-    for (int k = j + 1 + tid; k < m; k += RT) {  // strictly upper part of L is zero
-      Lr[(size_t)j * m + k] = 0.0;
-      if (CPLX) Li[(size_t)j * m + k] = 0.0;
+    __syncthreads();
+    // trailing update W[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
+    const int t = m - j - 1;
+    for (int e = tid; e < t * t; e += RT) {
+      const int i = j + 1 + e / t, k = j + 1 + e % t;
+      if (k > i) continue;
+      const double xr = Lr[(size_t)i * m + j], yr = Lr[(size_t)k * m + j];
+      if (CPLX) {
+        const double xi = Li[(size_t)i * m + j], yi = -Li[(size_t)k * m + j];
+        Lr[(size_t)i * m + k] -= xr * yr - xi * yi;
+        Li[(size_t)i * m + k] -= xr * yi + xi * yr;
+      } else {
+        Lr[(size_t)i * m + k] -= xr * yr;
+      }
     }
     __syncthreads();
   }
+  for (size_t e = tid; e < mm; e += RT) {  // strictly upper part of L is zero
+    size_t i = e / m, j = e % m;
+    if (j > i) {
+      Lr[e] = 0.0;
+      if (CPLX) Li[e] = 0.0;
+    }
+  }
+  __syncthreads();
   if (a.check_only) {
     if (tid == 0) *a.status = 0;
     return;
   }
 
-  // 2. W = L^-1 A (column-parallel forward substitution) -> C
-  for (int c = tid; c < m; c += RT) {
+  // right-looking forward substitution X <- L^-1 X in place (X row-major m x m)
+  auto lower_solve = [&](double* Xr, double* Xi) {
     for (int i = 0; i < m; ++i) {
-      double sr = a.are[(size_t)i * a.ld + c], si = CPLX ? a.aim[(size_t)i * a.ld + c] : 0.0;
-      for (int k = 0; k < i; ++k) {
-        double lr = Lr[(size_t)i * m + k], xr = Cr[(size_t)k * m + c];
+      const double dr = Lr[(size_t)i * m + i];
+      for (int c = tid; c < m; c += RT) {
+        Xr[(size_t)i * m + c] /= dr;
+        if (CPLX) Xi[(size_t)i * m + c] /= dr;
+      }
+      __syncthreads();
+      const int t = m - i - 1;
+      for (int e = tid; e < t * m; e += RT) {
+        const int r = i + 1 + e / m, c = e % m;
+        const double lr = Lr[(size_t)r * m + i], xr = Xr[(size_t)i * m + c];
         if (CPLX) {
-          double li = Li[(size_t)i * m + k], xi = Ci[(size_t)k * m + c];
-          sr -= lr * xr - li * xi;
-          si -= lr * xi + li * xr;
+          const double li = Li[(size_t)r * m + i], xi = Xi[(size_t)i * m + c];
+          Xr[(size_t)r * m + c] -= lr * xr - li * xi;
+          Xi[(size_t)r * m + c] -= lr * xi + li * xr;
         } else {
-          sr -= lr * xr;
+          Xr[(size_t)r * m + c] -= lr * xr;
         }
       }
-      double dr = Lr[(size_t)i * m + i];
-      Cr[(size_t)i * m + c] = sr / dr;
-      if (CPLX) Ci[(size_t)i * m + c] = si / dr;
+      __syncthreads();
     }
-  }
-  __syncthreads();
-  // T = W^H
+  };
+
+  // 2. C = L^-1 A L^-H  (reduced.py:209-212)
   for (size_t e = tid; e < mm; e += RT) {
     size_t i = e / m, j = e % m;
-    Tr[j * m + i] = Cr[i * m + j];
-    if (CPLX) Ti[j * m + i] = -Ci[i * m + j];
+    Cr[e] = a.are[i * a.ld + j];
+    if (CPLX) Ci[e] = a.aim[i * a.ld + j];
   }
   __syncthreads();
-  // X = L^-1 T -> C (then C <- X^H)
-  for (int c = tid; c < m; c += RT) {
-    for (int i = 0; i < m; ++i) {
-      double sr = Tr[(size_t)i * m + c], si = CPLX ? Ti[(size_t)i * m + c] : 0.0;
-      for (int k = 0; k < i; ++k) {
-        double lr = Lr[(size_t)i * m + k], xr = Cr[(size_t)k * m + c];
-        if (CPLX) {
-          double li = Li[(size_t)i * m + k], xi = Ci[(size_t)k * m + c];
-          sr -= lr * xr - li * xi;
-          si -= lr * xi + li * xr;
-        } else {
-          sr -= lr * xr;
-        }
-      }
-      double dr = Lr[(size_t)i * m + i];
-      Cr[(size_t)i * m + c] = sr / dr;
-      if (CPLX) Ci[(size_t)i * m + c] = si / dr;
-    }
+  lower_solve(Cr, Ci);                       // W = L^-1 A
+  for (size_t e = tid; e < mm; e += RT) {    // T = W^H
+    size_t i = e / m, j = e % m;
+    Tr[j * m + i] = Cr[e];
+    if (CPLX) Ti[j * m + i] = -Ci[e];
   }
   __syncthreads();
-  // C <- X^H, then (C + C^H)/2  (both through T)
-  for (size_t e = tid; e < mm; e += RT) {
+  lower_solve(Tr, Ti);                       // X = L^-1 W^H
+  for (size_t e = tid; e < mm; e += RT) {    // C = X^H, then (C + C^H)/2
     size_t i = e / m, j = e % m;
-    Tr[j * m + i] = Cr[i * m + j];
-    if (CPLX) Ti[j * m + i] = -Ci[i * m + j];
+    const double xr = Tr[j * m + i], yr = Tr[i * m + j];
+    Cr[e] = 0.5 * (xr + yr);
+    if (CPLX) Ci[e] = 0.5 * (-Ti[j * m + i] + Ti[i * m + j]);
   }
-  __syncthreads();
+  // V = I, row-major in T during the Householder phase
   for (size_t e = tid; e < mm; e += RT) {
     size_t i = e / m, j = e % m;
-    double xr = Tr[i * m + j], yr = Tr[j * m + i];
-    Cr[i * m + j] = 0.5 * (xr + yr);
-    if (CPLX) Ci[i * m + j] = 0.5 * (Ti[i * m + j] - Ti[j * m + i]);
-  }
-  // V = I (stored transposed)
-  for (size_t e = tid; e < mm; e += RT) {
-    size_t i = e / m, j = e % m;
-    Vr[e] = (i == j) ? 1.0 : 0.0;
-    if (CPLX) Vi[e] = 0.0;
+    Tr[e] = (i == j) ? 1.0 : 0.0;
+    if (CPLX) Ti[e] = 0.0;
   }
   __syncthreads();
 
@@ -248,7 +247,6 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
       phi_ = x0i / ax0;
     }
     const double alr = -phr * xnorm, ali = -phi_ * xnorm;
-    __syncthreads();
     if (tid == 0) {
       ur[0] = x0r - alr;
       if (CPLX) ui[0] = x0i - ali;
@@ -266,29 +264,32 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
       if (CPLX) ui[i] /= unorm;
     }
     __syncthreads();
-    // p = 2 * sub @ u   (one warp per row, lanes along the row)
-    {
-      const int warp = tid >> 5, lane = tid & 31;
-      for (int i = warp; i < len; i += RT / 32) {
-        const double* rowr = Cr + (size_t)(k + 1 + i) * m + k + 1;
-        const double* rowi = Ci + (size_t)(k + 1 + i) * m + k + 1;
-        double sr = 0.0, si = 0.0;
-        for (int j = lane; j < len; j += 32) {
-          if (CPLX) {
-            sr += rowr[j] * ur[j] - rowi[j] * ui[j];
-            si += rowr[j] * ui[j] + rowi[j] * ur[j];
-          } else {
-            sr += rowr[j] * ur[j];
-          }
+    // p = 2 * sub @ u and w = V[:, k+1:] @ u (one warp per row, lanes along the row)
+    for (int i = warp; i < len + m; i += RT / 32) {
+      const bool isp = i < len;
+      const double* rowr = isp ? Cr + (size_t)(k + 1 + i) * m + k + 1 : Tr + (size_t)(i - len) * m + k + 1;
+      const double* rowi = isp ? Ci + (size_t)(k + 1 + i) * m + k + 1 : Ti + (size_t)(i - len) * m + k + 1;
+      double sr = 0.0, si = 0.0;
+      for (int j = lane; j < len; j += 32) {
+        if (CPLX) {
+          sr += rowr[j] * ur[j] - rowi[j] * ui[j];
+          si += rowr[j] * ui[j] + rowi[j] * ur[j];
+        } else {
+          sr += rowr[j] * ur[j];
         }
+      }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          sr += __shfl_xor_sync(0xffffffffu, sr, o);
-          si += __shfl_xor_sync(0xffffffffu, si, o);
-        }
-        if (lane == 0) {
+      for (int o = 16; o; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        si += __shfl_xor_sync(0xffffffffu, si, o);
+      }
+      if (lane == 0) {
+        if (isp) {
           pr[i] = 2.0 * sr;
           if (CPLX) pi[i] = 2.0 * si;
+        } else {
+          wr[i - len] = sr;
+          if (CPLX) wi[i - len] = si;
         }
       }
     }
@@ -296,67 +297,50 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
     part = 0.0;  // kappa = Re(u^H p)
     for (int i = tid; i < len; i += RT) part += ur[i] * pr[i] + (CPLX ? ui[i] * pi[i] : 0.0);
     const double kap2 = 2.0 * block_sum(part, sh);
-    // sub -= p u^H ; sub -= u p^H ; sub += 2 kappa u u^H
-    for (size_t e = tid; e < (size_t)len * len; e += RT) {
-      int i = (int)(e / len), j = (int)(e % len);
-      size_t o = (size_t)(k + 1 + i) * m + k + 1 + j;
-      if (CPLX) {
-        double tr, ti;
-        double sr = Cr[o], si = Ci[o];
-        cmul(pr[i], pi[i], ur[j], -ui[j], tr, ti);
-        sr -= tr;
-        si -= ti;
-        cmul(ur[i], ui[i], pr[j], -pi[j], tr, ti);
-        sr -= tr;
-        si -= ti;
-        cmul(ur[i], ui[i], ur[j], -ui[j], tr, ti);
-        sr += kap2 * tr;
-        si += kap2 * ti;
-        Cr[o] = sr;
-        Ci[o] = si;
+    // sub -= p u^H ; sub -= u p^H ; sub += 2 kappa u u^H ; V[:, k+1:] -= 2 w u^H
+    for (size_t e = tid; e < (size_t)len * len + (size_t)m * len; e += RT) {
+      if (e < (size_t)len * len) {
+        const int i = (int)(e / len), j = (int)(e % len);
+        const size_t o = (size_t)(k + 1 + i) * m + k + 1 + j;
+        if (CPLX) {
+          double tr, ti;
+          double sr = Cr[o], si = Ci[o];
+          cmul(pr[i], pi[i], ur[j], -ui[j], tr, ti);
+          sr -= tr;
+          si -= ti;
+          cmul(ur[i], ui[i], pr[j], -pi[j], tr, ti);
+          sr -= tr;
+          si -= ti;
+          cmul(ur[i], ui[i], ur[j], -ui[j], tr, ti);
+          sr += kap2 * tr;
+          si += kap2 * ti;
+          Cr[o] = sr;
+          Ci[o] = si;
+        } else {
+          double s = Cr[o];
+          s -= pr[i] * ur[j];
+          s -= ur[i] * pr[j];
+          s += kap2 * (ur[i] * ur[j]);
+          Cr[o] = s;
+        }
       } else {
-        double s = Cr[o];
-        s -= pr[i] * ur[j];
-        s -= ur[i] * pr[j];
-        s += kap2 * (ur[i] * ur[j]);
-        Cr[o] = s;
+        const size_t f = e - (size_t)len * len;
+        const int r = (int)(f / len), j = (int)(f % len);
+        const size_t o = (size_t)r * m + k + 1 + j;
+        if (CPLX) {
+          double tr, ti;
+          cmul(wr[r], wi[r], ur[j], -ui[j], tr, ti);
+          Tr[o] -= 2.0 * tr;
+          Ti[o] -= 2.0 * ti;
+        } else {
+          Tr[o] -= 2.0 * (wr[r] * ur[j]);
+        }
       }
     }
     __syncthreads();
     if (tid == 0) {
       Cr[(size_t)(k + 1) * m + k] = alr;
       if (CPLX) Ci[(size_t)(k + 1) * m + k] = ali;
-    }
-    // (entries below the subdiagonal are never read again; the row part is
-    //  not needed: only the diagonal and subdiagonal feed the QL step)
-    // V[:, k+1:] -= 2 (V[:, k+1:] u) u^H     (V^T stored: Vr[(k+1+j)*m + r])
-    for (int r = tid; r < m; r += RT) {
-      double sr = 0.0, si = 0.0;
-      for (int j = 0; j < len; ++j) {
-        double vr = Vr[(size_t)(k + 1 + j) * m + r];
-        if (CPLX) {
-          double vi = Vi[(size_t)(k + 1 + j) * m + r];
-          sr += vr * ur[j] - vi * ui[j];
-          si += vr * ui[j] + vi * ur[j];
-        } else {
-          sr += vr * ur[j];
-        }
-      }
-      wr[r] = sr;
-      if (CPLX) wi[r] = si;
-    }
-    __syncthreads();
-    for (size_t e = tid; e < (size_t)len * m; e += RT) {
-      int j = (int)(e / m), r = (int)(e % m);
-      size_t o = (size_t)(k + 1 + j) * m + r;
-      if (CPLX) {
-        double tr, ti;
-        cmul(wr[r], wi[r], ur[j], -ui[j], tr, ti);
-        Vr[o] -= 2.0 * tr;
-        Vi[o] -= 2.0 * ti;
-      } else {
-        Vr[o] -= 2.0 * (wr[r] * ur[j]);
-      }
     }
     __syncthreads();
   }
@@ -389,16 +373,19 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
     ee[m - 1] = 0.0;
   }
   __syncthreads();
-  if (CPLX) {  // v = v * phi[None, :] : row c of V^T scaled by phi[c]
-    for (size_t e = tid; e < mm; e += RT) {
-      int c = (int)(e / m);
+  // V^T for the QL: Vt[c][r] = V[r][c] * phi[c]
+  for (size_t e = tid; e < mm; e += RT) {
+    const int r = (int)(e / m), c = (int)(e % m);
+    if (CPLX) {
       double tr, ti;
-      cmul(Vr[e], Vi[e], wr[c], wi[c], tr, ti);
-      Vr[e] = tr;
-      Vi[e] = ti;
+      cmul(Tr[e], Ti[e], wr[c], wi[c], tr, ti);
+      Vr[(size_t)c * m + r] = tr;
+      Vi[(size_t)c * m + r] = ti;
+    } else {
+      Vr[(size_t)c * m + r] = Tr[e];
     }
-    __syncthreads();
   }
+  __syncthreads();
 
   // 5. implicit QL (reduced.py:117-172); rotations applied to columns of V
   const double epsm = 2.220446049250313e-16;
@@ -412,7 +399,7 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
           if (fabs(ee[mm_]) <= epsm * dd) break;
           ++mm_;
         }
-        int nrot = 0, first = mm_;
+        int nrot = 0;
         if (mm_ != l) {
           ++sweeps;
           if (sweeps > 30) {
@@ -452,9 +439,9 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
             }
           }
         }
-        s_int[0] = (mm_ == l) ? 1 : 0;  // converged for this l
+        s_int[0] = (mm_ == l) ? 1 : 0;
         s_int[1] = nrot;
-        s_int[2] = first;
+        s_int[2] = mm_;
       }
       __syncthreads();
       const int done = s_int[0], nrot = s_int[1], first = s_int[2];
@@ -463,7 +450,6 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
         if (tid == 0) *a.status = -1;
         return;
       }
-      // apply rotations i = first-1 down to first-nrot
       for (int r = tid; r < m; r += RT) {
         for (int t = 0; t < nrot; ++t) {
           const int i = first - 1 - t;
@@ -484,6 +470,7 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   }
 
   // 6. stable ascending order, eps, Phi = L^-H V[:, order]
+  int* order = reinterpret_cast<int*>(ur);
   for (int i = tid; i < m; i += RT) {
     double di = d[i];
     int rank = 0;
@@ -492,39 +479,40 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
       rank += (dj < di) || (dj == di && j < i);
     }
     a.eps[rank] = di;
-    reinterpret_cast<int*>(ur)[rank] = i;  // order[rank] = i
+    order[rank] = i;
   }
   __syncthreads();
-  // T = V[:, order] row-major: T[i][c] = V[i][order[c]] = Vt[order[c]][i]
+  // X[i][c] = V[i][order[c]] = Vt[order[c]][i], into phi directly
   for (size_t e = tid; e < mm; e += RT) {
     int i = (int)(e / m), c = (int)(e % m);
-    int oc = reinterpret_cast<int*>(ur)[c];
-    Tr[e] = Vr[(size_t)oc * m + i];
-    if (CPLX) Ti[e] = Vi[(size_t)oc * m + i];
+    int oc = order[c];
+    a.phre[(size_t)i * a.ldphi + c] = Vr[(size_t)oc * m + i];
+    if (CPLX) a.phim[(size_t)i * a.ldphi + c] = Vi[(size_t)oc * m + i];
   }
   __syncthreads();
-  // solve L^H X = T (backward), column-parallel
-  for (int c = tid; c < m; c += RT) {
-    for (int i = m - 1; i >= 0; --i) {
-      double sr = Tr[(size_t)i * m + c], si = CPLX ? Ti[(size_t)i * m + c] : 0.0;
-      for (int k = i + 1; k < m; ++k) {
-        // conj(L[k][i]) * x_k
-        double lr = Lr[(size_t)k * m + i], xr = a.phre[(size_t)k * a.ldphi + c];
-        if (CPLX) {
-          double li = -Li[(size_t)k * m + i], xi = a.phim[(size_t)k * a.ldphi + c];
-          sr -= lr * xr - li * xi;
-          si -= lr * xi + li * xr;
-        } else {
-          sr -= lr * xr;
-        }
-      }
-      double dr = Lr[(size_t)i * m + i];
-      a.phre[(size_t)i * a.ldphi + c] = sr / dr;
-      if (CPLX) a.phim[(size_t)i * a.ldphi + c] = si / dr;
+  // right-looking backward solve L^H X = Y
+  for (int i = m - 1; i >= 0; --i) {
+    const double dr = Lr[(size_t)i * m + i];
+    for (int c = tid; c < m; c += RT) {
+      a.phre[(size_t)i * a.ldphi + c] /= dr;
+      if (CPLX) a.phim[(size_t)i * a.ldphi + c] /= dr;
     }
+    __syncthreads();
+    for (int e = tid; e < i * m; e += RT) {
+      const int r = e / m, c = e % m;
+      // X[r] -= conj(L[i][r]) X[i]
+      const double lr = Lr[(size_t)i * m + r], xr = a.phre[(size_t)i * a.ldphi + c];
+      if (CPLX) {
+        const double li = -Li[(size_t)i * m + r], xi = a.phim[(size_t)i * a.ldphi + c];
+        a.phre[(size_t)r * a.ldphi + c] -= lr * xr - li * xi;
+        a.phim[(size_t)r * a.ldphi + c] -= lr * xi + li * xr;
+      } else {
+        a.phre[(size_t)r * a.ldphi + c] -= lr * xr;
+      }
+    }
+    __syncthreads();
   }
   if (tid == 0) *a.status = 0;
-  (void)s_dbl;
 }
 
 size_t smem_for(int m) { return sizeof(double) * (4 * (size_t)m + 40); }
