@@ -25,6 +25,11 @@ namespace fb {
 namespace {
 
 constexpr int RT = 1024;  // threads
+constexpr int NWARP = RT / 32;
+// rows over warps, columns over lanes: no integer division, coalesced rows
+#define FOR2D(i, rows, j, cols)                              \
+  for (int i = threadIdx.x >> 5; i < (rows); i += NWARP)     \
+    for (int j = threadIdx.x & 31; j < (cols); j += 32)
 
 __device__ double block_sum(double x, double* sh) {
 #pragma unroll
@@ -89,8 +94,7 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   // finiteness (reduced.py:203-204)
   if (!a.check_only) {
     int bad = 0;
-    for (size_t e = tid; e < mm; e += RT) {
-      size_t i = e / m, j = e % m;
+    FOR2D(i, m, j, m) {
       double x = a.are[i * a.ld + j] + a.bre[i * a.ld + j];
       if (CPLX) x += a.aim[i * a.ld + j] + a.bim[i * a.ld + j];
       if (!isfinite(x)) bad = 1;
@@ -117,10 +121,9 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
 
   // 1. Cholesky L L^H = B, right-looking on a copy (reduced.py:22-40); the
   //    lower triangle of (Lr, Li) ends up holding L, the rest is zeroed.
-  for (size_t e = tid; e < mm; e += RT) {
-    size_t i = e / m, j = e % m;
-    Lr[e] = a.bre[i * a.ld + j];
-    if (CPLX) Li[e] = a.bim[i * a.ld + j];
+  FOR2D(i, m, j, m) {
+    Lr[(size_t)i * m + j] = a.bre[i * a.ld + j];
+    if (CPLX) Li[(size_t)i * m + j] = a.bim[i * a.ld + j];
   }
   __syncthreads();
   for (int j = 0; j < m; ++j) {
@@ -146,9 +149,8 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
     __syncthreads();
     // trailing update W[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
     const int t = m - j - 1;
-    for (int e = tid; e < t * t; e += RT) {
-      const int i = j + 1 + e / t, k = j + 1 + e % t;
-      if (k > i) continue;
+    FOR2D(ii, t, kk, ii + 1) {
+      const int i = j + 1 + ii, k = j + 1 + kk;
       const double xr = Lr[(size_t)i * m + j], yr = Lr[(size_t)k * m + j];
       if (CPLX) {
         const double xi = Li[(size_t)i * m + j], yi = -Li[(size_t)k * m + j];
@@ -160,11 +162,10 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
     }
     __syncthreads();
   }
-  for (size_t e = tid; e < mm; e += RT) {  // strictly upper part of L is zero
-    size_t i = e / m, j = e % m;
+  FOR2D(i, m, j, m) {  // strictly upper part of L is zero
     if (j > i) {
-      Lr[e] = 0.0;
-      if (CPLX) Li[e] = 0.0;
+      Lr[(size_t)i * m + j] = 0.0;
+      if (CPLX) Li[(size_t)i * m + j] = 0.0;
     }
   }
   __syncthreads();
@@ -183,8 +184,8 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
       }
       __syncthreads();
       const int t = m - i - 1;
-      for (int e = tid; e < t * m; e += RT) {
-        const int r = i + 1 + e / m, c = e % m;
+      FOR2D(rr, t, c, m) {
+        const int r = i + 1 + rr;
         const double lr = Lr[(size_t)r * m + i], xr = Xr[(size_t)i * m + c];
         if (CPLX) {
           const double li = Li[(size_t)r * m + i], xi = Xi[(size_t)i * m + c];
@@ -199,31 +200,28 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   };
 
   // 2. C = L^-1 A L^-H  (reduced.py:209-212)
-  for (size_t e = tid; e < mm; e += RT) {
-    size_t i = e / m, j = e % m;
-    Cr[e] = a.are[i * a.ld + j];
-    if (CPLX) Ci[e] = a.aim[i * a.ld + j];
+  FOR2D(i, m, j, m) {
+    Cr[(size_t)i * m + j] = a.are[i * a.ld + j];
+    if (CPLX) Ci[(size_t)i * m + j] = a.aim[i * a.ld + j];
   }
   __syncthreads();
   lower_solve(Cr, Ci);                       // W = L^-1 A
-  for (size_t e = tid; e < mm; e += RT) {    // T = W^H
-    size_t i = e / m, j = e % m;
-    Tr[j * m + i] = Cr[e];
-    if (CPLX) Ti[j * m + i] = -Ci[e];
+  FOR2D(j, m, i, m) {                        // T = W^H (coalesced writes)
+    Tr[(size_t)j * m + i] = Cr[(size_t)i * m + j];
+    if (CPLX) Ti[(size_t)j * m + i] = -Ci[(size_t)i * m + j];
   }
   __syncthreads();
   lower_solve(Tr, Ti);                       // X = L^-1 W^H
-  for (size_t e = tid; e < mm; e += RT) {    // C = X^H, then (C + C^H)/2
-    size_t i = e / m, j = e % m;
-    const double xr = Tr[j * m + i], yr = Tr[i * m + j];
-    Cr[e] = 0.5 * (xr + yr);
-    if (CPLX) Ci[e] = 0.5 * (-Ti[j * m + i] + Ti[i * m + j]);
+  FOR2D(i, m, j, m) {                        // C = X^H, then (C + C^H)/2
+    const double xr = Tr[(size_t)j * m + i], yr = Tr[(size_t)i * m + j];
+    Cr[(size_t)i * m + j] = 0.5 * (xr + yr);
+    if (CPLX) Ci[(size_t)i * m + j] = 0.5 * (-Ti[(size_t)j * m + i] + Ti[(size_t)i * m + j]);
   }
+  __syncthreads();
   // V = I, row-major in T during the Householder phase
-  for (size_t e = tid; e < mm; e += RT) {
-    size_t i = e / m, j = e % m;
-    Tr[e] = (i == j) ? 1.0 : 0.0;
-    if (CPLX) Ti[e] = 0.0;
+  FOR2D(i, m, j, m) {
+    Tr[(size_t)i * m + j] = (i == j) ? 1.0 : 0.0;
+    if (CPLX) Ti[(size_t)i * m + j] = 0.0;
   }
   __syncthreads();
 
@@ -298,42 +296,43 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
     for (int i = tid; i < len; i += RT) part += ur[i] * pr[i] + (CPLX ? ui[i] * pi[i] : 0.0);
     const double kap2 = 2.0 * block_sum(part, sh);
     // sub -= p u^H ; sub -= u p^H ; sub += 2 kappa u u^H ; V[:, k+1:] -= 2 w u^H
-    for (size_t e = tid; e < (size_t)len * len + (size_t)m * len; e += RT) {
-      if (e < (size_t)len * len) {
-        const int i = (int)(e / len), j = (int)(e % len);
-        const size_t o = (size_t)(k + 1 + i) * m + k + 1 + j;
-        if (CPLX) {
-          double tr, ti;
-          double sr = Cr[o], si = Ci[o];
-          cmul(pr[i], pi[i], ur[j], -ui[j], tr, ti);
-          sr -= tr;
-          si -= ti;
-          cmul(ur[i], ui[i], pr[j], -pi[j], tr, ti);
-          sr -= tr;
-          si -= ti;
-          cmul(ur[i], ui[i], ur[j], -ui[j], tr, ti);
-          sr += kap2 * tr;
-          si += kap2 * ti;
-          Cr[o] = sr;
-          Ci[o] = si;
+    for (int i = warp; i < len + m; i += NWARP) {
+      const bool isc = i < len;
+      for (int j = lane; j < len; j += 32) {
+        if (isc) {
+          const size_t o = (size_t)(k + 1 + i) * m + k + 1 + j;
+          if (CPLX) {
+            double tr, ti;
+            double sr = Cr[o], si = Ci[o];
+            cmul(pr[i], pi[i], ur[j], -ui[j], tr, ti);
+            sr -= tr;
+            si -= ti;
+            cmul(ur[i], ui[i], pr[j], -pi[j], tr, ti);
+            sr -= tr;
+            si -= ti;
+            cmul(ur[i], ui[i], ur[j], -ui[j], tr, ti);
+            sr += kap2 * tr;
+            si += kap2 * ti;
+            Cr[o] = sr;
+            Ci[o] = si;
+          } else {
+            double s_ = Cr[o];
+            s_ -= pr[i] * ur[j];
+            s_ -= ur[i] * pr[j];
+            s_ += kap2 * (ur[i] * ur[j]);
+            Cr[o] = s_;
+          }
         } else {
-          double s = Cr[o];
-          s -= pr[i] * ur[j];
-          s -= ur[i] * pr[j];
-          s += kap2 * (ur[i] * ur[j]);
-          Cr[o] = s;
-        }
-      } else {
-        const size_t f = e - (size_t)len * len;
-        const int r = (int)(f / len), j = (int)(f % len);
-        const size_t o = (size_t)r * m + k + 1 + j;
-        if (CPLX) {
-          double tr, ti;
-          cmul(wr[r], wi[r], ur[j], -ui[j], tr, ti);
-          Tr[o] -= 2.0 * tr;
-          Ti[o] -= 2.0 * ti;
-        } else {
-          Tr[o] -= 2.0 * (wr[r] * ur[j]);
+          const int r = i - len;
+          const size_t o = (size_t)r * m + k + 1 + j;
+          if (CPLX) {
+            double tr, ti;
+            cmul(wr[r], wi[r], ur[j], -ui[j], tr, ti);
+            Tr[o] -= 2.0 * tr;
+            Ti[o] -= 2.0 * ti;
+          } else {
+            Tr[o] -= 2.0 * (wr[r] * ur[j]);
+          }
         }
       }
     }
@@ -374,8 +373,8 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   }
   __syncthreads();
   // V^T for the QL: Vt[c][r] = V[r][c] * phi[c]
-  for (size_t e = tid; e < mm; e += RT) {
-    const int r = (int)(e / m), c = (int)(e % m);
+  FOR2D(c, m, r, m) {  // coalesced writes of V^T
+    const size_t e = (size_t)r * m + c;
     if (CPLX) {
       double tr, ti;
       cmul(Tr[e], Ti[e], wr[c], wi[c], tr, ti);
@@ -483,9 +482,8 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   }
   __syncthreads();
   // X[i][c] = V[i][order[c]] = Vt[order[c]][i], into phi directly
-  for (size_t e = tid; e < mm; e += RT) {
-    int i = (int)(e / m), c = (int)(e % m);
-    int oc = order[c];
+  FOR2D(c, m, i, m) {
+    const int oc = order[c];
     a.phre[(size_t)i * a.ldphi + c] = Vr[(size_t)oc * m + i];
     if (CPLX) a.phim[(size_t)i * a.ldphi + c] = Vi[(size_t)oc * m + i];
   }
@@ -498,8 +496,7 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
       if (CPLX) a.phim[(size_t)i * a.ldphi + c] /= dr;
     }
     __syncthreads();
-    for (int e = tid; e < i * m; e += RT) {
-      const int r = e / m, c = e % m;
+    FOR2D(r, i, c, m) {
       // X[r] -= conj(L[i][r]) X[i]
       const double lr = Lr[(size_t)i * m + r], xr = a.phre[(size_t)i * a.ldphi + c];
       if (CPLX) {
