@@ -449,18 +449,28 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
         if (tid == 0) *a.status = -1;
         return;
       }
-      for (int r = tid; r < m; r += RT) {
-        for (int t = 0; t < nrot; ++t) {
-          const int i = first - 1 - t;
-          const double c = rc[i], s = rs[i];
-          double zr = Vr[(size_t)i * m + r], zr1 = Vr[(size_t)(i + 1) * m + r];
-          Vr[(size_t)(i + 1) * m + r] = s * zr + c * zr1;
-          Vr[(size_t)i * m + r] = c * zr - s * zr1;
-          if (CPLX) {
-            double zi = Vi[(size_t)i * m + r], zi1 = Vi[(size_t)(i + 1) * m + r];
-            Vi[(size_t)(i + 1) * m + r] = s * zi + c * zi1;
-            Vi[(size_t)i * m + r] = c * zi - s * zi1;
+      // rotation t acts on rows (i, i+1), i = first-1-t; the new row i is the
+      // "row i+1" of rotation t+1, so it is carried in a register and only the
+      // independent loads of row i go to memory.
+      if (nrot > 0) {
+        for (int r = tid; r < m; r += RT) {
+          double cr = Vr[(size_t)first * m + r];
+          double ci = CPLX ? Vi[(size_t)first * m + r] : 0.0;
+          for (int t = 0; t < nrot; ++t) {
+            const int i = first - 1 - t;
+            const double c = rc[i], s = rs[i];
+            const double zr = Vr[(size_t)i * m + r];
+            Vr[(size_t)(i + 1) * m + r] = s * zr + c * cr;
+            cr = c * zr - s * cr;
+            if (CPLX) {
+              const double zi = Vi[(size_t)i * m + r];
+              Vi[(size_t)(i + 1) * m + r] = s * zi + c * ci;
+              ci = c * zi - s * ci;
+            }
           }
+          const int last = first - nrot;
+          Vr[(size_t)last * m + r] = cr;
+          if (CPLX) Vi[(size_t)last * m + r] = ci;
         }
       }
       __syncthreads();
