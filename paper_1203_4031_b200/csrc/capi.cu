@@ -13,6 +13,7 @@
 
 namespace fb {
 void panel_profile_read(unsigned long long* out);
+void reduced_profile_read(unsigned long long* out);
 }
 
 std::atomic<long long> fb::g_launches{0};
@@ -381,6 +382,11 @@ int fb_band_solve(fb_ctx* c, int n, int kl, int nrhs, const double* fr, const do
 // Debug only (not part of the ABI header): cycles per panel phase, CTA 0 / thread 0.
 int fb_debug_panel_profile(unsigned long long* out8) {
   fb::panel_profile_read(out8);
+  return FB_OK;
+}
+
+int fb_debug_reduced_profile(unsigned long long* out8) {
+  fb::reduced_profile_read(out8);
   return FB_OK;
 }
 

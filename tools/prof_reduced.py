@@ -18,7 +18,10 @@ for m, cplx in ((150, False), (160, False), (256, True), (512, True)):
     A, B = dev.upload(a, cplx=cplx), dev.upload(b, cplx=cplx)
     PHI = dev.empty(m, m, cplx)
     eps = torch.empty(m, dtype=torch.float64, device=dev.tdev)
+    import ctypes
+    buf = (ctypes.c_ulonglong * 8)()
     for rep in range(3):
+        dev.lib.fb_debug_reduced_profile(buf)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record()
         f = dev.chol_check(B, m)
@@ -31,3 +34,5 @@ for m, cplx in ((150, False), (160, False), (256, True), (512, True)):
     err = np.abs(eps.cpu().numpy() - ref).max()
     print(f"m={m} cplx={cplx}: chol {e[0].elapsed_time(e[1]):.3f} ms, eig {e[1].elapsed_time(e[2]):.3f} ms, "
           f"status={st} fail={f} max|d eps|={err:.2e}", flush=True)
+    dev.lib.fb_debug_reduced_profile(buf)
+    print("   cycles: chol(2 launches) %d, C %d, householder %d, fold %d, QL %d, backsolve %d" % tuple(buf[:6]))
