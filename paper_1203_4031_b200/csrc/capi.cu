@@ -14,6 +14,7 @@
 namespace fb {
 void panel_profile_read(unsigned long long* out);
 void reduced_profile_read(unsigned long long* out);
+void reduced_cluster_profile_read(unsigned long long* out);
 }
 
 std::atomic<long long> fb::g_launches{0};
@@ -316,9 +317,12 @@ int fb_residuals(fb_ctx* c, int n, int m, const double* axr, const double* axi, 
 int fb_chol_check(fb_ctx* c, int m, const double* bre, const double* bim, int64_t ld, int* fail) {
   CTX_GUARD(c);
   if (m <= 0 || !fail) return FB_ERR_ARG;
-  int r = ensure_scratch(c, fb::reduced_scratch_bytes(m));
+  const bool cl = fb::reduced_cluster_ok(m, bim != nullptr);
+  int r = ensure_scratch(c, cl ? fb::reduced_cluster_scratch_bytes(m) : fb::reduced_scratch_bytes(m));
   if (r) return r;
-  cudaError_t e = fb::chol_check_launch(m, bre, bim, ld, c->dev_word, (double*)c->scratch, c->stream);
+  cudaError_t e = cl ? fb::reduced_cluster_launch(m, bre, bim, bre, bim, ld, nullptr, nullptr, nullptr, 0,
+                                                  c->dev_word, (double*)c->scratch, 1, c->stream)
+                     : fb::chol_check_launch(m, bre, bim, ld, c->dev_word, (double*)c->scratch, c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(c->host_word, c->dev_word, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -332,10 +336,13 @@ int fb_reduced_eig(fb_ctx* c, int m, const double* are, const double* aim, const
                    int* status) {
   CTX_GUARD(c);
   if (m <= 0 || !status || !eps || !phre) return FB_ERR_ARG;
-  int r = ensure_scratch(c, fb::reduced_scratch_bytes(m));
+  const bool cl = fb::reduced_cluster_ok(m, bim != nullptr) && !getenv("FB_REDUCED_QL");
+  int r = ensure_scratch(c, cl ? fb::reduced_cluster_scratch_bytes(m) : fb::reduced_scratch_bytes(m));
   if (r) return r;
-  cudaError_t e = fb::reduced_eig_launch(m, are, aim, bre, bim, ld, eps, phre, phim, ldphi, c->dev_word,
-                                         (double*)c->scratch, c->stream);
+  cudaError_t e = cl ? fb::reduced_cluster_launch(m, are, aim, bre, bim, ld, eps, phre, phim, ldphi,
+                                                  c->dev_word, (double*)c->scratch, 0, c->stream)
+                     : fb::reduced_eig_launch(m, are, aim, bre, bim, ld, eps, phre, phim, ldphi, c->dev_word,
+                                              (double*)c->scratch, c->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(c->host_word, c->dev_word, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -386,7 +393,14 @@ int fb_debug_panel_profile(unsigned long long* out8) {
 }
 
 int fb_debug_reduced_profile(unsigned long long* out8) {
+  // single-CTA counters, or the cluster kernel's when it ran
+  unsigned long long c8[8];
   fb::reduced_profile_read(out8);
+  fb::reduced_cluster_profile_read(c8);
+  bool any = false;
+  for (int k = 0; k < 8; ++k) any |= c8[k] != 0;
+  if (any)
+    for (int k = 0; k < 8; ++k) out8[k] = c8[k];
   return FB_OK;
 }
 

@@ -25,5 +25,12 @@ cudaError_t reduced_eig_launch(int m, const double* are, const double* aim, cons
                                const double* bim, long long ld, double* eps, double* phre,
                                double* phim, long long ldphi, int* status, double* scratch,
                                cudaStream_t st);
+// cluster (DSMEM-resident) variant for M0 <= 256 (reduced_cluster.cu)
+bool reduced_cluster_ok(int m, bool cplx);
+size_t reduced_cluster_scratch_bytes(int m);
+cudaError_t reduced_cluster_launch(int m, const double* are, const double* aim, const double* bre,
+                                   const double* bim, long long ld, double* eps, double* phre, double* phim,
+                                   long long ldphi, int* status, double* scratch, int check_only,
+                                   cudaStream_t st);
 
 }  // namespace fb

@@ -241,33 +241,6 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   __shared__ int s_int[4];
   __shared__ double s_val[2];
 
-  // finiteness (reduced.py:203-204)
-  if (!a.check_only) {
-    int bad = 0;
-    FOR2D(i, m, j, m) {
-      double x = a.are[i * a.ld + j] + a.bre[i * a.ld + j];
-      if (CPLX) x += a.aim[i * a.ld + j] + a.bim[i * a.ld + j];
-      if (!isfinite(x)) bad = 1;
-    }
-    if (__syncthreads_or(bad)) {
-      if (tid == 0) *a.status = -2;
-      return;
-    }
-  }
-  if (m == 1 && !a.check_only) {  // reduced.py:205-210
-    if (tid == 0) {
-      double b00 = a.bre[0];
-      if (b00 <= 0) {
-        *a.status = -2;
-      } else {
-        a.eps[0] = a.are[0] / b00;
-        a.phre[0] = 1.0 / sqrt(b00);
-        if (CPLX) a.phim[0] = 0.0;
-        *a.status = 0;
-      }
-    }
-    return;
-  }
 
   // 1. Cholesky L L^H = B, right-looking on a copy (reduced.py:22-40); the
   //    lower triangle of (Lr, Li) ends up holding L, the rest is zeroed.
@@ -320,6 +293,31 @@ __global__ void __launch_bounds__(RT, 1) reduced_kernel(RArgs a) {
   }
   __syncthreads();
   RPROBE(0);
+  if (!a.check_only) {
+    // finiteness after the Cholesky: a pivot failure wins (the caller shrinks
+    // M0, kernel.py:385-400), otherwise non-finite input is the reduced solver
+    // error (reduced.py:203-204)
+    int bad = 0;
+    FOR2D(i, m, j, m) {
+      double x = a.are[i * a.ld + j] + a.bre[i * a.ld + j];
+      if (CPLX) x += a.aim[i * a.ld + j] + a.bim[i * a.ld + j];
+      if (!isfinite(x)) bad = 1;
+    }
+    if (__syncthreads_or(bad)) {
+      if (tid == 0) *a.status = -2;
+      return;
+    }
+    if (m == 1) {  // reduced.py:205-210
+      if (tid == 0) {
+        const double b00 = a.bre[0];
+        a.eps[0] = a.are[0] / b00;
+        a.phre[0] = 1.0 / sqrt(b00);
+        if (CPLX) a.phim[0] = 0.0;
+        *a.status = 0;
+      }
+      return;
+    }
+  }
   if (a.check_only) {
     if (tid == 0) *a.status = 0;
     return;

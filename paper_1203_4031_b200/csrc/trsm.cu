@@ -2,25 +2,31 @@
 //
 // One cooperative kernel per sweep replaces the 2*N/32 launches of a blocked
 // TRSM.  Blocks of 32 rows are finalised in processing order b(0), b(1), ...
-// (ascending for the L / U^H sweeps, descending for U / L^H); at step t:
-//   * "look-ahead" CTAs finalise the NEXT block for their 16-column chunk:
+// (ascending for the L / U^H sweeps, descending for U / L^H).  The right-hand
+// sides are cut into 32-column chunks and every CTA owns ONE chunk for the
+// whole sweep (a group of S CTAs per chunk), so at step t it stages the final
+// block X_{b(t)}[:, chunk] in shared memory once and then:
+//   * sub-CTA 0 of the group finalises the NEXT block ("look-ahead"):
 //       X_{b(t+1)} <- D_{b(t+1)} X_{b(t+1)} - G_{b(t+1)} X_{b(t)}
 //     with D the diagonal-block inverse and G = D * M(b(t+1), b(t)) precomputed
 //     per factor, so the critical path per step is ONE K=64 product;
-//   * all CTAs stream the rank-32 update of the rows still pending,
+//   * the group streams the rank-32 update of its share of the pending rows,
 //       X_i -= M(i, b(t)) X_{b(t)},   i in b(t+2) ...
-//     as (32-row block, 16-column chunk) items, double-buffered with cp.async
-//     (operator tile reused while consecutive items share a row block);
-//   * one grid barrier per step (its gpu-scope fence also invalidates L1, so
-//     the .ca cp.async reads of X never see stale lines).
+//     with the 32x32 M tiles double-buffered by 16-byte cp.async and the X_i
+//     accumulators prefetched straight into registers (L2-only loads);
+//   * one grid barrier per step.
 // All products run on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA),
-// complex as 4 real DMMAs on planar operands.
+// complex as 4 real DMMAs on planar operands; each warp owns a 16x16 sub-tile
+// (8 independent accumulator chains).
 //
 //   variant 0  L   forward  (direct solve, after the row gather P B)
 //   variant 1  U   backward (direct solve)
 //   variant 2  U^H forward  (adjoint solve)
 //   variant 3  L^H backward (adjoint solve, then the row scatter P^T)
 #include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdint>
 
 #include "common.cuh"
 #include "trsm.cuh"
@@ -31,17 +37,12 @@ namespace fb {
 
 namespace {
 
-constexpr int BS = 32;   // block rows (= PW of the factorization)
-constexpr int CW = 16;   // right-hand-side columns per chunk
-constexpr int TT = 128;  // threads (4 warps, 8 rows each)
-constexpr int PA = 36;   // A tile pitch: conflict-free A fragments
-constexpr int PB = 24;   // B tile pitch: conflict-free B fragments
-constexpr int PC = 18;   // C tile pitch
-constexpr int A_SZ = 2 * BS * PA;
-constexpr int B_SZ = 2 * BS * PB;
-constexpr int C_SZ = 2 * BS * PC;
-constexpr int STAGE = A_SZ + B_SZ + C_SZ;  // doubles per pipeline stage
-constexpr int GM_BLK = 4 * BS * BS;        // per (variant, block): G re/im, D re/im
+constexpr int BS = 32;                 // block rows (= PW of the factorization)
+constexpr int CW = 32;                 // right-hand-side columns per chunk
+constexpr int TT = 128;                // threads: 4 warps in a 2x2 grid of 16x16 sub-tiles
+constexpr int PA = 36;                 // tile pitch (= 4 mod 16: conflict-free fragments, both orientations)
+constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 tile in shared memory
+constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): G re/im, D re/im
 
 struct SweepArgs {
   int n, nrhs, nblk, variant;
@@ -67,134 +68,199 @@ __device__ __forceinline__ int blk_at(const SweepArgs& a, int t) {
   return (a.variant == 0 || a.variant == 2) ? t : a.nblk - 1 - t;
 }
 
-// --- cp.async tile loaders ------------------------------------------------------
-// A tile of M(i, b) (rows of block i, columns of block b); for the adjoint
-// variants the tile is the transpose of LU(b, i) and is conjugated at use.
-__device__ __forceinline__ void cp_m_tile(const SweepArgs& a, int bi, int bb, double* s) {
-  const int i0 = bi * BS, b0 = bb * BS;
-  const bool trans = a.variant >= 2;
-  for (int e = threadIdx.x; e < BS * BS; e += TT) {
-    int r, k;
-    if (!trans) { r = e / BS; k = e % BS; } else { k = e / BS; r = e % BS; }
-    const int gr = i0 + r, gk = b0 + k;
-    const bool ok = gr < a.n && gk < a.n;
-    const long long o = ok ? (trans ? (long long)gk * a.ld + gr : (long long)gr * a.ld + gk) : 0;
-    cp_async8(s + r * PA + k, a.lre + o, ok);
-    cp_async8(s + BS * PA + r * PA + k, a.lim + o, ok);
+// --- cp.async tile loader ---------------------------------------------------------
+// Natural copy of the planar block [r0, r0 + 32) x [c0, c0 + 32) of a row-major
+// matrix (row stride ld) into a pitch-PA tile; rows >= nr / cols >= nc read 0.
+template <bool VEC>
+__device__ __forceinline__ void cp_block(const double* re, const double* im, long long ld, int r0, int c0,
+                                         int nr, int nc, double* s) {
+  if (VEC) {
+    for (int e = threadIdx.x; e < BS * BS / 2; e += TT) {
+      const int r = e >> 4, c = (e & 15) * 2;
+      const int gr = r0 + r, gc = c0 + c;
+      const int valid = gr < nr ? max(0, min(2, nc - gc)) : 0;
+      const long long o = valid ? (long long)gr * ld + gc : 0;
+      cp_async16(s + r * PA + c, re + o, valid * 8);
+      cp_async16(s + BS * PA + r * PA + c, im + o, valid * 8);
+    }
+  } else {
+    for (int e = threadIdx.x; e < BS * BS; e += TT) {
+      const int r = e >> 5, c = e & 31;
+      const int gr = r0 + r, gc = c0 + c;
+      const bool ok = gr < nr && gc < nc;
+      const long long o = ok ? (long long)gr * ld + gc : 0;
+      cp_async8(s + r * PA + c, re + o, ok);
+      cp_async8(s + BS * PA + r * PA + c, im + o, ok);
+    }
   }
 }
 
-// A tile from the per-factor operator store (G or D of this variant)
-__device__ __forceinline__ void cp_op_tile(const double* src, double* s) {
-  for (int e = threadIdx.x; e < BS * BS; e += TT) {
-    const int r = e / BS, k = e % BS;
-    cp_async8(s + r * PA + k, src + e, true);
-    cp_async8(s + BS * PA + r * PA + k, src + BS * BS + e, true);
-  }
+// contiguous 32x32 operator tile (G or D of this variant)
+template <bool VEC>
+__device__ __forceinline__ void cp_op(const double* src, double* s) {
+  cp_block<VEC>(src, src + BS * BS, BS, 0, 0, BS, BS, s);
 }
 
-// rows of block b, columns [c0, c0 + CW) of X into a tile with pitch P
-template <int P>
-__device__ __forceinline__ void cp_x_tile(const SweepArgs& a, int b, int c0, double* s) {
-  const int r0 = b * BS;
-  for (int e = threadIdx.x; e < BS * CW; e += TT) {
-    const int k = e / CW, c = e % CW;
-    const int gr = r0 + k, gc = c0 + c;
-    const bool ok = gr < a.n && gc < a.nrhs;
-    const long long o = ok ? (long long)gr * a.ldx + gc : 0;
-    cp_async8(s + k * P + c, a.xre + o, ok);
-    cp_async8(s + BS * P + k * P + c, a.xim + o, ok);
-  }
+// --- warp sub-tile arithmetic ---------------------------------------------------
+// accumulator fragment: rows wr*16 + mt*8 + (lane>>2), cols wc*16 + nt*8 + 2*(lane&3) + e
+struct Acc {
+  double r[2][2][2], i[2][2][2];
+};
+
+__device__ __forceinline__ void acc_zero(Acc& c) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) c.r[mt][nt][e] = c.i[mt][nt][e] = 0.0;
 }
 
-// acc (8 rows x 16 cols per warp) += sign * A(32x32) B(32x16); conj_a negates Im(A)
-__device__ __forceinline__ void tile_mma(double (&ar_)[2][2], double (&ai_)[2][2], const double* A,
-                                         const double* B, double sign, double sign_i) {
+// acc += (sr*Re A + i*si*Im A) (32x32) * B (32x32 tile of X); A is read as
+// A[r][k] = S[r*PA + k] (TR = false) or S[k*PA + r] (TR = true)
+template <bool TR>
+__device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* B, double sr, double si) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int row = w * 8 + (lane >> 2);
-  const double* Ar = A;
+  const int wr = w >> 1, wc = w & 1;
   const double* Ai = A + BS * PA;
-  const double* Br = B;
-  const double* Bi = B + BS * PB;
+  const double* Bi = B + BS * PA;
 #pragma unroll
   for (int k0 = 0; k0 < BS; k0 += 4) {
     const int k = k0 + (lane & 3);
-    const double a_r = sign * Ar[row * PA + k];
-    const double a_i = sign_i * Ai[row * PA + k];
-    const double na_i = -a_i;
+    double ar[2], ai[2], nai[2], br[2], bi[2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = wr * 16 + mt * 8 + (lane >> 2);
+      const int o = TR ? k * PA + r : r * PA + k;
+      ar[mt] = sr * A[o];
+      ai[mt] = si * Ai[o];
+      nai[mt] = -ai[mt];
+    }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const double b_r = Br[k * PB + nt * 8 + (lane >> 2)];
-      const double b_i = Bi[k * PB + nt * 8 + (lane >> 2)];
-      dmma(ar_[nt][0], ar_[nt][1], a_r, b_r);
-      dmma(ar_[nt][0], ar_[nt][1], na_i, b_i);
-      dmma(ai_[nt][0], ai_[nt][1], a_r, b_i);
-      dmma(ai_[nt][0], ai_[nt][1], a_i, b_r);
+      const int col = wc * 16 + nt * 8 + (lane >> 2);
+      br[nt] = B[k * PA + col];
+      bi[nt] = Bi[k * PA + col];
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        dmma(c.r[mt][nt][0], c.r[mt][nt][1], ar[mt], br[nt]);
+        dmma(c.i[mt][nt][0], c.i[mt][nt][1], ar[mt], bi[nt]);
+      }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        dmma(c.r[mt][nt][0], c.r[mt][nt][1], nai[mt], bi[nt]);
+        dmma(c.i[mt][nt][0], c.i[mt][nt][1], ai[mt], br[nt]);
+      }
+  }
+}
+
+// global X <-> accumulator fragments (L2-only loads: other CTAs wrote X in
+// earlier steps)
+template <bool VEC>
+__device__ __forceinline__ void acc_load(const SweepArgs& a, int b, int c0, Acc& c) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wr = w >> 1, wc = w & 1;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int gr = b * BS + wr * 16 + mt * 8 + (lane >> 2);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int gc = c0 + wc * 16 + nt * 8 + 2 * (lane & 3);
+      const long long o = (long long)gr * a.ldx + gc;
+      if (VEC && gr < a.n && gc + 1 < a.nrhs) {
+        const double2 vr = __ldcg(reinterpret_cast<const double2*>(a.xre + o));
+        const double2 vi = __ldcg(reinterpret_cast<const double2*>(a.xim + o));
+        c.r[mt][nt][0] = vr.x; c.r[mt][nt][1] = vr.y;
+        c.i[mt][nt][0] = vi.x; c.i[mt][nt][1] = vi.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = gr < a.n && gc + e < a.nrhs;
+          c.r[mt][nt][e] = ok ? __ldcg(a.xre + o + e) : 0.0;
+          c.i[mt][nt][e] = ok ? __ldcg(a.xim + o + e) : 0.0;
+        }
+      }
     }
   }
 }
 
-__device__ __forceinline__ void acc_from_smem(const double* C, double (&ar_)[2][2], double (&ai_)[2][2]) {
+template <bool VEC>
+__device__ __forceinline__ void acc_store(const SweepArgs& a, int b, int c0, const Acc& c) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = w * 8 + (lane >> 2);
+  const int wr = w >> 1, wc = w & 1;
 #pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
+  for (int mt = 0; mt < 2; ++mt) {
+    const int gr = b * BS + wr * 16 + mt * 8 + (lane >> 2);
+    if (gr >= a.n) continue;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int c = nt * 8 + 2 * (lane & 3) + e;
-      ar_[nt][e] = C[r * PC + c];
-      ai_[nt][e] = C[BS * PC + r * PC + c];
-    }
-}
-
-__device__ __forceinline__ void acc_store(const SweepArgs& a, int b, int c0, const double (&ar_)[2][2],
-                                          const double (&ai_)[2][2]) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int gr = b * BS + w * 8 + (lane >> 2);
-  if (gr >= a.n) return;
+    for (int nt = 0; nt < 2; ++nt) {
+      const int gc = c0 + wc * 16 + nt * 8 + 2 * (lane & 3);
+      const long long o = (long long)gr * a.ldx + gc;
+      if (VEC && gc + 1 < a.nrhs) {
+        __stcg(reinterpret_cast<double2*>(a.xre + o), make_double2(c.r[mt][nt][0], c.r[mt][nt][1]));
+        __stcg(reinterpret_cast<double2*>(a.xim + o), make_double2(c.i[mt][nt][0], c.i[mt][nt][1]));
+      } else {
 #pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int gc = c0 + nt * 8 + 2 * (lane & 3) + e;
-      if (gc < a.nrhs) {
-        const long long o = (long long)gr * a.ldx + gc;
-        a.xre[o] = ar_[nt][e];
-        a.xim[o] = ai_[nt][e];
+        for (int e = 0; e < 2; ++e)
+          if (gc + e < a.nrhs) {
+            __stcg(a.xre + o + e, c.r[mt][nt][e]);
+            __stcg(a.xim + o + e, c.i[mt][nt][e]);
+          }
       }
     }
+  }
 }
 
 __device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b, int which) {
   return a.gmat + ((size_t)a.variant * a.nblk + b) * GM_BLK + which * 2 * BS * BS;  // 0: G, 1: D
 }
 
-__global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
-  extern __shared__ __align__(16) double s[];
-  SweepArgs a = a0;
-  offset_item(a, blockIdx.y);
-  cg::grid_group grid = cg::this_grid();
+// X tile rows of block b, chunk columns [c0, c0 + 32)
+template <bool VEC>
+__device__ __forceinline__ void cp_x(const SweepArgs& a, int b, int c0, double* s) {
+  cp_block<VEC>(a.xre, a.xim, a.ldx, b * BS, c0, a.n, a.nrhs, s);
+}
+
+// streamed operator tile M(i, b) (TR: stored as the natural block LU(b, i))
+template <bool VEC>
+__device__ __forceinline__ void cp_m(const SweepArgs& a, int bi, int bb, double* s) {
+  if (a.variant < 2)
+    cp_block<VEC>(a.lre, a.lim, a.ld, bi * BS, bb * BS, a.n, a.n, s);
+  else
+    cp_block<VEC>(a.lre, a.lim, a.ld, bb * BS, bi * BS, a.n, a.n, s);
+}
+
+template <bool TR, bool VEC>
+__device__ void sweep_body(SweepArgs& a, cg::grid_group& grid, double* s) {
   const int G = gridDim.x, g = blockIdx.x;
   const int C = ceil_div(a.nrhs, CW);
-  const double conj_i = a.variant >= 2 ? -1.0 : 1.0;  // Im sign of the streamed M tiles
-  double* st0 = s;
-  double* st1 = s + STAGE;
-  auto A_of = [&](double* st) { return st; };
-  auto B_of = [&](double* st) { return st + A_SZ; };
-  auto C_of = [&](double* st) { return st + A_SZ + B_SZ; };
+  // chunk group of this CTA: one chunk if G >= C, else chunks g, g + G, ...
+  const int S = G >= C ? G / C + (g % C < G % C ? 1 : 0) : 1;
+  const int sub = G >= C ? g / C : 0;
+  const double conj_i = TR ? -1.0 : 1.0;  // Im sign of the streamed M tiles
+  double* Xt = s;             // X_{b(t)} chunk (B operand of every product this step)
+  double* Xn = s + TILE;      // X_{b(t+1)} chunk (look-ahead)
+  double* T0 = s + 2 * TILE;  // operator stage 0
+  double* T1 = s + 3 * TILE;  // operator stage 1
 
   // prologue: the first block of the sweep is final after D
-  {
+  if (sub == 0) {
     const int b0 = blk_at(a, 0);
     for (int c = g; c < C; c += G) {
-      cp_op_tile(op_ptr(a, b0, 1), A_of(st0));
-      cp_x_tile<PB>(a, b0, c * CW, B_of(st0));
+      cp_op<VEC>(op_ptr(a, b0, 1), T0);
+      cp_x<VEC>(a, b0, c * CW, Xt);
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
-      double accr[2][2] = {{0, 0}, {0, 0}}, acci[2][2] = {{0, 0}, {0, 0}};
-      tile_mma(accr, acci, A_of(st0), B_of(st0), 1.0, 1.0);
-      acc_store(a, b0, c * CW, accr, acci);
+      Acc acc;
+      acc_zero(acc);
+      tile_mma<false>(acc, T0, Xt, 1.0, 1.0);
+      acc_store<VEC>(a, b0, c * CW, acc);
       __syncthreads();
     }
   }
@@ -202,63 +268,68 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
 
   for (int t = 0; t < a.nblk; ++t) {
     const int bt = blk_at(a, t);
-    // look-ahead: finalise block b(t+1) = D X_{b(t+1)} - G X_{b(t)}
-    if (t + 1 < a.nblk) {
-      const int bn = blk_at(a, t + 1);
-      for (int c = g; c < C; c += G) {
-        cp_op_tile(op_ptr(a, bn, 1), A_of(st0));
-        cp_x_tile<PB>(a, bn, c * CW, B_of(st0));
-        cp_op_tile(op_ptr(a, bn, 0), A_of(st1));
-        cp_x_tile<PB>(a, bt, c * CW, B_of(st1));
+    const bool ahead = t + 1 < a.nblk;
+    const int R = max(0, a.nblk - t - 2);  // pending row blocks
+    // units: [0, 2) = look-ahead (weight of two products), then one per pending row block
+    const int U = R + (ahead ? 2 : 0), u_off = ahead ? 2 : 0;
+    const int ub = (int)((long long)sub * U / S), ue = (int)((long long)(sub + 1) * U / S);
+    const bool do_ahead = ahead && ub == 0 && ue > 0;
+    const int qb = max(ub - u_off, 0), qe = max(ue - u_off, 0);
+    for (int c = (G >= C ? g % C : g); c < C; c += (G >= C ? C : G)) {
+      const int c0 = c * CW;
+      if (!do_ahead && qb >= qe) break;
+      cp_x<VEC>(a, bt, c0, Xt);
+      if (do_ahead) {
+        const int bn = blk_at(a, t + 1);
+        cp_x<VEC>(a, bn, c0, Xn);
+        cp_op<VEC>(op_ptr(a, bn, 1), T0);
+        cp_op<VEC>(op_ptr(a, bn, 0), T1);
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
-        double accr[2][2] = {{0, 0}, {0, 0}}, acci[2][2] = {{0, 0}, {0, 0}};
-        tile_mma(accr, acci, A_of(st0), B_of(st0), 1.0, 1.0);
-        tile_mma(accr, acci, A_of(st1), B_of(st1), -1.0, -1.0);
-        acc_store(a, bn, c * CW, accr, acci);
+        Acc acc;
+        acc_zero(acc);
+        tile_mma<false>(acc, T0, Xn, 1.0, 1.0);
+        tile_mma<false>(acc, T1, Xt, -1.0, -1.0);
+        acc_store<VEC>(a, bn, c0, acc);
         __syncthreads();
       }
-    }
-    // streamed rank-32 updates, items (row block, chunk), contiguous per CTA
-    const int nrest = a.nblk - t - 2;
-    if (nrest > 0) {
-      const int Q = nrest * C;
-      int w = (g - C) % G;
-      if (w < 0) w += G;
-      const int qb = (int)((long long)w * Q / G), qe = (int)((long long)(w + 1) * Q / G);
-      int a_rb[2] = {-1, -1};
-      auto issue = [&](int q, int sidx) {
-        double* st = sidx ? st1 : st0;
-        const int rb = blk_at(a, t + 2 + q / C), c0 = (q % C) * CW;
-        if (a_rb[sidx] != rb) {
-          cp_m_tile(a, rb, bt, A_of(st));
-          a_rb[sidx] = rb;
-        }
-        cp_x_tile<PB>(a, bt, c0, B_of(st));
-        cp_x_tile<PC>(a, rb, c0, C_of(st));
+      if (qb < qe) {
+        Acc cur, nxt;
+        cp_m<VEC>(a, blk_at(a, t + 2 + qb), bt, T0);
         cp_async_commit();
-      };
-      if (qb < qe) issue(qb, 0);
-      for (int q = qb; q < qe; ++q) {
-        const int sidx = (q - qb) & 1;
-        if (q + 1 < qe) {
-          issue(q + 1, sidx ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
+        acc_load<VEC>(a, blk_at(a, t + 2 + qb), c0, nxt);
+        for (int q = qb; q < qe; ++q) {
+          const int rb = blk_at(a, t + 2 + q);
+          double* Tq = ((q - qb) & 1) ? T1 : T0;
+          cur = nxt;
+          if (q + 1 < qe) {
+            const int rn = blk_at(a, t + 3 + q);
+            cp_m<VEC>(a, rn, bt, ((q - qb) & 1) ? T0 : T1);
+            cp_async_commit();
+            acc_load<VEC>(a, rn, c0, nxt);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncthreads();
+          tile_mma<TR>(cur, Tq, Xt, -1.0, -conj_i);
+          acc_store<VEC>(a, rb, c0, cur);
+          __syncthreads();
         }
-        __syncthreads();
-        double* st = sidx ? st1 : st0;
-        double accr[2][2], acci[2][2];
-        acc_from_smem(C_of(st), accr, acci);
-        tile_mma(accr, acci, A_of(st), B_of(st), -1.0, -conj_i);
-        acc_store(a, blk_at(a, t + 2 + q / C), (q % C) * CW, accr, acci);
-        __syncthreads();
       }
     }
     grid.sync();
   }
+}
+
+template <bool TR, bool VEC>
+__global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
+  extern __shared__ __align__(16) double s[];
+  SweepArgs a = a0;
+  offset_item(a, blockIdx.y);
+  cg::grid_group grid = cg::this_grid();
+  sweep_body<TR, VEC>(a, grid, s);
 }
 
 // Per (block, variant): D_v (the variant's diagonal inverse, conj-transposed for
@@ -320,9 +391,7 @@ __global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
   }
 }
 
-int g_sweep_blocks = 0;
-
-size_t sweep_smem() { return sizeof(double) * 2 * STAGE; }
+size_t sweep_smem() { return sizeof(double) * 4 * TILE; }
 
 }  // namespace
 
@@ -347,22 +416,33 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
   a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.xre = xre; a.xim = xim; a.ldx = ldx;
   a.slu = slu; a.sdinv = sdinv; a.sx = sx;
-  size_t smem = sweep_smem();
-  if (g_sweep_blocks == 0) {
-    cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // 16-byte paths need every row start 16-byte aligned
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool vec = ld % 2 == 0 && ldx % 2 == 0 && slu % 2 == 0 && sx % 2 == 0 && sdinv % 2 == 0 &&
+                   al(lre) && al(lim) && al(xre) && al(xim) && al(gmat);
+  const bool tr = variant >= 2;
+  void* fn = tr ? (vec ? (void*)sweep_kernel<true, true> : (void*)sweep_kernel<true, false>)
+                : (vec ? (void*)sweep_kernel<false, true> : (void*)sweep_kernel<false, false>);
+  const int ki = (tr ? 2 : 0) + (vec ? 1 : 0);
+  static int blocks[4] = {0, 0, 0, 0};
+  const size_t smem = sweep_smem();
+  if (blocks[ki] == 0) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel, TT, smem);
-    g_sweep_blocks = std::max(1, nb);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, TT, smem);
+    blocks[ki] = std::max(1, nb);
   }
   const int C = ceil_div(nrhs, CW);
-  const long long items = (long long)std::max(0, a.nblk - 2) * C;
-  const int cap = std::max(1, (g_sweep_blocks * kSMs) / count);
+  const int cap = (blocks[ki] * kSMs) / count;
   if (cap < 1) return cudaErrorInvalidValue;
-  int G = (int)std::min<long long>(cap, std::max<long long>(C, items));
+  // enough CTAs per chunk group to spread the pending rows, whole groups when possible
+  const int want = C * std::max(1, ceil_div(a.nblk, 2));
+  int G = std::min(cap, want);
+  if (G > C) G -= G % C;
   G = std::max(G, 1);
   void* args[] = {&a};
   count_launch();
-  return cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(G, count), dim3(TT), args, smem, st);
+  return cudaLaunchCooperativeKernel(fn, dim3(G, count), dim3(TT), args, smem, st);
 }
 
 }  // namespace fb

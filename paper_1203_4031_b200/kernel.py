@@ -389,12 +389,16 @@ class _RciKernel:
             dev.symmetrize(AQ)
             dev.symmetrize(BQ)
 
-            # shrink the subspace while the projected B fails its Cholesky (kernel.py:385-400)
+            # shrink the subspace while the projected B fails its Cholesky
+            # (kernel.py:385-400).  The reduced solve starts with that same
+            # Cholesky and reports its 1-based failing pivot, so the check and
+            # the solve are one launch; a failure shrinks M0 and retries.
+            st = 0
             while m0 > 0:
-                fail = dev.chol_check(BQ.rows_view(0, m0).cols_view(0, m0), m0)
-                if fail == 0:
+                st = dev.reduced_eig(self.AQ, self.BQ, m0, self.e_dev.data_ptr(), self.PHI)
+                if st <= 0:
                     break
-                m0 = fail - 1
+                m0 = st - 1
             if m0 == 0:
                 self.info = -3
                 if verbose:
@@ -409,7 +413,6 @@ class _RciKernel:
                 AP = AP.cols_view(0, m0)
                 W1 = W1.cols_view(0, m0)
                 X = X.cols_view(0, m0)
-            st = dev.reduced_eig(self.AQ, self.BQ, m0, self.e_dev.data_ptr(), self.PHI)
             if st != 0:
                 self.info = -3
                 if verbose:

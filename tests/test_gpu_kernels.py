@@ -178,6 +178,57 @@ def test_chol_check_failure_index(dev, unit_golden):
         assert fail == int(g[f"spd_{name}_fail"])
 
 
+def test_reduced_eig_reports_cholesky_pivot(dev, unit_golden):
+    """The reduced solve's status is the same 1-based failing pivot as
+    spd_factor (reduced.py:22-40); kernel.py's M0 shrink relies on it."""
+    g = unit_golden
+    for name in ("neg2", "neg1", "sing"):
+        mat = g[f"spd_{name}_in"]
+        n = mat.shape[0]
+        A, B = dev.upload(np.eye(n), cplx=False), dev.upload(mat, cplx=False)
+        PHI = dev.empty(n, n, False)
+        eps = dev.torch.empty(n, dtype=dev.torch.float64, device=dev.tdev)
+        assert dev.reduced_eig(A, B, n, eps.data_ptr(), PHI) == int(g[f"spd_{name}_fail"])
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_reduced_eig_nonfinite_is_solver_error(dev, cplx):
+    rng = np.random.default_rng(11)
+    n = 24
+    a = rng.standard_normal((n, n))
+    a = a + a.T
+    a[3, 5] = a[5, 3] = np.nan
+    b = np.eye(n)
+    A, B = dev.upload(a, cplx=cplx), dev.upload(b, cplx=cplx)
+    PHI = dev.empty(n, n, cplx)
+    eps = dev.torch.empty(n, dtype=dev.torch.float64, device=dev.tdev)
+    assert dev.reduced_eig(A, B, n, eps.data_ptr(), PHI) == -2
+
+
+@pytest.mark.parametrize("n,cplx", [(1, False), (3, True), (64, False), (150, False), (152, True),
+                                    (160, False), (256, True), (257, False), (300, True)])
+def test_reduced_eig_sizes(dev, n, cplx):
+    """Cluster path (M0 <= 256) and single-CTA path (larger) against LAPACK:
+    eigenvalues, A Phi = B Phi diag(eps) and Phi^H B Phi = I."""
+    import scipy.linalg as sla
+    rng = np.random.default_rng(n)
+    g = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+    a = (g + g.conj().T) / 2
+    h = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+    b = np.eye(n) + 0.1 * h @ h.conj().T / n
+    A, B = dev.upload(a, cplx=cplx), dev.upload(b, cplx=cplx)
+    PHI = dev.empty(n, n, cplx)
+    eps = dev.torch.empty(n, dtype=dev.torch.float64, device=dev.tdev)
+    assert dev.reduced_eig(A, B, n, eps.data_ptr(), PHI) == 0
+    e = eps.cpu().numpy()
+    ref = sla.eigh(a, b, eigvals_only=True)
+    scale = max(1.0, np.abs(ref).max())
+    assert np.abs(e - ref).max() <= 1e-12 * scale
+    phi = dev.download(PHI)
+    assert np.abs(a @ phi - b @ phi * e[None, :]).max() <= 1e-10 * scale
+    assert np.abs(phi.conj().T @ b @ phi - np.eye(n)).max() <= 1e-10
+
+
 def test_residuals_match_oracle(dev):
     rng = np.random.default_rng(5)
     n, m = 1500, 23

@@ -35,4 +35,6 @@ for m, cplx in ((150, False), (160, False), (256, True), (512, True)):
     print(f"m={m} cplx={cplx}: chol {e[0].elapsed_time(e[1]):.3f} ms, eig {e[1].elapsed_time(e[2]):.3f} ms, "
           f"status={st} fail={f} max|d eps|={err:.2e}", flush=True)
     dev.lib.fb_debug_reduced_profile(buf)
-    print("   cycles: chol(2 launches) %d, C %d, householder %d, fold %d, QL %d, backsolve %d" % tuple(buf[:6]))
+    print("   cycles: " + ", ".join(f"{k} {v}" for k, v in zip(
+        ("chol(2 launches)", "C", "householder", "fold|bisect", "QL|invit", "backsolve|backtransform", "-|backsolve"),
+        buf[:7])))
