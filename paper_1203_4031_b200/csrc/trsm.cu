@@ -14,7 +14,9 @@
 //       X_i -= M(i, b(t)) X_{b(t)},   i in b(t+2) ...
 //     with the 32x32 M tiles double-buffered by 16-byte cp.async and the X_i
 //     accumulators prefetched straight into registers (L2-only loads);
-//   * one grid barrier per step.
+//   * no grid barriers: per (row block, chunk) counters in global memory
+//     (release/acquire) let each CTA start a step as soon as the blocks it
+//     reads are final, so steps overlap (see sweep_body).
 // All products run on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA),
 // complex as 4 real DMMAs on planar operands; each warp owns a 16x16 sub-tile
 // (8 independent accumulator chains).
@@ -27,6 +29,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 
 #include "common.cuh"
 #include "trsm.cuh"
@@ -53,6 +58,7 @@ struct SweepArgs {
   double *xre, *xim;
   long long ldx;
   long long slu, sdinv, sx;  // batch strides (item b: + b * stride)
+  int *upd, *fin;             // dataflow counters [count][nblk][C] (zeroed per launch)
 };
 
 __device__ __forceinline__ void offset_item(SweepArgs& a, long long b) {
@@ -62,6 +68,9 @@ __device__ __forceinline__ void offset_item(SweepArgs& a, long long b) {
   a.gmat += b * a.sdinv;
   a.xre += b * a.sx;
   a.xim += b * a.sx;
+  const long long nc = (long long)a.nblk * ceil_div(a.nrhs, CW);
+  a.upd += b * nc;
+  a.fin += b * nc;
 }
 
 __device__ __forceinline__ int blk_at(const SweepArgs& a, int t) {
@@ -220,10 +229,23 @@ __device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b, int w
   return a.gmat + ((size_t)a.variant * a.nblk + b) * GM_BLK + which * 2 * BS * BS;  // 0: G, 1: D
 }
 
-// X tile rows of block b, chunk columns [c0, c0 + 32)
+// X tile rows of block b, chunk columns [c0, c0 + 32).  X is written by other
+// CTAs during the sweep, so it is read through L2 only (cp.async.cg, or plain
+// .cg loads on the unaligned path).
 template <bool VEC>
 __device__ __forceinline__ void cp_x(const SweepArgs& a, int b, int c0, double* s) {
-  cp_block<VEC>(a.xre, a.xim, a.ldx, b * BS, c0, a.n, a.nrhs, s);
+  if (VEC) {
+    cp_block<true>(a.xre, a.xim, a.ldx, b * BS, c0, a.n, a.nrhs, s);
+  } else {
+    for (int e = threadIdx.x; e < BS * BS; e += TT) {
+      const int r = e >> 5, c = e & 31;
+      const int gr = b * BS + r, gc = c0 + c;
+      const bool ok = gr < a.n && gc < a.nrhs;
+      const long long o = (long long)gr * a.ldx + gc;
+      s[r * PA + c] = ok ? __ldcg(a.xre + o) : 0.0;
+      s[BS * PA + r * PA + c] = ok ? __ldcg(a.xim + o) : 0.0;
+    }
+  }
 }
 
 // streamed operator tile M(i, b) (TR: stored as the natural block LU(b, i))
@@ -235,8 +257,39 @@ __device__ __forceinline__ void cp_m(const SweepArgs& a, int bi, int bb, double*
     cp_block<VEC>(a.lre, a.lim, a.ld, bb * BS, bi * BS, a.n, a.n, s);
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_ge(const int* p, int v) {
+  while (ld_acquire(p) < v) __nanosleep(20);
+}
+// after a __syncthreads that follows the tile stores: publish (thread 0)
+__device__ __forceinline__ void publish(int* p, int v) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(p, v);
+  }
+}
+
+// Dataflow schedule (no grid barriers).  Per (row block i, chunk c):
+//   upd[i][c] = number of streamed rank-32 updates applied so far,
+//   fin[i][c] = 1 once X_i[:, c] is final.
+// Step t: the look-ahead for b(t+1) needs fin[b(t)] and upd[b(t+1)] == t;
+// the streamed update of row block i needs fin[b(t)] and upd[i] == t.  Every
+// wait points at an earlier step and CTAs walk the steps in order, so with
+// all CTAs co-resident (cooperative launch) the schedule cannot deadlock.
+// Sub-CTA 0 of a chunk group owns the critical chain (look-ahead + the next
+// row block); the others stream the remaining rows and may run ahead.
 template <bool TR, bool VEC>
-__device__ void sweep_body(SweepArgs& a, cg::grid_group& grid, double* s) {
+__device__ void sweep_body(SweepArgs& a, double* s) {
   const int G = gridDim.x, g = blockIdx.x;
   const int C = ceil_div(a.nrhs, CW);
   // chunk group of this CTA: one chunk if G >= C, else chunks g, g + G, ...
@@ -247,11 +300,14 @@ __device__ void sweep_body(SweepArgs& a, cg::grid_group& grid, double* s) {
   double* Xn = s + TILE;      // X_{b(t+1)} chunk (look-ahead)
   double* T0 = s + 2 * TILE;  // operator stage 0
   double* T1 = s + 3 * TILE;  // operator stage 1
+  auto upd = [&](int blk, int c) { return a.upd + (size_t)blk * C + c; };
+  auto fin = [&](int blk, int c) { return a.fin + (size_t)blk * C + c; };
+  const int c_first = G >= C ? g % C : g, c_step = G >= C ? C : G;
 
   // prologue: the first block of the sweep is final after D
   if (sub == 0) {
     const int b0 = blk_at(a, 0);
-    for (int c = g; c < C; c += G) {
+    for (int c = c_first; c < C; c += c_step) {
       cp_op<VEC>(op_ptr(a, b0, 1), T0);
       cp_x<VEC>(a, b0, c * CW, Xt);
       cp_async_commit();
@@ -262,22 +318,27 @@ __device__ void sweep_body(SweepArgs& a, cg::grid_group& grid, double* s) {
       tile_mma<false>(acc, T0, Xt, 1.0, 1.0);
       acc_store<VEC>(a, b0, c * CW, acc);
       __syncthreads();
+      publish(fin(b0, c), 1);
     }
   }
-  grid.sync();
 
   for (int t = 0; t < a.nblk; ++t) {
     const int bt = blk_at(a, t);
     const bool ahead = t + 1 < a.nblk;
-    const int R = max(0, a.nblk - t - 2);  // pending row blocks
-    // units: [0, 2) = look-ahead (weight of two products), then one per pending row block
+    const int R = max(0, a.nblk - t - 2);  // pending row blocks b(t+2) ...
+    // units: [0, 2) = look-ahead (weight of two products), then one per
+    // pending row block; sub-CTA s takes units [s*U/S, (s+1)*U/S), so sub 0
+    // holds the look-ahead and the nearest rows (the critical chain)
     const int U = R + (ahead ? 2 : 0), u_off = ahead ? 2 : 0;
     const int ub = (int)((long long)sub * U / S), ue = (int)((long long)(sub + 1) * U / S);
-    const bool do_ahead = ahead && ub == 0 && ue > 0;
     const int qb = max(ub - u_off, 0), qe = max(ue - u_off, 0);
-    for (int c = (G >= C ? g % C : g); c < C; c += (G >= C ? C : G)) {
+    const bool do_ahead = ahead && ub == 0 && ue > 0;
+    if (!do_ahead && qb >= qe) continue;
+    for (int c = c_first; c < C; c += c_step) {
       const int c0 = c * CW;
-      if (!do_ahead && qb >= qe) break;
+      if (threadIdx.x == 0) wait_ge(fin(bt, c), 1);
+      if (do_ahead && threadIdx.x == 32) wait_ge(upd(blk_at(a, t + 1), c), t);
+      __syncthreads();
       cp_x<VEC>(a, bt, c0, Xt);
       if (do_ahead) {
         const int bn = blk_at(a, t + 1);
@@ -293,8 +354,12 @@ __device__ void sweep_body(SweepArgs& a, cg::grid_group& grid, double* s) {
         tile_mma<false>(acc, T1, Xt, -1.0, -1.0);
         acc_store<VEC>(a, bn, c0, acc);
         __syncthreads();
+        publish(fin(bn, c), 1);
       }
       if (qb < qe) {
+        // the rows' previous-step updates
+        for (int q = qb + threadIdx.x; q < qe; q += TT) wait_ge(upd(blk_at(a, t + 2 + q), c), t);
+        __syncthreads();
         Acc cur, nxt;
         cp_m<VEC>(a, blk_at(a, t + 2 + qb), bt, T0);
         cp_async_commit();
@@ -317,9 +382,15 @@ __device__ void sweep_body(SweepArgs& a, cg::grid_group& grid, double* s) {
           acc_store<VEC>(a, rb, c0, cur);
           __syncthreads();
         }
+        // one fence for the CTA's rows of this step, then the counters
+        if (threadIdx.x == 0) {
+          __threadfence();
+          for (int q = qb; q < qe; ++q) st_relaxed(upd(blk_at(a, t + 2 + q), c), t + 1);
+        }
       }
+      cp_async_wait<0>();
+      __syncthreads();  // Xt is restaged by the next chunk / step
     }
-    grid.sync();
   }
 }
 
@@ -328,8 +399,7 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
   extern __shared__ __align__(16) double s[];
   SweepArgs a = a0;
   offset_item(a, blockIdx.y);
-  cg::grid_group grid = cg::this_grid();
-  sweep_body<TR, VEC>(a, grid, s);
+  sweep_body<TR, VEC>(a, s);
 }
 
 // Per (block, variant): D_v (the variant's diagonal inverse, conj-transposed for
@@ -440,6 +510,28 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
   int G = std::min(cap, want);
   if (G > C) G -= G % C;
   G = std::max(G, 1);
+  // dataflow counters (upd, fin), zeroed on the stream before the sweep
+  const size_t cnt = (size_t)2 * count * a.nblk * C;
+  int* ctr = nullptr;
+  {
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, std::pair<int*, size_t>> bufs;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& b = bufs[st];
+    if (b.second < cnt) {
+      if (b.first) cudaFree(b.first);
+      b.first = nullptr;
+      b.second = 0;
+      cudaError_t e = cudaMalloc(&b.first, cnt * sizeof(int));
+      if (e != cudaSuccess) return e;
+      b.second = cnt;
+    }
+    ctr = b.first;
+  }
+  cudaError_t e = cudaMemsetAsync(ctr, 0, cnt * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  a.upd = ctr;
+  a.fin = ctr + cnt / 2;
   void* args[] = {&a};
   count_launch();
   return cudaLaunchCooperativeKernel(fn, dim3(G, count), dim3(TT), args, smem, st);

@@ -10,7 +10,7 @@ ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Met
 gi = hdr.index("Grid Size") if "Grid Size" in hdr else None
 agg = collections.defaultdict(lambda: [0, 0.0])
 tot = 0.0
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 for r in rows[h + 1:]:
     if len(r) <= vi:
         continue
