@@ -128,17 +128,24 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
           bi[t] = sb * bs[BE + sB];
         }
       }
+      // all first products, then the dependent second ones: 32 independent
+      // accumulator chains between two DMMAs on the same accumulator
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           dmma(accr[a][b][0], accr[a][b][1], ar[a], br[b]);
-          if (CPLX) {
+          if (CPLX) dmma(acci[a][b][0], acci[a][b][1], ar[a], bi[b]);
+        }
+      if (CPLX) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
             dmma(accr[a][b][0], accr[a][b][1], nai[a], bi[b]);
-            dmma(acci[a][b][0], acci[a][b][1], ar[a], bi[b]);
             dmma(acci[a][b][0], acci[a][b][1], ai[a], br[b]);
           }
-        }
+      }
     }
   }
   cp_async_wait<0>();
