@@ -179,6 +179,26 @@ int fb_band_solve(fb_ctx* ctx, int n, int kl, int nrhs,
                   const double* fact_re, const double* fact_im, const int* ipiv,
                   int adjoint, double* x_re, double* x_im, int64_t ldx);
 
+/* Partitioned (SPIKE) band path, batched over count shifts (count <= 64,
+ * 1 <= kl <= 16).  Replaces the per-shift _BandedOps.factorize / solve
+ * (banded.py:156-170) for the whole contour: the band is cut into partitions
+ * factored independently (pivoting inside partitions) and coupled through a
+ * small interface system.  Per shift b: fact (3kl+1) x n planar at
+ * fact + b*fact_stride, ipiv[n] at ipiv + b*ipiv_stride, aux at
+ * aux + b*aux_stride (fb_band_aux_doubles(n, kl) doubles). */
+int64_t fb_band_aux_doubles(int n, int kl);
+int fb_band_factor_batched(fb_ctx* ctx, int count, int n, int kl, const double* z_re, const double* z_im,
+                           const double* fa_re, const double* fa_im,
+                           const double* fb_re, const double* fb_im, int64_t ldb,
+                           double* fact_re, double* fact_im, int64_t fact_stride,
+                           int* ipiv, int64_t ipiv_stride, double* aux, int64_t aux_stride, int* info);
+/* In place: X_b <- S(z_b)^-1 X_b (direct solve only; the Hermitian banded
+ * driver serves A^H solves from the factor of conj(z), S(z)^H = S(conj z)). */
+int fb_band_solve_batched(fb_ctx* ctx, int count, int n, int kl, int nrhs,
+                          const double* fact_re, const double* fact_im, int64_t fact_stride,
+                          const int* ipiv, int64_t ipiv_stride, const double* aux, int64_t aux_stride,
+                          double* x_re, double* x_im, int64_t ldx, int64_t x_stride);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,11 @@ SIGNATURES = {
     "fb_band_matvec": (c_int, [P, c_int, c_int, c_int, P, P, c_int64, P, P, c_int64, P, P, c_int64]),
     "fb_band_factor": (c_int, [P, c_int, c_int, c_double, c_double, P, P, P, P, c_int64, P, P, P, P]),
     "fb_band_solve": (c_int, [P, c_int, c_int, c_int, P, P, P, c_int, P, P, c_int64]),
+    "fb_band_aux_doubles": (c_int64, [c_int, c_int]),
+    "fb_band_factor_batched": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P, P, c_int64, P, P, c_int64,
+                                       P, c_int64, P, c_int64, P]),
+    "fb_band_solve_batched": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
+                                      P, P, c_int64, c_int64]),
 }
 
 FB_OK, FB_ERR_ALLOC, FB_ERR_SINGULAR, FB_ERR_REDUCED, FB_ERR_ARG, FB_ERR_CUDA = 0, -1, -2, -3, -10, -11

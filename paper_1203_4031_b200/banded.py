@@ -8,8 +8,11 @@ device through libfeastb200.so.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
+from . import _lib
 from ._driver import SolverOptions, run_rci
 from ._errors import SingularMatrixError
 from .device import Planar, get_device
@@ -61,24 +64,119 @@ def pad_band(fb, kl_from: int, kl_to: int):
 
 
 class _BandFactor:
-    __slots__ = ("z", "w", "ipiv", "info")
+    """A factored shift.  Sequential path: (w, ipiv) own arrays.  Partitioned
+    path: (batch, idx) into a _BandBatch; ``adj`` is the factor of conj(z)
+    that serves A^H solves of Hermitian pencils (S(z)^H = S(conj z))."""
 
-    def __init__(self, z, w, ipiv, info):
+    __slots__ = ("z", "w", "ipiv", "info", "batch", "idx", "adj")
+
+    def __init__(self, z, w=None, ipiv=None, info=None, batch=None, idx=0, adj=None):
         self.z, self.w, self.ipiv, self.info = z, w, ipiv, info
+        self.batch, self.idx, self.adj = batch, idx, adj
+
+
+class _BandBatch:
+    """count partitioned (SPIKE) factors: fact (2, count, (3kl+1) n),
+    ipiv (count, n), aux (count, fb_band_aux_doubles(n, kl)), info (count)."""
+
+    def __init__(self, dev, n, kl, count):
+        t = dev.torch
+        self.count, self.n, self.kl = count, n, kl
+        self.lw = (3 * kl + 1) * n
+        self.auxd = int(dev.lib.fb_band_aux_doubles(n, kl))
+        self.fact = t.empty((2, count, self.lw), dtype=t.float64, device=dev.tdev)
+        self.ipiv = t.empty((count, max(n, 1)), dtype=t.int32, device=dev.tdev)
+        self.aux = t.empty((count, self.auxd), dtype=t.float64, device=dev.tdev)
+        self.info = t.empty(count, dtype=t.int32, device=dev.tdev)
+        self.zs = [None] * count
+
+    def args(self, i0=0):
+        return (self.fact[0, i0].data_ptr(), self.fact[1, i0].data_ptr(), self.lw,
+                self.ipiv[i0].data_ptr(), self.ipiv.shape[1], self.aux[i0].data_ptr(), self.auxd)
+
+    @staticmethod
+    def nbytes(dev, n, kl, count):
+        return count * (8 * (2 * (3 * kl + 1) * n + int(dev.lib.fb_band_aux_doubles(n, kl))) + 4 * n)
 
 
 class DeviceBandOps:
-    """Device backend for the banded drivers (banded.py:149-178)."""
+    """Device backend for the banded drivers (banded.py:149-178).
+
+    For 1 <= kl <= 16 the shifts are factored together by the partitioned
+    band LU (fb_band_factor_batched) and each contour pass solves every
+    resident shift in one batched call (fb_band_solve_batched); larger
+    bandwidths use the sequential per-shift kernels."""
 
     on_device = True
 
-    def __init__(self, dev, FA: Planar, FB: Planar | None, kl: int, hermitian: bool):
+    def __init__(self, dev, FA: Planar, FB: Planar | None, kl: int, hermitian: bool, cache_bytes=None):
         self.dev, self.FA, self.FB, self.kl, self.hermitian = dev, FA, FB, kl, hermitian
         self.n = FA.cols
         self.factorizations = 0
+        self.partitioned = int(dev.lib.fb_band_aux_doubles(self.n, kl)) > 0 if self.n > 0 else False
+        if cache_bytes is None:
+            free, _ = dev.torch.cuda.mem_get_info(dev.tdev)
+            cache_bytes = int(0.85 * free)
+        self.cache_left = cache_bytes
+        self._batches = []
+        self._pass = {}
+
+    # -- factorization ---------------------------------------------------------------
+    def _factor_batch(self, bb, zs):
+        dev, n, kl = self.dev, self.n, self.kl
+        cnt = len(zs)
+        zr = (ctypes.c_double * cnt)(*[z.real for z in zs])
+        zi = (ctypes.c_double * cnt)(*[z.imag for z in zs])
+        FA, FB = self.FA, self.FB
+        fr, fi, fs, piv, ps, aux, as_ = bb.args()
+        dev.check(dev.lib.fb_band_factor_batched(
+            dev.h, cnt, n, kl, zr, zi, FA.re, FA.im, FB.re if FB is not None else None,
+            FB.im if FB is not None else None, FA.ld, fr, fi, fs, piv, ps, aux, as_,
+            bb.info.data_ptr()), "band_factor_batched")
+        self.factorizations += cnt
+        bad = (ctypes.c_int * cnt)()
+        rc = dev.lib.fb_read_info_batched(dev.h, cnt, bb.info.data_ptr(), bad)
+        if rc not in (0, _lib.FB_ERR_SINGULAR):
+            dev.check(rc, "read_info")
+        for i, z in enumerate(zs):
+            if bad[i] >= 0:
+                raise SingularMatrixError(f"zero pivot at band column {bad[i]} (shift {z})")
+            bb.zs[i] = z
+
+    def prefactorize(self, zs):
+        """All shifts (and conj shifts for Hermitian pencils) in batched calls."""
+        zs = [complex(z) for z in zs]
+        if not self.partitioned:
+            return {z: self.factorize(z) for z in zs}
+        want = list(zs)
+        if self.hermitian:
+            want += [z.conjugate() for z in zs]
+        per = _BandBatch.nbytes(self.dev, self.n, self.kl, 1)
+        if per * len(want) > self.cache_left:
+            raise MemoryError("band factors exceed the device cache")
+        self.cache_left -= per * len(want)
+        made = {}
+        for c0 in range(0, len(want), 64):
+            chunk = want[c0:c0 + 64]
+            bb = _BandBatch(self.dev, self.n, self.kl, len(chunk))
+            self._factor_batch(bb, chunk)
+            self._batches.append(bb)
+            for i, z in enumerate(chunk):
+                made.setdefault(z, (bb, i))
+        out = {}
+        for z in zs:
+            bb, i = made[z]
+            adj = None
+            if self.hermitian:
+                ab, ai = made[z.conjugate()]
+                adj = _BandFactor(z.conjugate(), batch=ab, idx=ai)
+            out[z] = _BandFactor(z, batch=bb, idx=i, adj=adj)
+        return out
 
     def factorize(self, z):
         z = complex(z)
+        if self.partitioned:
+            return self.prefactorize([z])[z]
         dev, n, kl, torch = self.dev, self.n, self.kl, self.dev.torch
         w = dev.empty(n, 3 * kl + 1, True)     # column-major band working array
         ipiv = torch.empty(max(n, 1), dtype=torch.int32, device=dev.tdev)
@@ -94,7 +192,50 @@ class DeviceBandOps:
             raise SingularMatrixError(f"zero pivot at band column {bad}")
         return _BandFactor(z, w, ipiv, info)
 
+    # -- solves ----------------------------------------------------------------------
+    def solve_pass(self, Y: Planar, hermitian: bool):
+        """Every resident shift solved against this pass's Y in one call per batch
+        (A^H solves of Hermitian pencils are the direct solves of conj(z))."""
+        self._pass = {}
+        if not self.partitioned:
+            return
+        dev, n, m = self.dev, self.n, Y.cols
+        for bb in self._batches:
+            cnt = bb.count
+            X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+            X[0].copy_(Y.plane(0).unsqueeze(0).expand(cnt, n, m))
+            if Y.cplx:
+                X[1].copy_(Y.plane(1).unsqueeze(0).expand(cnt, n, m))
+            else:
+                X[1].zero_()
+            fr, fi, fs, piv, ps, aux, as_ = bb.args()
+            dev.check(dev.lib.fb_band_solve_batched(dev.h, cnt, n, self.kl, m, fr, fi, fs, piv, ps, aux, as_,
+                                                    X[0].data_ptr(), X[1].data_ptr(), m, n * m),
+                      "band_solve_batched")
+            for i in range(cnt):
+                self._pass[(id(bb), i)] = (X, i)
+
+    def _solve_batched(self, f, W: Planar):
+        hit = self._pass.get((id(f.batch), f.idx))
+        if hit is not None:
+            X, i = hit
+            W.plane(0).copy_(X[0, i][:, :W.cols])
+            W.plane(1).copy_(X[1, i][:, :W.cols])
+            return
+        dev = self.dev
+        fr, fi, fs, piv, ps, aux, as_ = f.batch.args(f.idx)
+        dev.check(dev.lib.fb_band_solve_batched(dev.h, 1, self.n, self.kl, W.cols, fr, fi, fs, piv, ps, aux, as_,
+                                                W.re, W.im, W.ld, 0), "band_solve_batched")
+
     def _solve(self, f, W: Planar, adjoint):
+        if f.batch is not None:
+            if adjoint:
+                if f.adj is None:
+                    raise AssertionError("adjoint band solve needs the conj(z) factor")
+                self._solve_batched(f.adj, W)
+            else:
+                self._solve_batched(f, W)
+            return
         dev = self.dev
         dev.check(dev.lib.fb_band_solve(dev.h, self.n, self.kl, W.cols, f.w.re, f.w.im,
                                         f.ipiv.data_ptr(), 1 if adjoint else 0, W.re, W.im, W.ld),

@@ -1,0 +1,821 @@
+// Partitioned (SPIKE) shifted band LU and multi-RHS solve (banded.py:68-146,
+// 156-164), batched over contour shifts.
+//
+// S = z*FB - FA (n x n, kl sub- and super-diagonals) is cut into P row/column
+// partitions.  With A_j the diagonal blocks, B_j / C_j the kl x kl couplings
+// to the next / previous partition,
+//     S = diag(A_j) * (I + spikes),  V_j = A_j^-1 [0; B_j],  W_j = A_j^-1 [C_j; 0].
+// Factor (once per shift):
+//   pfactor   every partition's band LU with partial pivoting inside the
+//             partition (dgbtf2 scheme, kv = 2kl), one warp per partition,
+//             the active (kl+1) x (2kl+1) window in shared memory;
+//   spikes    V_j, W_j by the partition solve with the 2kl coupling columns;
+//   rfactor   the interface system (unknowns y_i = (x_i^bottom, x_{i+1}^top),
+//             block tridiagonal with 2kl x 2kl blocks) by block LU; the pivot
+//             blocks are inverted by Gauss-Jordan with partial pivoting.
+// Solve (per contour pass):
+//   psolve    g = A_j^-1 f_j for every partition (one warp per partition and
+//             32 right-hand sides, lanes = columns, register windows);
+//   rsolve    interface values from the block LU (one CTA per shift and chunk);
+//   correct   x_j = g_j - V_j x_{j+1}^top - W_j x_{j-1}^bottom.
+// Every partition block of z*B - A is nonsingular for Im z != 0 (B HPD), so
+// pivoting inside partitions is enough.  The partitioned pivot order differs
+// from the reference's whole-band LU; results agree to rounding.
+//
+// Factor storage (per shift) is the reference's working array, COLUMN-major,
+// W[j*(3kl+1) + kv + i - j] = LU(i, j) (banded.py:68-103), pivots ipiv[j]
+// (global row index, inside the partition).  aux (per shift):
+//   spikes  [n][2kl] re | [n][2kl] im   (columns 0..kl-1: V, kl..2kl-1: W)
+//   Dinv    [P-1][2kl][2kl] re | im      inverse pivot blocks of the interface LU
+//   F       [P-1][kl][2kl] re | im       multipliers (top kl rows)
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <vector>
+
+#include "band.cuh"
+#include "common.cuh"
+
+namespace fb {
+
+namespace {
+
+constexpr int KLMAX = 16;
+constexpr int WPB = 4;  // warps per CTA in the per-partition kernels
+constexpr int WIN = (KLMAX + 1) * (2 * KLMAX + 1);
+
+struct Zs {
+  double r[64], i[64];
+};
+
+__host__ __device__ __forceinline__ int part_lo(int j, int n, int P) { return (int)((long long)j * n / P); }
+
+// S[r][c] of z*FB - FA inside partition [lo, hi) (zero outside it or the band),
+// with the rounding of band_shift_kernel (numpy order, banded.py:158-163)
+__device__ __forceinline__ void s_entry(int r, int c, int lo, int hi, int kl, double zr, double zi,
+                                        const double* far_, const double* fai, const double* fbr,
+                                        const double* fbi, long long ldb, double& vr, double& vi) {
+  vr = 0.0;
+  vi = 0.0;
+  const int s = r - c;
+  if (r < lo || r >= hi || c < lo || c >= hi || s > kl || s < -kl) return;
+  const long long o = (long long)(kl + s) * ldb + c;
+  const double ar = far_[o], ai = fai ? fai[o] : 0.0;
+  if (fbr) {
+    const double br = fbr[o], bi = fbi ? fbi[o] : 0.0;
+    const double pr = __dsub_rn(__dmul_rn(zr, br), __dmul_rn(zi, bi));
+    const double pi = __dadd_rn(__dmul_rn(zr, bi), __dmul_rn(zi, br));
+    vr = (0.0 - ar) + pr;
+    vi = (0.0 - ai) + pi;
+  } else {
+    vr = s == 0 ? (0.0 - ar) + zr : (0.0 - ar);
+    vi = s == 0 ? (0.0 - ai) + zi : (0.0 - ai);
+  }
+}
+
+struct PFArgs {
+  int n, kl, P;
+  Zs z;
+  const double *far_, *fai, *fbr, *fbi;
+  long long ldb;
+  double *wr, *wi;
+  long long sw;  // factor batch stride (doubles)
+  int* ipiv;
+  long long sp;
+  int* info;  // [count], INT_MAX = ok, else 1 + first zero-pivot column
+};
+
+// ---- partition band LU: one warp per (partition, shift) ------------------------
+__global__ void __launch_bounds__(WPB * 32) band_pfactor_kernel(PFArgs a) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int part = blockIdx.x * WPB + wid, k = blockIdx.y;
+  if (part >= a.P) return;
+  const int kl = a.kl, kv = 2 * kl, LW = 3 * kl + 1, RW = kl + 1, CW = 2 * kl + 1;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  __shared__ double swin[WPB][2][WIN];
+  double* xr = swin[wid][0];  // window, column-major by slot: x[cslot * RW + rslot]
+  double* xi = swin[wid][1];
+  double* Wr = a.wr + k * a.sw;
+  double* Wi = a.wi + k * a.sw;
+  int* ipiv = a.ipiv + k * a.sp;
+  const double zr = a.z.r[k], zi = a.z.i[k];
+  auto S = [&](int r, int c, double& vr, double& vi) {
+    s_entry(r, c, lo, hi, kl, zr, zi, a.far_, a.fai, a.fbr, a.fbi, a.ldb, vr, vi);
+  };
+  for (int e = lane; e < RW * CW; e += 32) {
+    const int ri = e % RW, ci = e / RW;
+    double vr, vi;
+    S(lo + ri, lo + ci, vr, vi);
+    xr[ci * RW + ri] = vr;
+    xi[ci * RW + ri] = vi;
+  }
+  int rb = 0, cb = 0;  // slots of row j / column j
+  int ju = lo, bad = 0;
+  for (int j = lo; j < hi; ++j) {
+    __syncwarp();
+    const int km = min(kl, hi - 1 - j);
+    auto RS = [&](int i) { const int s = rb + i; return s >= RW ? s - RW : s; };
+    auto CS = [&](int c) { const int s = cb + c; return s >= CW ? s - CW : s; };
+    const int c0 = CS(0) * RW;
+    // pivot: first row of max |.| among j..j+km (banded.py:79-84)
+    double best = -1.0;
+    int bi = 0;
+    if (lane <= km) {
+      best = hypot(xr[c0 + RS(lane)], xi[c0 + RS(lane)]);
+      bi = lane;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    int jp = bi;
+    if (!(best > 0.0)) {
+      if (!bad) bad = j + 1;
+      jp = 0;
+    }
+    if (lane == 0) ipiv[j] = j + jp;
+    ju = max(ju, min(j + kl + jp, hi - 1));
+    if (jp) {
+      const int sa = RS(0), sb = RS(jp);
+      for (int c = lane; c <= ju - j; c += 32) {
+        const int cs = CS(c) * RW;
+        double t = xr[cs + sa];
+        xr[cs + sa] = xr[cs + sb];
+        xr[cs + sb] = t;
+        t = xi[cs + sa];
+        xi[cs + sa] = xi[cs + sb];
+        xi[cs + sb] = t;
+      }
+    }
+    __syncwarp();
+    const double pr = xr[c0 + RS(0)], pim = xi[c0 + RS(0)];
+    const bool zero = !(pr != 0.0 || pim != 0.0);
+    if (km > 0 && !zero) {
+      const double den = pr * pr + pim * pim;
+      const double ir = pr / den, ii = -pim / den;
+      if (lane < km) {
+        const int s = c0 + RS(1 + lane);
+        const double x_r = xr[s], x_i = xi[s];
+        xr[s] = x_r * ir - x_i * ii;
+        xi[s] = x_r * ii + x_i * ir;
+      }
+      __syncwarp();
+      for (int c = lane; c < ju - j; c += 32) {  // column j+1+c -= l * u
+        const int cs = CS(1 + c) * RW;
+        const double ur = xr[cs + RS(0)], ui = xi[cs + RS(0)];
+        if (ur == 0.0 && ui == 0.0) continue;
+        for (int i = 0; i < km; ++i) {
+          const int s = RS(1 + i);
+          const double lr = xr[c0 + s], li = xi[c0 + s];
+          xr[cs + s] -= lr * ur - li * ui;
+          xi[cs + s] -= lr * ui + li * ur;
+        }
+      }
+    }
+    __syncwarp();
+    // row j of U (columns j..j+kv) and the multipliers of column j leave the window
+    for (int c = lane; c <= kv; c += 32) {
+      if (j + c < hi) {
+        const long long o = (long long)(j + c) * LW + kv - c;
+        Wr[o] = xr[CS(c) * RW + RS(0)];
+        Wi[o] = xi[CS(c) * RW + RS(0)];
+      }
+    }
+    if (lane < kl) {
+      const long long o = (long long)j * LW + kv + 1 + lane;
+      Wr[o] = lane < km ? xr[c0 + RS(1 + lane)] : 0.0;
+      Wi[o] = lane < km ? xi[c0 + RS(1 + lane)] : 0.0;
+    }
+    __syncwarp();
+    // slide: row j+kl+1 takes row j's slot, column j+2kl+1 takes column j's slot
+    const int rn = j + RW, cn = j + CW;
+    for (int c = lane; c < CW; c += 32) {
+      double vr, vi;
+      S(rn, j + 1 + c, vr, vi);
+      const int cs = CS(1 + c) * RW;  // c = kv wraps onto column j's slot (= column cn)
+      xr[cs + RS(0)] = vr;
+      xi[cs + RS(0)] = vi;
+    }
+    for (int i = lane; i < kl; i += 32) {
+      double vr, vi;
+      S(j + 1 + i, cn, vr, vi);
+      xr[c0 + RS(1 + i)] = vr;
+      xi[c0 + RS(1 + i)] = vi;
+    }
+    rb = RS(1);
+    cb = CS(1);
+  }
+  if (bad && lane == 0) atomicMin(a.info + k, bad);
+}
+
+// ---- partition solve (direct): one warp per (partition, 32 columns, shift) ----
+struct PSArgs {
+  int n, kl, P, nrhs;
+  const double *wr, *wi;
+  long long sw;
+  const int* ipiv;
+  long long sp;
+  double *xr, *xi;
+  long long ldx, sx;
+};
+
+template <int KL>
+__global__ void __launch_bounds__(WPB * 32) band_psolve_kernel(PSArgs a) {
+  constexpr int KV = 2 * KL, LW = 3 * KL + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int part = blockIdx.x * WPB + wid, chunk = blockIdx.y, k = blockIdx.z;
+  if (part >= a.P) return;
+  const int col = chunk * 32 + lane;
+  const bool on = col < a.nrhs;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  const double* Wr = a.wr + k * a.sw;
+  const double* Wi = a.wi + k * a.sw;
+  const int* ipiv = a.ipiv + k * a.sp;
+  double* Xr = a.xr + k * a.sx;
+  double* Xi = a.xi + k * a.sx;
+  auto ld = [&](int r, double& vr, double& vi) {
+    if (on && r < hi) {
+      const long long o = (long long)r * a.ldx + col;
+      vr = Xr[o];
+      vi = Xi[o];
+    } else {
+      vr = vi = 0.0;
+    }
+  };
+  // forward: pivots interleaved with unit L (rows j..j+KL live)
+  double wr_[KL + 1], wi_[KL + 1];
+#pragma unroll
+  for (int i = 0; i <= KL; ++i) ld(lo + i, wr_[i], wi_[i]);
+  for (int j = lo; j < hi; ++j) {
+    const int p = ipiv[j] - j;
+    if (p) {
+#pragma unroll
+      for (int i = 1; i <= KL; ++i)
+        if (i == p) {
+          const double tr = wr_[0], ti = wi_[0];
+          wr_[0] = wr_[i];
+          wi_[0] = wi_[i];
+          wr_[i] = tr;
+          wi_[i] = ti;
+        }
+    }
+    const double x0r = wr_[0], x0i = wi_[0];
+    const double* lr = Wr + (long long)j * LW + KV + 1;
+    const double* li = Wi + (long long)j * LW + KV + 1;
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {  // multipliers beyond the partition are stored as 0
+      const double ar = __ldg(lr + i), ai = __ldg(li + i);
+      wr_[1 + i] -= ar * x0r - ai * x0i;
+      wi_[1 + i] -= ar * x0i + ai * x0r;
+    }
+    if (on) {
+      const long long o = (long long)j * a.ldx + col;
+      Xr[o] = x0r;
+      Xi[o] = x0i;
+    }
+#pragma unroll
+    for (int i = 0; i < KL; ++i) {
+      wr_[i] = wr_[i + 1];
+      wi_[i] = wi_[i + 1];
+    }
+    ld(j + KL + 1, wr_[KL], wi_[KL]);
+  }
+  // backward: x_j = y_j / U_jj, then y[j-KV..j-1] -= U[., j] x_j (rows j-KV..j live)
+  double ur_[KV + 1], ui_[KV + 1];
+  auto ldb = [&](int r, double& vr, double& vi) {
+    if (on && r >= lo) {
+      const long long o = (long long)r * a.ldx + col;
+      vr = Xr[o];
+      vi = Xi[o];
+    } else {
+      vr = vi = 0.0;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i <= KV; ++i) ldb(hi - 1 - KV + i, ur_[i], ui_[i]);
+  for (int j = hi - 1; j >= lo; --j) {
+    const double* cr = Wr + (long long)j * LW;
+    const double* ci = Wi + (long long)j * LW;
+    const double dr = __ldg(cr + KV), di = __ldg(ci + KV);
+    const double den = dr * dr + di * di;
+    const double yr = ur_[KV], yi = ui_[KV];
+    const double qr = (yr * dr + yi * di) / den, qi = (yi * dr - yr * di) / den;
+#pragma unroll
+    for (int i = 0; i < KV; ++i) {  // U entries above the partition are stored as 0
+      const double br = __ldg(cr + i), bi = __ldg(ci + i);
+      ur_[i] -= br * qr - bi * qi;
+      ui_[i] -= br * qi + bi * qr;
+    }
+    if (on) {
+      const long long o = (long long)j * a.ldx + col;
+      Xr[o] = qr;
+      Xi[o] = qi;
+    }
+#pragma unroll
+    for (int i = KV; i > 0; --i) {
+      ur_[i] = ur_[i - 1];
+      ui_[i] = ui_[i - 1];
+    }
+    ldb(j - 1 - KV, ur_[0], ui_[0]);
+  }
+}
+
+// ---- spike right-hand sides: [0; B_j] in columns 0..kl-1, [C_j; 0] in kl..2kl-1 ----
+struct SIArgs {
+  int n, kl, P;
+  Zs z;
+  const double *far_, *fai, *fbr, *fbi;
+  long long ldb;
+  double *sr, *si;  // spike buffers [n][2kl]
+  long long ss;
+};
+
+__global__ void band_spike_init_kernel(SIArgs a) {
+  const int k = blockIdx.y, kl = a.kl, w = 2 * kl;
+  double* Sr = a.sr + k * a.ss;
+  double* Si = a.si + k * a.ss;
+  const double zr = a.z.r[k], zi = a.z.i[k];
+  const long long total = (long long)a.n * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / w), c = (int)(e % w);
+    // partition of row r
+    int j = (int)(((long long)r * a.P) / a.n);
+    while (j + 1 < a.P && part_lo(j + 1, a.n, a.P) <= r) ++j;
+    while (part_lo(j, a.n, a.P) > r) --j;
+    const int lo = part_lo(j, a.n, a.P), hi = part_lo(j + 1, a.n, a.P);
+    double vr = 0.0, vi = 0.0;
+    if (c < kl) {  // B_j: rows hi-kl..hi-1, columns hi..hi+kl-1 of S
+      if (j + 1 < a.P && r >= hi - kl) {
+        const int nhi = part_lo(j + 2, a.n, a.P);
+        s_entry(r, hi + c, 0, nhi, kl, zr, zi, a.far_, a.fai, a.fbr, a.fbi, a.ldb, vr, vi);
+      }
+    } else {  // C_j: rows lo..lo+kl-1, columns lo-kl..lo-1 of S
+      if (j > 0 && r < lo + kl) {
+        s_entry(r, lo - kl + (c - kl), 0, hi, kl, zr, zi, a.far_, a.fai, a.fbr, a.fbi, a.ldb, vr, vi);
+      }
+    }
+    Sr[e] = vr;
+    Si[e] = vi;
+  }
+}
+
+// ---- interface system: block LU, one CTA per shift ------------------------------
+// Block row i (interface between partitions i and i+1), unknowns y_i =
+// (x_i^b, x_{i+1}^t):  D_i = [[I, V_i^b], [W_{i+1}^t, I]],
+// L_i = [[W_i^b, 0], [0, 0]] (on y_{i-1}), U_i = [[0, 0], [0, V_{i+1}^t]] (on y_{i+1}).
+// D'_0 = D_0, F_i = L_i D'_{i-1}^-1 (top kl rows), D'_i = D_i - F_i U_{i-1}.
+struct RFArgs {
+  int n, kl, P;
+  const double *sr, *si;
+  long long ss;
+  double *dr, *di;  // Dinv [P-1][2kl][2kl]
+  double *fr, *fi;  // F    [P-1][kl][2kl]
+  long long sa;     // aux batch stride
+  int* info;
+};
+
+constexpr int RT = 256;
+constexpr int M2 = 2 * KLMAX;  // 32
+
+__global__ void __launch_bounds__(RT) band_rfactor_kernel(RFArgs a) {
+  const int k = blockIdx.x, kl = a.kl, w = 2 * kl, tid = threadIdx.x;
+  const double* Sr = a.sr + k * a.ss;
+  const double* Si = a.si + k * a.ss;
+  double* Dr = a.dr + k * a.sa;
+  double* Di = a.di + k * a.sa;
+  double* Fr = a.fr + k * a.sa;
+  double* Fi = a.fi + k * a.sa;
+  __shared__ double ar[M2][2 * M2 + 1], ai[M2][2 * M2 + 1];  // [D' | I] -> [I | D'^-1]
+  __shared__ double pinv[KLMAX][M2 + 1], pinvi[KLMAX][M2 + 1];  // top kl rows of the previous D'^-1
+  __shared__ int s_piv;
+  auto sp = [&](int row, int col, double& vr, double& vi) {  // spike buffer entry
+    const long long o = (long long)row * w + col;
+    vr = Sr[o];
+    vi = Si[o];
+  };
+  for (int i = 0; i + 1 < a.P; ++i) {
+    const int hi_i = part_lo(i + 1, a.n, a.P);  // first row of partition i+1
+    // D_i
+    for (int e = tid; e < w * w; e += RT) {
+      const int r = e / w, c = e % w;
+      double vr = (r == c) ? 1.0 : 0.0, vi = 0.0;
+      if (r < kl && c >= kl) sp(hi_i - kl + r, c - kl, vr, vi);            // V_i^b
+      else if (r >= kl && c < kl) sp(hi_i + (r - kl), kl + c, vr, vi);     // W_{i+1}^t
+      ar[r][c] = vr;
+      ai[r][c] = vi;
+      ar[r][w + c] = (r == c) ? 1.0 : 0.0;
+      ai[r][w + c] = 0.0;
+    }
+    __syncthreads();
+    if (i > 0) {
+      // F_i (top kl rows) = W_i^b * D'_{i-1}^-1[0:kl, :]
+      const int lo_i = part_lo(i, a.n, a.P);
+      for (int e = tid; e < kl * w; e += RT) {
+        const int r = e / w, c = e % w;
+        double s_r = 0.0, s_i = 0.0;
+        for (int q = 0; q < kl; ++q) {
+          double vr, vi;
+          sp(hi_i - kl + r, kl + q, vr, vi);  // W_i^b[r][q]
+          s_r += vr * pinv[q][c] - vi * pinvi[q][c];
+          s_i += vr * pinvi[q][c] + vi * pinv[q][c];
+        }
+        Fr[(long long)(i * kl + r) * w + c] = s_r;
+        Fi[(long long)(i * kl + r) * w + c] = s_i;
+      }
+      __syncthreads();
+      // D'_i[0:kl, kl:2kl] -= F_i[:, kl:2kl] V_i^t
+      for (int e = tid; e < kl * kl; e += RT) {
+        const int r = e / kl, c = e % kl;
+        double s_r = 0.0, s_i = 0.0;
+        for (int q = 0; q < kl; ++q) {
+          double vr, vi;
+          sp(lo_i + q, c, vr, vi);  // V_i^t[q][c]
+          const double f_r = Fr[(long long)(i * kl + r) * w + kl + q];
+          const double f_i = Fi[(long long)(i * kl + r) * w + kl + q];
+          s_r += f_r * vr - f_i * vi;
+          s_i += f_r * vi + f_i * vr;
+        }
+        ar[r][kl + c] -= s_r;
+        ai[r][kl + c] -= s_i;
+      }
+      __syncthreads();
+    }
+    // Gauss-Jordan with partial pivoting on [D' | I]
+    for (int p = 0; p < w; ++p) {
+      if (tid < 32) {
+        double best = -1.0;
+        int bi = p;
+        const int r = p + tid;
+        if (r < w) {
+          best = hypot(ar[r][p], ai[r][p]);
+          bi = r;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) {
+            best = ov;
+            bi = oi;
+          }
+        }
+        if (tid == 0) {
+          s_piv = bi;
+          if (!(best > 0.0)) atomicMin(a.info + k, INT_MAX - 1);
+        }
+      }
+      __syncthreads();
+      const int q = s_piv;
+      if (q != p)
+        for (int c = tid; c < 2 * w; c += RT) {
+          double t = ar[p][c];
+          ar[p][c] = ar[q][c];
+          ar[q][c] = t;
+          t = ai[p][c];
+          ai[p][c] = ai[q][c];
+          ai[q][c] = t;
+        }
+      __syncthreads();
+      const double pr = ar[p][p], pim = ai[p][p];
+      const double den = pr * pr + pim * pim;
+      const double ir = den > 0.0 ? pr / den : 0.0, ii = den > 0.0 ? -pim / den : 0.0;
+      __syncthreads();
+      for (int c = tid; c < 2 * w; c += RT) {  // scale row p
+        const double x_r = ar[p][c], x_i = ai[p][c];
+        ar[p][c] = x_r * ir - x_i * ii;
+        ai[p][c] = x_r * ii + x_i * ir;
+      }
+      __syncthreads();
+      for (int e = tid; e < w * 2 * w; e += RT) {  // eliminate column p elsewhere
+        const int r = e / (2 * w), c = e % (2 * w);
+        if (r == p) continue;
+        const double fr2 = ar[r][p], fi2 = ai[r][p];
+        if (c == p) continue;
+        ar[r][c] -= fr2 * ar[p][c] - fi2 * ai[p][c];
+        ai[r][c] -= fr2 * ai[p][c] + fi2 * ar[p][c];
+      }
+      __syncthreads();
+      for (int r = tid; r < w; r += RT)
+        if (r != p) {
+          ar[r][p] = 0.0;
+          ai[r][p] = 0.0;
+        }
+      __syncthreads();
+    }
+    for (int e = tid; e < w * w; e += RT) {
+      const int r = e / w, c = e % w;
+      if (r < kl) {
+        pinv[r][c] = ar[r][w + c];
+        pinvi[r][c] = ai[r][w + c];
+      }
+      Dr[(long long)i * w * w + e] = ar[r][w + c];
+      Di[(long long)i * w * w + e] = ai[r][w + c];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- interface solve: one CTA per (shift, 32-column chunk) ------------------------
+struct RSArgs {
+  int n, kl, P, nrhs;
+  const double *sr, *si;
+  long long ss;
+  const double *dr, *di, *fr, *fi;
+  long long sa;
+  const double *xr, *xi;  // g (after the partition solves)
+  long long ldx, sx;
+  double *yr, *yi;  // interface values [count][P-1][2kl][nrhs]
+  long long sy;
+};
+
+__global__ void __launch_bounds__(RT) band_rsolve_kernel(RSArgs a) {
+  const int k = blockIdx.x, chunk = blockIdx.y, kl = a.kl, w = 2 * kl, tid = threadIdx.x;
+  const int c0 = chunk * 32, nc = min(32, a.nrhs - c0);
+  const double* Sr = a.sr + k * a.ss;
+  const double* Si = a.si + k * a.ss;
+  const double* Dr = a.dr + k * a.sa;
+  const double* Di = a.di + k * a.sa;
+  const double* Fr = a.fr + k * a.sa;
+  const double* Fi = a.fi + k * a.sa;
+  const double* Xr = a.xr + k * a.sx;
+  const double* Xi = a.xi + k * a.sx;
+  double* Yr = a.yr + k * a.sy;
+  double* Yi = a.yi + k * a.sy;
+  __shared__ double zr[M2][33], zi[M2][33], pr_[M2][33], pi_[M2][33];
+  auto yo = [&](int i, int r, int c) { return ((long long)i * w + r) * a.nrhs + c0 + c; };
+  // forward: z_i = r_i - F_i z_{i-1} (top kl rows)
+  for (int i = 0; i + 1 < a.P; ++i) {
+    const int hi_i = part_lo(i + 1, a.n, a.P);
+    for (int e = tid; e < w * nc; e += RT) {
+      const int r = e / nc, c = e % nc;
+      const int row = r < kl ? hi_i - kl + r : hi_i + (r - kl);
+      const long long o = (long long)row * a.ldx + c0 + c;
+      double vr = Xr[o], vi = Xi[o];
+      if (i > 0 && r < kl) {
+        for (int q = 0; q < w; ++q) {
+          const double f_r = Fr[(long long)(i * kl + r) * w + q], f_i = Fi[(long long)(i * kl + r) * w + q];
+          vr -= f_r * pr_[q][c] - f_i * pi_[q][c];
+          vi -= f_r * pi_[q][c] + f_i * pr_[q][c];
+        }
+      }
+      zr[r][c] = vr;
+      zi[r][c] = vi;
+    }
+    __syncthreads();
+    for (int e = tid; e < w * nc; e += RT) {
+      const int r = e / nc, c = e % nc;
+      pr_[r][c] = zr[r][c];
+      pi_[r][c] = zi[r][c];
+      Yr[yo(i, r, c)] = zr[r][c];
+      Yi[yo(i, r, c)] = zi[r][c];
+    }
+    __syncthreads();
+  }
+  // backward: y_i = D'^-1_i (z_i - (0; V_{i+1}^t y_{i+1}[kl:]))
+  for (int i = a.P - 2; i >= 0; --i) {
+    const int hi_i = part_lo(i + 1, a.n, a.P);
+    for (int e = tid; e < w * nc; e += RT) {
+      const int r = e / nc, c = e % nc;
+      double vr = Yr[yo(i, r, c)], vi = Yi[yo(i, r, c)];
+      if (r >= kl && i + 2 < a.P) {
+        for (int q = 0; q < kl; ++q) {  // V_{i+1}^t[r-kl][q] * y_{i+1}[kl+q]
+          const long long o = (long long)(hi_i + (r - kl)) * w + q;
+          const double v_r = Sr[o], v_i = Si[o];
+          vr -= v_r * pr_[kl + q][c] - v_i * pi_[kl + q][c];
+          vi -= v_r * pi_[kl + q][c] + v_i * pr_[kl + q][c];
+        }
+      }
+      zr[r][c] = vr;
+      zi[r][c] = vi;
+    }
+    __syncthreads();
+    for (int e = tid; e < w * nc; e += RT) {
+      const int r = e / nc, c = e % nc;
+      double vr = 0.0, vi = 0.0;
+      for (int q = 0; q < w; ++q) {
+        const double d_r = Dr[(long long)i * w * w + r * w + q], d_i = Di[(long long)i * w * w + r * w + q];
+        vr += d_r * zr[q][c] - d_i * zi[q][c];
+        vi += d_r * zi[q][c] + d_i * zr[q][c];
+      }
+      pr_[r][c] = vr;
+      pi_[r][c] = vi;
+    }
+    __syncthreads();
+    for (int e = tid; e < w * nc; e += RT) {
+      const int r = e / nc, c = e % nc;
+      Yr[yo(i, r, c)] = pr_[r][c];
+      Yi[yo(i, r, c)] = pi_[r][c];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- correction x_j = g_j - V_j x_{j+1}^t - W_j x_{j-1}^b -----------------------
+struct CKArgs {
+  int n, kl, P, nrhs;
+  const double *sr, *si;
+  long long ss;
+  const double *yr, *yi;
+  long long sy;
+  double *xr, *xi;
+  long long ldx, sx;
+};
+
+template <int KL>
+__global__ void __launch_bounds__(WPB * 32) band_correct_kernel(CKArgs a) {
+  constexpr int W2 = 2 * KL;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int part = blockIdx.x * WPB + wid, chunk = blockIdx.y, k = blockIdx.z;
+  if (part >= a.P) return;
+  const int col = chunk * 32 + lane;
+  if (col >= a.nrhs) return;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  const double* Sr = a.sr + k * a.ss;
+  const double* Si = a.si + k * a.ss;
+  const double* Yr = a.yr + k * a.sy;
+  const double* Yi = a.yi + k * a.sy;
+  double* Xr = a.xr + k * a.sx;
+  double* Xi = a.xi + k * a.sx;
+  double tr[W2], ti[W2];  // (x_{j+1}^t, x_{j-1}^b)
+#pragma unroll
+  for (int q = 0; q < KL; ++q) {
+    const bool nx = part + 1 < a.P, pv = part > 0;
+    const long long on = ((long long)part * W2 + KL + q) * a.nrhs + col;        // y_part[kl + q]
+    const long long op = ((long long)(part - 1) * W2 + q) * a.nrhs + col;       // y_{part-1}[q]
+    tr[q] = nx ? Yr[on] : 0.0;
+    ti[q] = nx ? Yi[on] : 0.0;
+    tr[KL + q] = pv ? Yr[op] : 0.0;
+    ti[KL + q] = pv ? Yi[op] : 0.0;
+  }
+  for (int r = lo; r < hi; ++r) {
+    const double* sr = Sr + (long long)r * W2;
+    const double* si = Si + (long long)r * W2;
+    double ar = 0.0, ai = 0.0;
+#pragma unroll
+    for (int q = 0; q < W2; ++q) {
+      const double vr = __ldg(sr + q), vi = __ldg(si + q);
+      ar += vr * tr[q] - vi * ti[q];
+      ai += vr * ti[q] + vi * tr[q];
+    }
+    const long long o = (long long)r * a.ldx + col;
+    Xr[o] -= ar;
+    Xi[o] -= ai;
+  }
+}
+
+using PsFn = void (*)(PSArgs);
+using CkFn = void (*)(CKArgs);
+#define FB_KL_TABLE(kern, T) \
+  static const T tbl[KLMAX + 1] = {nullptr, kern<1>, kern<2>, kern<3>, kern<4>, kern<5>, kern<6>, kern<7>, \
+                                   kern<8>, kern<9>, kern<10>, kern<11>, kern<12>, kern<13>, kern<14>,   \
+                                   kern<15>, kern<16>};
+
+PsFn psolve_fn(int kl) {
+  FB_KL_TABLE(band_psolve_kernel, PsFn)
+  return tbl[kl];
+}
+CkFn correct_fn(int kl) {
+  FB_KL_TABLE(band_correct_kernel, CkFn)
+  return tbl[kl];
+}
+
+int g_part_target = 0;
+
+}  // namespace
+
+void band_spike_set_part_target(int t) { g_part_target = t; }
+
+int band_spike_parts(int n, int kl) {
+  if (g_part_target == 0) {
+    const char* e = getenv("FB_BAND_PART");
+    g_part_target = e && atoi(e) > 0 ? atoi(e) : 4096;
+  }
+  const int minsz = std::max(2 * kl + 1, std::min(64, g_part_target));
+  int P = (n + g_part_target - 1) / g_part_target;
+  P = std::min(P, std::max(1, n / std::max(1, minsz)));
+  return std::max(1, P);
+}
+
+bool band_spike_ok(int kl) { return kl >= 1 && kl <= KLMAX; }
+
+size_t band_spike_aux_doubles(int n, int kl) {
+  const int P = band_spike_parts(n, kl);
+  return (size_t)4 * kl * n + (size_t)12 * kl * kl * (P > 1 ? P - 1 : 0) + 64;
+}
+
+size_t band_spike_solve_scratch_doubles(int n, int kl, int nrhs, int count) {
+  const int P = band_spike_parts(n, kl);
+  return (size_t)count * (P > 1 ? P - 1 : 0) * 2 * kl * nrhs * 2 + 64;
+}
+
+// aux pointers of item base
+static void aux_ptrs(int n, int kl, double* aux, double** sr, double** si, double** dr, double** di, double** fr,
+                     double** fi) {
+  const int P = band_spike_parts(n, kl);
+  const size_t ns = (size_t)2 * kl * n, nd = (size_t)4 * kl * kl * (P > 1 ? P - 1 : 0),
+               nf = (size_t)2 * kl * kl * (P > 1 ? P - 1 : 0);
+  *sr = aux;
+  *si = aux + ns;
+  *dr = aux + 2 * ns;
+  *di = *dr + nd;
+  *fr = *di + nd;
+  *fi = *fr + nf;
+}
+
+cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const double* zi, const double* far_,
+                              const double* fai, const double* fbr, const double* fbi, long long ldb,
+                              double* wr, double* wi, long long sw, int* ipiv, long long sp, double* aux,
+                              long long sa, int* info, cudaStream_t st) {
+  if (n <= 0 || count <= 0) return cudaSuccess;
+  if (count > 64 || !band_spike_ok(kl)) return cudaErrorInvalidValue;
+  const int P = band_spike_parts(n, kl);
+  cudaError_t e;
+  // zero factor arrays (entries outside the partitions are never written)
+  for (int k = 0; k < count; ++k) {
+    if ((e = cudaMemsetAsync(wr + k * sw, 0, sizeof(double) * band_fact_doubles(n, kl), st))) return e;
+    if ((e = cudaMemsetAsync(wi + k * sw, 0, sizeof(double) * band_fact_doubles(n, kl), st))) return e;
+  }
+  std::vector<int> big(count, INT_MAX);
+  if ((e = cudaMemcpyAsync(info, big.data(), sizeof(int) * count, cudaMemcpyHostToDevice, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;  // host vector lifetime
+  PFArgs pa{};
+  pa.n = n; pa.kl = kl; pa.P = P;
+  for (int k = 0; k < count; ++k) {
+    pa.z.r[k] = zr[k];
+    pa.z.i[k] = zi[k];
+  }
+  pa.far_ = far_; pa.fai = fai; pa.fbr = fbr; pa.fbi = fbi; pa.ldb = ldb;
+  pa.wr = wr; pa.wi = wi; pa.sw = sw; pa.ipiv = ipiv; pa.sp = sp; pa.info = info;
+  band_pfactor_kernel<<<dim3(ceil_div(P, WPB), count), WPB * 32, 0, st>>>(pa);
+  count_launch();
+  if ((e = cudaGetLastError())) return e;
+  if (P == 1) return cudaSuccess;
+  double *sr, *si, *dr, *di, *fr, *fi;
+  aux_ptrs(n, kl, aux, &sr, &si, &dr, &di, &fr, &fi);
+  SIArgs s{};
+  s.n = n; s.kl = kl; s.P = P; s.z = pa.z;
+  s.far_ = far_; s.fai = fai; s.fbr = fbr; s.fbi = fbi; s.ldb = ldb;
+  s.sr = sr; s.si = si; s.ss = sa;
+  const long long tot = (long long)n * 2 * kl;
+  band_spike_init_kernel<<<dim3((int)std::min<long long>((tot + 255) / 256, 8 * kSMs), count), 256, 0, st>>>(s);
+  count_launch();
+  if ((e = cudaGetLastError())) return e;
+  PSArgs ps{};
+  ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = 2 * kl;
+  ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
+  ps.xr = sr; ps.xi = si; ps.ldx = 2 * kl; ps.sx = sa;
+  psolve_fn(kl)<<<dim3(ceil_div(P, WPB), 1, count), WPB * 32, 0, st>>>(ps);
+  count_launch();
+  if ((e = cudaGetLastError())) return e;
+  RFArgs rf{};
+  rf.n = n; rf.kl = kl; rf.P = P;
+  rf.sr = sr; rf.si = si; rf.ss = sa;
+  rf.dr = dr; rf.di = di; rf.fr = fr; rf.fi = fi; rf.sa = sa; rf.info = info;
+  band_rfactor_kernel<<<count, RT, 0, st>>>(rf);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* wr, const double* wi, long long sw,
+                             const int* ipiv, long long sp, const double* aux, long long sa, double* xr,
+                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st) {
+  if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
+  if (!band_spike_ok(kl)) return cudaErrorInvalidValue;
+  const int P = band_spike_parts(n, kl);
+  const int chunks = ceil_div(nrhs, 32);
+  PSArgs ps{};
+  ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = nrhs;
+  ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
+  ps.xr = xr; ps.xi = xi; ps.ldx = ldx; ps.sx = sx;
+  psolve_fn(kl)<<<dim3(ceil_div(P, WPB), chunks, count), WPB * 32, 0, st>>>(ps);
+  count_launch();
+  cudaError_t e;
+  if ((e = cudaGetLastError())) return e;
+  if (P == 1) return cudaSuccess;
+  double *sr, *si, *dr, *di, *fr, *fi;
+  aux_ptrs(n, kl, const_cast<double*>(aux), &sr, &si, &dr, &di, &fr, &fi);
+  const long long sy = (long long)(P - 1) * 2 * kl * nrhs;
+  RSArgs rs{};
+  rs.n = n; rs.kl = kl; rs.P = P; rs.nrhs = nrhs;
+  rs.sr = sr; rs.si = si; rs.ss = sa; rs.dr = dr; rs.di = di; rs.fr = fr; rs.fi = fi; rs.sa = sa;
+  rs.xr = xr; rs.xi = xi; rs.ldx = ldx; rs.sx = sx;
+  rs.yr = scratch; rs.yi = scratch + count * sy; rs.sy = sy;
+  band_rsolve_kernel<<<dim3(count, chunks), RT, 0, st>>>(rs);
+  count_launch();
+  if ((e = cudaGetLastError())) return e;
+  CKArgs ck{};
+  ck.n = n; ck.kl = kl; ck.P = P; ck.nrhs = nrhs;
+  ck.sr = sr; ck.si = si; ck.ss = sa; ck.yr = rs.yr; ck.yi = rs.yi; ck.sy = sy;
+  ck.xr = xr; ck.xi = xi; ck.ldx = ldx; ck.sx = sx;
+  correct_fn(kl)<<<dim3(ceil_div(P, WPB), chunks, count), WPB * 32, 0, st>>>(ck);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace fb

@@ -386,6 +386,45 @@ int fb_band_solve(fb_ctx* c, int n, int kl, int nrhs, const double* fr, const do
                  "band_solve");
 }
 
+int64_t fb_band_aux_doubles(int n, int kl) {
+  if (n <= 0 || !fb::band_spike_ok(kl)) return 0;
+  return (int64_t)fb::band_spike_aux_doubles(n, kl);
+}
+
+int fb_band_factor_batched(fb_ctx* c, int count, int n, int kl, const double* zr, const double* zi,
+                           const double* far_, const double* fai, const double* fbr, const double* fbi,
+                           int64_t ldb, double* fr, double* fi, int64_t fs, int* ipiv, int64_t ps, double* aux,
+                           int64_t as, int* info) {
+  CTX_GUARD(c);
+  if (count < 0 || count > 64 || n < 0 || !fb::band_spike_ok(kl) || !zr || !zi || !far_ || !fr || !fi ||
+      !ipiv || !aux || !info)
+    return FB_ERR_ARG;
+  return set_err(c, fb::band_spike_factor(count, n, kl, zr, zi, far_, fai, fbr, fbi, ldb, fr, fi, fs, ipiv, ps,
+                                          aux, as, info, c->stream),
+                 "band_factor_batched");
+}
+
+int fb_band_solve_batched(fb_ctx* c, int count, int n, int kl, int nrhs, const double* fr, const double* fi,
+                          int64_t fs, const int* ipiv, int64_t ps, const double* aux, int64_t as, double* xr,
+                          double* xi, int64_t ldx, int64_t xs) {
+  CTX_GUARD(c);
+  if (count < 0 || count > 64 || n < 0 || nrhs < 0 || !fb::band_spike_ok(kl) || !fr || !fi || !ipiv || !aux ||
+      !xr || !xi)
+    return FB_ERR_ARG;
+  int r = ensure_scratch(c, sizeof(double) * fb::band_spike_solve_scratch_doubles(n, kl, nrhs, count));
+  if (r) return r;
+  return set_err(c, fb::band_spike_solve(count, n, kl, nrhs, fr, fi, fs, ipiv, ps, aux, as, xr, xi, ldx, xs,
+                                         (double*)c->scratch, c->stream),
+                 "band_solve_batched");
+}
+
+// Debug only (not part of the ABI header): partition size target of the
+// SPIKE band path (tests force many partitions at small n); returns P.
+int fb_debug_band_part_target(int target, int n, int kl) {
+  fb::band_spike_set_part_target(target);
+  return fb::band_spike_parts(n, kl);
+}
+
 // Debug only (not part of the ABI header): cycles per panel phase, CTA 0 / thread 0.
 int fb_debug_panel_profile(unsigned long long* out8) {
   fb::panel_profile_read(out8);
