@@ -120,6 +120,7 @@ class DeviceBandOps:
         self.cache_left = cache_bytes
         self._batches = []
         self._pass = {}
+        self._xbuf = {}
 
     # -- factorization ---------------------------------------------------------------
     def _factor_batch(self, bb, zs):
@@ -202,7 +203,10 @@ class DeviceBandOps:
         dev, n, m = self.dev, self.n, Y.cols
         for bb in self._batches:
             cnt = bb.count
-            X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+            X = self._xbuf.get(id(bb))
+            if X is None or X.shape[3] != m:
+                X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+                self._xbuf[id(bb)] = X
             X[0].copy_(Y.plane(0).unsqueeze(0).expand(cnt, n, m))
             if Y.cplx:
                 X[1].copy_(Y.plane(1).unsqueeze(0).expand(cnt, n, m))

@@ -669,6 +669,309 @@ __global__ void __launch_bounds__(WPB * 32) band_correct_kernel(CKArgs a) {
   }
 }
 
+// ---- staged partition solves: one CTA per (partition, column block, shift) -------
+// All warps of a CTA share the factor columns, staged through shared memory in
+// chunks of TC columns by cp.async (double-buffered); each thread keeps its
+// right-hand-side column's active rows in registers.  Forward (pivots + unit L)
+// and backward (U) are separate kernels so each keeps its own register window.
+constexpr int TC = 32;     // factor columns per staged chunk
+constexpr int SNW = 3;     // warps per CTA (96 right-hand sides)
+
+// Each thread keeps its right-hand-side column's active rows in a register
+// window and the next QD rows in a prefetch queue, so the global load of a row
+// entering the window was issued QD steps earlier.
+constexpr int QD = 4;
+
+template <int KL>
+__global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) {
+  constexpr int KV = 2 * KL, LW = 3 * KL + 1;
+  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x;
+  const int col = blockIdx.y * blockDim.x + tid;
+  const bool on = col < a.nrhs;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  const double* Wr = a.wr + k * a.sw;
+  const double* Wi = a.wi + k * a.sw;
+  const int* ipiv = a.ipiv + k * a.sp;
+  double* Xr = a.xr + k * a.sx;
+  double* Xi = a.xi + k * a.sx;
+  __shared__ double sl[2][2][TC][KL];
+  __shared__ int spv[2][TC];
+  auto stage = [&](int buf, int j0) {
+    for (int e = tid; e < TC * KL; e += blockDim.x) {
+      const int jj = e / KL, i = e % KL, j = j0 + jj;
+      const bool ok = j < hi;
+      const long long o = ok ? (long long)j * LW + KV + 1 + i : 0;
+      cp_async8(&sl[buf][0][jj][i], Wr + o, ok);
+      cp_async8(&sl[buf][1][jj][i], Wi + o, ok);
+    }
+    for (int jj = tid; jj < TC; jj += blockDim.x) spv[buf][jj] = (j0 + jj < hi) ? ipiv[j0 + jj] - (j0 + jj) : 0;
+    cp_async_commit();
+  };
+  auto ld = [&](int r, double& vr, double& vi) {
+    if (on && r < hi) {
+      const long long o = (long long)r * a.ldx + col;
+      vr = __ldcs(Xr + o);
+      vi = __ldcs(Xi + o);
+    } else {
+      vr = vi = 0.0;
+    }
+  };
+  double wr_[KL + 1], wi_[KL + 1], qr_[QD], qi_[QD];
+#pragma unroll
+  for (int i = 0; i <= KL; ++i) ld(lo + i, wr_[i], wi_[i]);
+#pragma unroll
+  for (int d = 0; d < QD; ++d) ld(lo + KL + 1 + d, qr_[d], qi_[d]);
+  stage(0, lo);
+  int buf = 0;
+  for (int j0 = lo; j0 < hi; j0 += TC, buf ^= 1) {
+    if (j0 + TC < hi) {
+      stage(buf ^ 1, j0 + TC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int jn = min(TC, hi - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      const int j = j0 + jj;
+      const int p = spv[buf][jj];
+      if (p) {
+#pragma unroll
+        for (int i = 1; i <= KL; ++i)
+          if (i == p) {
+            const double tr = wr_[0], ti = wi_[0];
+            wr_[0] = wr_[i];
+            wi_[0] = wi_[i];
+            wr_[i] = tr;
+            wi_[i] = ti;
+          }
+      }
+      const double x0r = wr_[0], x0i = wi_[0];
+#pragma unroll
+      for (int i = 0; i < KL; ++i) {
+        const double ar = sl[buf][0][jj][i], ai = sl[buf][1][jj][i];
+        wr_[1 + i] -= ar * x0r - ai * x0i;
+        wi_[1 + i] -= ar * x0i + ai * x0r;
+      }
+      if (on) {
+        const long long o = (long long)j * a.ldx + col;
+        Xr[o] = x0r;
+        Xi[o] = x0i;
+      }
+#pragma unroll
+      for (int i = 0; i < KL; ++i) {
+        wr_[i] = wr_[i + 1];
+        wi_[i] = wi_[i + 1];
+      }
+      wr_[KL] = qr_[0];
+      wi_[KL] = qi_[0];
+#pragma unroll
+      for (int d = 0; d + 1 < QD; ++d) {
+        qr_[d] = qr_[d + 1];
+        qi_[d] = qi_[d + 1];
+      }
+      ld(j + KL + 1 + QD, qr_[QD - 1], qi_[QD - 1]);
+    }
+    __syncthreads();
+  }
+}
+
+// Backward sweep: the (2kl+1)-row window of one right-hand side is split over
+// a lane pair (lane 2c: the upper kl rows, lane 2c+1: the lower kl+1 rows incl.
+// the current row), which halves the registers per thread; per step the pair
+// exchanges x_j and the row crossing the split by shuffles.
+template <int KL>
+__global__ void __launch_bounds__(2 * SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) {
+  constexpr int KV = 2 * KL, LW = 3 * KL + 1;
+  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, lane = tid & 31;
+  const int h = lane & 1;                                  // 0: rows j-KV..j-KL-1, 1: rows j-KL..j
+  const int col = blockIdx.y * (blockDim.x / 2) + (tid >> 1);
+  const bool on = col < a.nrhs;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  const double* Wr = a.wr + k * a.sw;
+  const double* Wi = a.wi + k * a.sw;
+  double* Xr = a.xr + k * a.sx;
+  double* Xi = a.xi + k * a.sx;
+  __shared__ double su[2][2][TC][KV + 1];  // U column j (rows j-KV..j)
+  __shared__ double sd[2][TC];             // 1 / U_jj
+  auto stage = [&](int buf, int j1) {
+    for (int e = tid; e < TC * (KV + 1); e += blockDim.x) {
+      const int jj = e / (KV + 1), i = e % (KV + 1), j = j1 - jj;
+      const bool ok = j >= lo;
+      const long long o = ok ? (long long)j * LW + i : 0;
+      cp_async8(&su[buf][0][jj][i], Wr + o, ok);
+      cp_async8(&su[buf][1][jj][i], Wi + o, ok);
+    }
+    cp_async_commit();
+  };
+  auto ld = [&](int r, double& vr, double& vi) {
+    if (on && r >= lo && r < hi) {
+      const long long o = (long long)r * a.ldx + col;
+      vr = __ldcs(Xr + o);
+      vi = __ldcs(Xi + o);
+    } else {
+      vr = vi = 0.0;
+    }
+  };
+  // local window: h = 0 holds window rows 0..KL-1 (row j-KV+t), h = 1 rows KL..KV
+  constexpr int NL = KL + 1;
+  double wr_[NL], wi_[NL], qr_[QD], qi_[QD];
+  const int base = h ? KL : 0, cnt = h ? KL + 1 : KL;
+#pragma unroll
+  for (int t = 0; t < NL; ++t) {
+    if (t < cnt) ld(hi - 1 - KV + base + t, wr_[t], wi_[t]);
+    else wr_[t] = wi_[t] = 0.0;
+  }
+#pragma unroll
+  for (int d = 0; d < QD; ++d) {
+    if (h == 0) ld(hi - 2 - KV - d, qr_[d], qi_[d]);
+    else qr_[d] = qi_[d] = 0.0;
+  }
+  stage(0, hi - 1);
+  int buf = 0;
+  for (int j1 = hi - 1; j1 >= lo; j1 -= TC, buf ^= 1) {
+    if (j1 - TC >= lo) {
+      stage(buf ^ 1, j1 - TC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    for (int jj = tid; jj < TC; jj += blockDim.x) {
+      const double dr = su[buf][0][jj][KV], di = su[buf][1][jj][KV];
+      const double den = dr * dr + di * di;
+      sd[0][jj] = den > 0.0 ? dr / den : 0.0;
+      sd[1][jj] = den > 0.0 ? -di / den : 0.0;
+    }
+    __syncthreads();
+    const int jn = min(TC, j1 - lo + 1);
+    for (int jj = 0; jj < jn; ++jj) {
+      const int j = j1 - jj;
+      // x_j = y_j / U_jj on the lower lane, broadcast to the pair
+      const double dr = sd[0][jj], di = sd[1][jj];
+      double qr = wr_[KL] * dr - wi_[KL] * di, qi = wr_[KL] * di + wi_[KL] * dr;
+      qr = __shfl_sync(0xffffffffu, qr, lane | 1);
+      qi = __shfl_sync(0xffffffffu, qi, lane | 1);
+      // rows j-KV+base+t -= U(row, j) x_j
+#pragma unroll
+      for (int t = 0; t < KL; ++t) {
+        const double br = su[buf][0][jj][base + t], bi = su[buf][1][jj][base + t];
+        wr_[t] -= br * qr - bi * qi;
+        wi_[t] -= br * qi + bi * qr;
+      }
+      if (on && h) {
+        const long long o = (long long)j * a.ldx + col;
+        Xr[o] = qr;
+        Xi[o] = qi;
+      }
+      // slide one row: upper lane's last row crosses to the lower lane
+      const double cr = __shfl_sync(0xffffffffu, wr_[KL - 1], lane & ~1);
+      const double ci = __shfl_sync(0xffffffffu, wi_[KL - 1], lane & ~1);
+#pragma unroll
+      for (int t = NL - 1; t > 0; --t) {
+        wr_[t] = wr_[t - 1];
+        wi_[t] = wi_[t - 1];
+      }
+      if (h) {
+        wr_[0] = cr;
+        wi_[0] = ci;
+      } else {
+        wr_[0] = qr_[0];
+        wi_[0] = qi_[0];
+#pragma unroll
+        for (int d = 0; d + 1 < QD; ++d) {
+          qr_[d] = qr_[d + 1];
+          qi_[d] = qi_[d + 1];
+        }
+        ld(j - 2 - KV - (QD - 1), qr_[QD - 1], qi_[QD - 1]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// correction with the spike rows staged through shared memory (cp.async 16 B)
+template <int KL>
+__global__ void __launch_bounds__(SNW * 32) band_correct2_kernel(CKArgs a) {
+  constexpr int W2 = 2 * KL;
+  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x;
+  const int col = blockIdx.y * blockDim.x + tid;
+  const bool on = col < a.nrhs;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  const double* Sr = a.sr + k * a.ss;
+  const double* Si = a.si + k * a.ss;
+  const double* Yr = a.yr + k * a.sy;
+  const double* Yi = a.yi + k * a.sy;
+  double* Xr = a.xr + k * a.sx;
+  double* Xi = a.xi + k * a.sx;
+  __shared__ __align__(16) double ss[2][2][TC][W2];
+  double tr[W2], ti[W2];  // (x_{j+1}^t, x_{j-1}^b) of this column
+#pragma unroll
+  for (int q = 0; q < KL; ++q) {
+    const bool nx = part + 1 < a.P && on, pv = part > 0 && on;
+    const long long on_ = ((long long)part * W2 + KL + q) * a.nrhs + col;
+    const long long op = ((long long)(part - 1) * W2 + q) * a.nrhs + col;
+    tr[q] = nx ? Yr[on_] : 0.0;
+    ti[q] = nx ? Yi[on_] : 0.0;
+    tr[KL + q] = pv ? Yr[op] : 0.0;
+    ti[KL + q] = pv ? Yi[op] : 0.0;
+  }
+  const bool v16 = (W2 % 2) == 0;
+  auto stage = [&](int buf, int r0) {
+    if (v16) {
+      for (int e = tid; e < TC * W2 / 2; e += blockDim.x) {
+        const int rr = e / (W2 / 2), q = (e % (W2 / 2)) * 2, r = r0 + rr;
+        const int ok = r < hi ? 16 : 0;
+        const long long o = ok ? (long long)r * W2 + q : 0;
+        cp_async16(&ss[buf][0][rr][q], Sr + o, ok);
+        cp_async16(&ss[buf][1][rr][q], Si + o, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  stage(0, lo);
+  int buf = 0;
+  for (int r0 = lo; r0 < hi; r0 += TC, buf ^= 1) {
+    if (r0 + TC < hi) {
+      stage(buf ^ 1, r0 + TC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int rn = min(TC, hi - r0);
+    if (on) {
+      constexpr int G8 = 8;
+      for (int g0 = 0; g0 < rn; g0 += G8) {
+        double xr8[G8], xi8[G8];
+#pragma unroll
+        for (int u = 0; u < G8; ++u) {
+          const bool ok = g0 + u < rn;
+          const long long o = (long long)(r0 + g0 + u) * a.ldx + col;
+          xr8[u] = ok ? __ldcs(Xr + o) : 0.0;
+          xi8[u] = ok ? __ldcs(Xi + o) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < G8; ++u) {
+          const int rr = g0 + u;
+          if (rr >= rn) break;
+          double ar = 0.0, ai = 0.0;
+#pragma unroll
+          for (int q = 0; q < W2; ++q) {
+            const double vr = ss[buf][0][rr][q], vi = ss[buf][1][rr][q];
+            ar += vr * tr[q] - vi * ti[q];
+            ai += vr * ti[q] + vi * tr[q];
+          }
+          const long long o = (long long)(r0 + rr) * a.ldx + col;
+          __stcs(Xr + o, xr8[u] - ar);
+          __stcs(Xi + o, xi8[u] - ai);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 using PsFn = void (*)(PSArgs);
 using CkFn = void (*)(CKArgs);
 #define FB_KL_TABLE(kern, T) \
@@ -676,13 +979,27 @@ using CkFn = void (*)(CKArgs);
                                    kern<8>, kern<9>, kern<10>, kern<11>, kern<12>, kern<13>, kern<14>,   \
                                    kern<15>, kern<16>};
 
-PsFn psolve_fn(int kl) {
-  FB_KL_TABLE(band_psolve_kernel, PsFn)
+PsFn psolve_fwd_fn(int kl) {
+  FB_KL_TABLE(band_psolve_fwd_kernel, PsFn)
+  return tbl[kl];
+}
+PsFn psolve_bwd_fn(int kl) {
+  FB_KL_TABLE(band_psolve_bwd_kernel, PsFn)
   return tbl[kl];
 }
 CkFn correct_fn(int kl) {
-  FB_KL_TABLE(band_correct_kernel, CkFn)
+  FB_KL_TABLE(band_correct2_kernel, CkFn)
   return tbl[kl];
+}
+
+// g = A_j^-1 X_j for every partition of every item (in place)
+cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
+  const int nw = std::min(SNW, ceil_div(ps.nrhs, 32));
+  const dim3 grid(ps.P, ceil_div(ps.nrhs, 32 * nw), count);
+  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, 0, st>>>(ps);
+  psolve_bwd_fn(ps.kl)<<<grid, 64 * nw, 0, st>>>(ps);
+  count_launch(2);
+  return cudaGetLastError();
 }
 
 int g_part_target = 0;
@@ -770,9 +1087,7 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = 2 * kl;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
   ps.xr = sr; ps.xi = si; ps.ldx = 2 * kl; ps.sx = sa;
-  psolve_fn(kl)<<<dim3(ceil_div(P, WPB), 1, count), WPB * 32, 0, st>>>(ps);
-  count_launch();
-  if ((e = cudaGetLastError())) return e;
+  if ((e = psolve_launch(ps, count, st))) return e;
   RFArgs rf{};
   rf.n = n; rf.kl = kl; rf.P = P;
   rf.sr = sr; rf.si = si; rf.ss = sa;
@@ -793,10 +1108,8 @@ cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* w
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = nrhs;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
   ps.xr = xr; ps.xi = xi; ps.ldx = ldx; ps.sx = sx;
-  psolve_fn(kl)<<<dim3(ceil_div(P, WPB), chunks, count), WPB * 32, 0, st>>>(ps);
-  count_launch();
   cudaError_t e;
-  if ((e = cudaGetLastError())) return e;
+  if ((e = psolve_launch(ps, count, st))) return e;
   if (P == 1) return cudaSuccess;
   double *sr, *si, *dr, *di, *fr, *fi;
   aux_ptrs(n, kl, const_cast<double*>(aux), &sr, &si, &dr, &di, &fr, &fi);
@@ -813,7 +1126,10 @@ cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* w
   ck.n = n; ck.kl = kl; ck.P = P; ck.nrhs = nrhs;
   ck.sr = sr; ck.si = si; ck.ss = sa; ck.yr = rs.yr; ck.yi = rs.yi; ck.sy = sy;
   ck.xr = xr; ck.xi = xi; ck.ldx = ldx; ck.sx = sx;
-  correct_fn(kl)<<<dim3(ceil_div(P, WPB), chunks, count), WPB * 32, 0, st>>>(ck);
+  {
+    const int nw = std::min(SNW, ceil_div(nrhs, 32));
+    correct_fn(kl)<<<dim3(P, ceil_div(nrhs, 32 * nw), count), 32 * nw, 0, st>>>(ck);
+  }
   count_launch();
   return cudaGetLastError();
 }

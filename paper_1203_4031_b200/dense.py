@@ -108,6 +108,7 @@ class DeviceDenseOps:
         self.factorizations = 0
         self._batches = []
         self._pass = {}          # (id(batch), idx, adjoint) -> Planar result of this pass
+        self._xbuf = {}          # (id(batch), adjoint) -> pass result buffer, reused across passes
 
     # -- factorization -------------------------------------------------------------
     def _factor_batch(self, fb_, zs):
@@ -189,7 +190,10 @@ class DeviceDenseOps:
         for fb_ in self._batches:
             cnt = fb_.count
             for adj in ((0, 1) if hermitian else (0,)):
-                X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+                X = self._xbuf.get((id(fb_), adj))
+                if X is None or X.shape[3] != m:
+                    X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+                    self._xbuf[(id(fb_), adj)] = X
                 re, im, ld, slu, piv, spiv, dinv, sdinv = fb_.args()
                 dev.check(dev.lib.fb_zgetrs_batched(dev.h, cnt, n, m, re, im, ld, slu, piv, spiv, dinv, sdinv,
                                                     adj, W.re, W.im, W.ld, 0, X[0].data_ptr(),

@@ -170,6 +170,43 @@ class Device:
                 dst.plane(1).zero_()
         return dst
 
+    _BOUNCE = 32 << 20  # bytes per pinned bounce buffer
+
+    def _d2h(self, t):
+        """Device tensor -> new numpy array.  Large arrays go through two
+        pinned bounce buffers (D2H of chunk k overlaps the host copy of k-1)
+        instead of torch's pageable copy."""
+        torch = self.torch
+        t = t.contiguous()
+        nbytes = t.numel() * t.element_size()
+        if nbytes <= (8 << 20):
+            return t.cpu().numpy()
+        if getattr(self, "_pins", None) is None:
+            self._pins = [torch.empty(self._BOUNCE, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            self._pin_ev = [torch.cuda.Event() for _ in range(2)]
+        npdt = {torch.float64: np.float64, torch.float32: np.float32, torch.int32: np.int32,
+                torch.int64: np.int64}.get(t.dtype)
+        if npdt is None:
+            return t.cpu().numpy()
+        out = np.empty(tuple(t.shape), dtype=npdt)
+        src = t.view(-1).view(torch.uint8)
+        dst = out.reshape(-1).view(np.uint8)
+        prev = None
+        for k, off in enumerate(range(0, nbytes, self._BOUNCE)):
+            n = min(self._BOUNCE, nbytes - off)
+            buf, ev = self._pins[k % 2], self._pin_ev[k % 2]
+            buf[:n].copy_(src[off:off + n], non_blocking=True)
+            ev.record()
+            if prev is not None:
+                pbuf, pev, poff, pn = prev
+                pev.synchronize()
+                dst[poff:poff + pn] = pbuf[:pn].numpy()
+            prev = (buf, ev, off, n)
+        pbuf, pev, poff, pn = prev
+        pev.synchronize()
+        dst[poff:poff + pn] = pbuf[:pn].numpy()
+        return out
+
     def download(self, p: Planar, as_complex=None):
         """Planar -> numpy (complex128 when the view is complex)."""
         as_complex = p.cplx if as_complex is None else as_complex
@@ -178,9 +215,9 @@ class Device:
             tmp = torch.empty((p.rows, p.cols, 2), dtype=torch.float64, device=self.tdev)
             self.check(self.lib.fb_pack(self.h, p.rows, p.cols, _P(tmp.data_ptr()), p.cols, _P(p.re),
                                         _P(p.im), p.ld, 0), "unpack")
-            out = tmp.cpu().numpy().view(np.complex128).reshape(p.rows, p.cols)
+            out = self._d2h(tmp).view(np.complex128).reshape(p.rows, p.cols)
             return out if as_complex else out.real.copy()
-        out = p.plane(0).cpu().numpy()
+        out = self._d2h(p.plane(0))
         return out.astype(np.complex128) if as_complex else out
 
     # -- arithmetic (each is one C-ABI call) -------------------------------
