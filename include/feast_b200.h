@@ -117,6 +117,19 @@ int fb_accumulate(fb_ctx* ctx, int variant, int n, int m,
                   double* q_re, double* q_im, int64_t ldq,
                   double weight, double radius, double theta);
 
+/* All quadrature terms of one contour pass in one sweep over Q (the
+ * accumulate_subspace calls of kernel.py:350-364 / 500-503 / 527-531 for every
+ * point of the pass, in the given order): term k is fb_accumulate's update
+ * with (variant[k], w[k], radius, theta[k]) on the solve result
+ * (x_re[k], x_im[k]) (host array of device pointers, common ldx).  Bitwise
+ * equal to calling fb_accumulate term by term; Q is read and written once.
+ * count <= 64; variants must be all 0 or all in {1, 2}. */
+int fb_accumulate_terms(fb_ctx* ctx, int count, const int* variant, const double* weight,
+                        double radius, const double* theta,
+                        const double* const* x_re, const double* const* x_im,
+                        int n, int m, int64_t ldx,
+                        double* q_re, double* q_im, int64_t ldq);
+
 /* C = alpha op(A) op(B) + beta C on planar / real FP64 (DMMA tensor pipe).
  * op: 'N', 'T' or 'C'.  Used for the dense multiplies (dense.py:111-117),
  * projections Q^H A Q, Q^H B Q (kernel.py:377-379) and the Ritz products

@@ -41,6 +41,7 @@ SIGNATURES = {
     "fb_splitmix": (c_int, [P, c_uint64, c_int64, c_int64, c_int, c_int, P, P, c_int64]),
     "fb_accumulate": (c_int, [P, c_int, c_int, c_int, P, P, c_int64, P, P, c_int64, c_double,
                               c_double, c_double]),
+    "fb_accumulate_terms": (c_int, [P, c_int, P, P, c_double, P, P, P, c_int, c_int, c_int64, P, P, c_int64]),
     "fb_gemm": (c_int, [P, c_int, c_char, c_char, c_int, c_int, c_int, c_double, c_double, P, P,
                         c_int64, P, P, c_int64, c_double, c_double, P, P, c_int64]),
     "fb_symmetrize": (c_int, [P, c_int, P, P, c_int64]),

@@ -121,6 +121,7 @@ class DeviceBandOps:
         self._batches = []
         self._pass = {}
         self._xbuf = {}
+        self._zmap = {}          # z -> (batch, idx) of every factored shift
 
     # -- factorization ---------------------------------------------------------------
     def _factor_batch(self, bb, zs):
@@ -164,6 +165,7 @@ class DeviceBandOps:
             self._batches.append(bb)
             for i, z in enumerate(chunk):
                 made.setdefault(z, (bb, i))
+                self._zmap.setdefault(z, (bb, i))
         out = {}
         for z in zs:
             bb, i = made[z]
@@ -218,6 +220,18 @@ class DeviceBandOps:
                       "band_solve_batched")
             for i in range(cnt):
                 self._pass[(id(bb), i)] = (X, i)
+
+    def pass_result(self, z, adjoint):
+        """Planar view of this pass's solve for shift z (A^H: the conj(z) factor)."""
+        z = complex(z)
+        hit = self._zmap.get(z.conjugate() if adjoint else z)
+        if hit is None:
+            return None
+        got = self._pass.get((id(hit[0]), hit[1]))
+        if got is None:
+            return None
+        X, i = got
+        return Planar(X[:, i], True, X.shape[2], X.shape[3], X.shape[3])
 
     def _solve_batched(self, f, W: Planar):
         hit = self._pass.get((id(f.batch), f.idx))

@@ -40,6 +40,99 @@ __global__ void band_matvec_kernel(int n, int kl, int m, const double* __restric
   }
 }
 
+
+// Tiled band matvec for kl <= 16: one CTA = RT consecutive rows x (32 * warps)
+// columns.  The band entries of the CTA's rows are staged in shared memory
+// row-aligned (sb[t][ii] = A(i0+ii, i0+ii-KL+t)) so every lane of a warp reads
+// the same word (broadcast); each thread slides a register window of its
+// column's x values (rows i-KL..i+KL) down the rows, so X is read from HBM
+// once (plus a 2KL-row halo per tile) and Y written once.
+constexpr int MV_RT = 128;
+template <int KL, bool CPLX>
+__global__ void __launch_bounds__(128) band_matvec_tiled(int n, int m, const double* __restrict__ fbr,
+                                                         const double* __restrict__ fbi, long long ldb,
+                                                         const double* __restrict__ xr,
+                                                         const double* __restrict__ xi, long long ldx,
+                                                         double* __restrict__ yr, double* __restrict__ yi,
+                                                         long long ldy) {
+  constexpr int W = 2 * KL + 1;
+  extern __shared__ double sb[];  // [CPLX ? 2 : 1][W][MV_RT]
+  const int i0 = blockIdx.x * MV_RT;
+  const int rows = min(MV_RT, n - i0);
+  for (int e = threadIdx.x; e < W * MV_RT; e += blockDim.x) {
+    const int t = e / MV_RT, ii = e % MV_RT, i = i0 + ii, j = i - KL + t;
+    double vr = 0.0, vi = 0.0;
+    if (ii < rows && j >= 0 && j < n) {
+      const long long o = (long long)(2 * KL - t) * ldb + j;  // fb[KL + (i - j)][j]
+      vr = fbr[o];
+      if (CPLX && fbi) vi = fbi[o];
+    }
+    sb[e] = vr;
+    if (CPLX) sb[W * MV_RT + e] = vi;
+  }
+  __syncthreads();
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  auto ld = [&](int j, double& vr, double& vi) {
+    vr = vi = 0.0;
+    if (j >= 0 && j < n) {
+      vr = xr[(long long)j * ldx + c];
+      if (CPLX && xi) vi = xi[(long long)j * ldx + c];
+    }
+  };
+  constexpr int QD = 8;  // rows prefetched ahead of the window
+  double wr[W], wi[W], qr[QD], qi[QD];
+#pragma unroll
+  for (int t = 0; t < W; ++t) ld(i0 - KL + t, wr[t], wi[t]);
+#pragma unroll
+  for (int d = 0; d < QD; ++d) ld(i0 + KL + 1 + d, qr[d], qi[d]);
+  for (int ii = 0; ii < rows; ++ii) {
+    // numpy's order and rounding (banded.py:55-64): s = -KL..KL, i.e. j = i+KL
+    // down to i-KL, each term a plain product added to y (no FMA contraction)
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int t = W - 1; t >= 0; --t) {
+      const double ar = sb[t * MV_RT + ii];
+      if (CPLX) {
+        const double ai = sb[W * MV_RT + t * MV_RT + ii];
+        sr = __dadd_rn(sr, __dsub_rn(__dmul_rn(ar, wr[t]), __dmul_rn(ai, wi[t])));
+        si = __dadd_rn(si, __dadd_rn(__dmul_rn(ar, wi[t]), __dmul_rn(ai, wr[t])));
+      } else {
+        sr = __dadd_rn(sr, __dmul_rn(ar, wr[t]));
+      }
+    }
+    const long long o = (long long)(i0 + ii) * ldy + c;
+    yr[o] = sr;
+    if (CPLX) yi[o] = si;
+#pragma unroll
+    for (int t = 0; t + 1 < W; ++t) {
+      wr[t] = wr[t + 1];
+      if (CPLX) wi[t] = wi[t + 1];
+    }
+    wr[W - 1] = qr[0];
+    wi[W - 1] = qi[0];
+#pragma unroll
+    for (int d = 0; d + 1 < QD; ++d) {
+      qr[d] = qr[d + 1];
+      qi[d] = qi[d + 1];
+    }
+    ld(i0 + ii + KL + 1 + QD, qr[QD - 1], qi[QD - 1]);
+  }
+}
+
+using MvFn = void (*)(int, int, const double*, const double*, long long, const double*, const double*, long long,
+                      double*, double*, long long);
+template <bool CPLX>
+MvFn matvec_fn(int kl) {
+  static const MvFn tbl[17] = {band_matvec_tiled<0, CPLX>,  band_matvec_tiled<1, CPLX>,  band_matvec_tiled<2, CPLX>,
+                               band_matvec_tiled<3, CPLX>,  band_matvec_tiled<4, CPLX>,  band_matvec_tiled<5, CPLX>,
+                               band_matvec_tiled<6, CPLX>,  band_matvec_tiled<7, CPLX>,  band_matvec_tiled<8, CPLX>,
+                               band_matvec_tiled<9, CPLX>,  band_matvec_tiled<10, CPLX>, band_matvec_tiled<11, CPLX>,
+                               band_matvec_tiled<12, CPLX>, band_matvec_tiled<13, CPLX>, band_matvec_tiled<14, CPLX>,
+                               band_matvec_tiled<15, CPLX>, band_matvec_tiled<16, CPLX>};
+  return tbl[kl];
+}
+
 // Shift into the working array: W[j][kl + r'] = z*FB[r'][j] - FA[r'][j], r' = 0..2kl.
 __global__ void band_shift_kernel(int n, int kl, double zr, double zi, const double* __restrict__ far_,
                                   const double* __restrict__ fai, const double* __restrict__ fbr,
@@ -277,9 +370,23 @@ cudaError_t band_matvec_launch(int n, int kl, int m, const double* fbr, const do
                                const double* xr, const double* xi, long long ldx, double* yr, double* yi,
                                long long ldy, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
+  count_launch();
+  const bool cplx = fbi != nullptr || xi != nullptr;
+  if (kl >= 0 && kl <= 16 && (!cplx || yi != nullptr)) {
+    const size_t smem = sizeof(double) * (cplx ? 2 : 1) * (2 * kl + 1) * MV_RT;
+    const MvFn fn = cplx ? matvec_fn<true>(kl) : matvec_fn<false>(kl);
+    static bool cfg[2][17] = {};
+    if (!cfg[cplx][kl]) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg[cplx][kl] = true;
+    }
+    const int nt = m >= 96 ? 96 : (m >= 64 ? 64 : 32);
+    fn<<<dim3(ceil_div(n, MV_RT), ceil_div(m, nt)), nt, smem, st>>>(n, m, fbr, fbi, ldb, xr, xi, ldx, yr,
+                                                                     cplx ? yi : nullptr, ldy);
+    return cudaGetLastError();
+  }
   long long total = (long long)n * m;
   int blocks = (int)std::min<long long>((total + 255) / 256, 16 * kSMs);
-  count_launch();
   band_matvec_kernel<<<blocks, 256, 0, st>>>(n, kl, m, fbr, fbi, ldb, xr, xi, ldx, yr, yi, ldy);
   return cudaGetLastError();
 }

@@ -222,6 +222,10 @@ struct PSArgs {
   long long sp;
   double *xr, *xi;
   long long ldx, sx;
+  // forward sweep input (nullptr: in place from x); fi == nullptr: real input;
+  // sf = 0: one right-hand-side block shared by every item (the pass's Y)
+  const double *fr, *fi;
+  long long ldf, sf;
 };
 
 template <int KL>
@@ -671,16 +675,35 @@ __global__ void __launch_bounds__(WPB * 32) band_correct_kernel(CKArgs a) {
 
 // ---- staged partition solves: one CTA per (partition, column block, shift) -------
 // All warps of a CTA share the factor columns, staged through shared memory in
-// chunks of TC columns by cp.async (double-buffered); each thread keeps its
-// right-hand-side column's active rows in registers.  Forward (pivots + unit L)
-// and backward (U) are separate kernels so each keeps its own register window.
+// chunks of TC columns by cp.async (double-buffered) with re/im interleaved so
+// one LDS.128 feeds a complex multiply-add; each thread keeps its right-hand
+// side column's active rows in a register window and the next QD rows in a
+// prefetch queue (the global load of a row entering the window was issued QD
+// steps earlier).  Forward (pivots + unit L) and backward (U) are separate
+// kernels so each keeps its own register window.
 constexpr int TC = 32;     // factor columns per staged chunk
 constexpr int SNW = 3;     // warps per CTA (96 right-hand sides)
-
-// Each thread keeps its right-hand-side column's active rows in a register
-// window and the next QD rows in a prefetch queue, so the global load of a row
-// entering the window was issued QD steps earlier.
 constexpr int QD = 4;
+
+// One forward step with the row interchange (0 <-> P) folded in at compile
+// time: x0 = w[P]; the window slides by one as each multiply-add writes row
+// i+1's update into register i, so neither the interchange nor the slide
+// costs a move.  The caller dispatches on the warp-uniform P with a switch.
+template <int KL, int P>
+__device__ __forceinline__ void fwd_step(double (&wr)[KL + 1], double (&wi)[KL + 1], const double2* __restrict__ l,
+                                         double& x0r, double& x0i) {
+  x0r = wr[P];
+  x0i = wi[P];
+  const double o_r = wr[0], o_i = wi[0];
+#pragma unroll
+  for (int i = 0; i < KL; ++i) {
+    const double sr = (i + 1 == P) ? o_r : wr[i + 1];
+    const double si = (i + 1 == P) ? o_i : wi[i + 1];
+    const double2 lv = l[i];
+    wr[i] = fma(-lv.x, x0r, fma(lv.y, x0i, sr));
+    wi[i] = fma(-lv.x, x0i, fma(-lv.y, x0r, si));
+  }
+}
 
 template <int KL>
 __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) {
@@ -694,26 +717,29 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
   const int* ipiv = a.ipiv + k * a.sp;
   double* Xr = a.xr + k * a.sx;
   double* Xi = a.xi + k * a.sx;
-  __shared__ double sl[2][2][TC][KL];
+  const bool sep = a.fr != nullptr;
+  const double* Fr = sep ? a.fr + k * a.sf : Xr;
+  const double* Fi = sep ? (a.fi ? a.fi + k * a.sf : nullptr) : Xi;
+  const long long ldf = sep ? a.ldf : a.ldx;
+  __shared__ double2 sl[2][TC][KL];  // multipliers (re, im) of column j
   __shared__ int spv[2][TC];
   auto stage = [&](int buf, int j0) {
     for (int e = tid; e < TC * KL; e += blockDim.x) {
       const int jj = e / KL, i = e % KL, j = j0 + jj;
       const bool ok = j < hi;
       const long long o = ok ? (long long)j * LW + KV + 1 + i : 0;
-      cp_async8(&sl[buf][0][jj][i], Wr + o, ok);
-      cp_async8(&sl[buf][1][jj][i], Wi + o, ok);
+      cp_async8(&sl[buf][jj][i].x, Wr + o, ok);
+      cp_async8(&sl[buf][jj][i].y, Wi + o, ok);
     }
     for (int jj = tid; jj < TC; jj += blockDim.x) spv[buf][jj] = (j0 + jj < hi) ? ipiv[j0 + jj] - (j0 + jj) : 0;
     cp_async_commit();
   };
   auto ld = [&](int r, double& vr, double& vi) {
+    vr = vi = 0.0;
     if (on && r < hi) {
-      const long long o = (long long)r * a.ldx + col;
-      vr = __ldcs(Xr + o);
-      vi = __ldcs(Xi + o);
-    } else {
-      vr = vi = 0.0;
+      const long long o = (long long)r * ldf + col;
+      vr = __ldcs(Fr + o);
+      if (Fi) vi = __ldcs(Fi + o);
     }
   };
   double wr_[KL + 1], wi_[KL + 1], qr_[QD], qi_[QD];
@@ -732,36 +758,27 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
     }
     __syncthreads();
     const int jn = min(TC, hi - j0);
+#pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
       const int j = j0 + jj;
       const int p = spv[buf][jj];
-      if (p) {
-#pragma unroll
-        for (int i = 1; i <= KL; ++i)
-          if (i == p) {
-            const double tr = wr_[0], ti = wi_[0];
-            wr_[0] = wr_[i];
-            wi_[0] = wi_[i];
-            wr_[i] = tr;
-            wi_[i] = ti;
-          }
+      const double2* lcol = sl[buf][jj];
+      double x0r, x0i;
+#define FB_FWD_CASE(I)                                                          \
+  case I:                                                                       \
+    if constexpr (I <= KL) fwd_step<KL, (I <= KL ? I : 0)>(wr_, wi_, lcol, x0r, x0i); \
+    break;
+      switch (p) {
+        FB_FWD_CASE(1) FB_FWD_CASE(2) FB_FWD_CASE(3) FB_FWD_CASE(4) FB_FWD_CASE(5) FB_FWD_CASE(6)
+        FB_FWD_CASE(7) FB_FWD_CASE(8) FB_FWD_CASE(9) FB_FWD_CASE(10) FB_FWD_CASE(11) FB_FWD_CASE(12)
+        FB_FWD_CASE(13) FB_FWD_CASE(14) FB_FWD_CASE(15) FB_FWD_CASE(16)
+        default: fwd_step<KL, 0>(wr_, wi_, lcol, x0r, x0i); break;
       }
-      const double x0r = wr_[0], x0i = wi_[0];
-#pragma unroll
-      for (int i = 0; i < KL; ++i) {
-        const double ar = sl[buf][0][jj][i], ai = sl[buf][1][jj][i];
-        wr_[1 + i] -= ar * x0r - ai * x0i;
-        wi_[1 + i] -= ar * x0i + ai * x0r;
-      }
+#undef FB_FWD_CASE
       if (on) {
         const long long o = (long long)j * a.ldx + col;
         Xr[o] = x0r;
         Xi[o] = x0i;
-      }
-#pragma unroll
-      for (int i = 0; i < KL; ++i) {
-        wr_[i] = wr_[i + 1];
-        wi_[i] = wi_[i + 1];
       }
       wr_[KL] = qr_[0];
       wi_[KL] = qi_[0];
@@ -776,31 +793,28 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
   }
 }
 
-// Backward sweep: the (2kl+1)-row window of one right-hand side is split over
-// a lane pair (lane 2c: the upper kl rows, lane 2c+1: the lower kl+1 rows incl.
-// the current row), which halves the registers per thread; per step the pair
-// exchanges x_j and the row crossing the split by shuffles.
+// Backward sweep: one thread per right-hand side holds rows j-KV..j in
+// registers; the U column (re, im interleaved, 1/U_jj precomputed per chunk)
+// comes from shared memory.
 template <int KL>
-__global__ void __launch_bounds__(2 * SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) {
+__global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) {
   constexpr int KV = 2 * KL, LW = 3 * KL + 1;
-  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, lane = tid & 31;
-  const int h = lane & 1;                                  // 0: rows j-KV..j-KL-1, 1: rows j-KL..j
-  const int col = blockIdx.y * (blockDim.x / 2) + (tid >> 1);
+  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x;
+  const int col = blockIdx.y * blockDim.x + tid;
   const bool on = col < a.nrhs;
   const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
   const double* Wr = a.wr + k * a.sw;
   const double* Wi = a.wi + k * a.sw;
   double* Xr = a.xr + k * a.sx;
   double* Xi = a.xi + k * a.sx;
-  __shared__ double su[2][2][TC][KV + 1];  // U column j (rows j-KV..j)
-  __shared__ double sd[2][TC];             // 1 / U_jj
+  __shared__ double2 su[2][TC][KV + 1];  // U column j (rows j-KV..j); slot KV <- 1/U_jj
   auto stage = [&](int buf, int j1) {
     for (int e = tid; e < TC * (KV + 1); e += blockDim.x) {
       const int jj = e / (KV + 1), i = e % (KV + 1), j = j1 - jj;
       const bool ok = j >= lo;
       const long long o = ok ? (long long)j * LW + i : 0;
-      cp_async8(&su[buf][0][jj][i], Wr + o, ok);
-      cp_async8(&su[buf][1][jj][i], Wi + o, ok);
+      cp_async8(&su[buf][jj][i].x, Wr + o, ok);
+      cp_async8(&su[buf][jj][i].y, Wi + o, ok);
     }
     cp_async_commit();
   };
@@ -813,20 +827,11 @@ __global__ void __launch_bounds__(2 * SNW * 32, 2) band_psolve_bwd_kernel(PSArgs
       vr = vi = 0.0;
     }
   };
-  // local window: h = 0 holds window rows 0..KL-1 (row j-KV+t), h = 1 rows KL..KV
-  constexpr int NL = KL + 1;
-  double wr_[NL], wi_[NL], qr_[QD], qi_[QD];
-  const int base = h ? KL : 0, cnt = h ? KL + 1 : KL;
+  double wr_[KV + 1], wi_[KV + 1], qr_[QD], qi_[QD];  // wr_[t] = row j-KV+t
 #pragma unroll
-  for (int t = 0; t < NL; ++t) {
-    if (t < cnt) ld(hi - 1 - KV + base + t, wr_[t], wi_[t]);
-    else wr_[t] = wi_[t] = 0.0;
-  }
+  for (int t = 0; t <= KV; ++t) ld(hi - 1 - KV + t, wr_[t], wi_[t]);
 #pragma unroll
-  for (int d = 0; d < QD; ++d) {
-    if (h == 0) ld(hi - 2 - KV - d, qr_[d], qi_[d]);
-    else qr_[d] = qi_[d] = 0.0;
-  }
+  for (int d = 0; d < QD; ++d) ld(hi - 2 - KV - d, qr_[d], qi_[d]);
   stage(0, hi - 1);
   int buf = 0;
   for (int j1 = hi - 1; j1 >= lo; j1 -= TC, buf ^= 1) {
@@ -838,53 +843,38 @@ __global__ void __launch_bounds__(2 * SNW * 32, 2) band_psolve_bwd_kernel(PSArgs
     }
     __syncthreads();
     for (int jj = tid; jj < TC; jj += blockDim.x) {
-      const double dr = su[buf][0][jj][KV], di = su[buf][1][jj][KV];
-      const double den = dr * dr + di * di;
-      sd[0][jj] = den > 0.0 ? dr / den : 0.0;
-      sd[1][jj] = den > 0.0 ? -di / den : 0.0;
+      const double2 d = su[buf][jj][KV];
+      const double den = d.x * d.x + d.y * d.y;
+      su[buf][jj][KV] = den > 0.0 ? make_double2(d.x / den, -d.y / den) : make_double2(0.0, 0.0);
     }
     __syncthreads();
     const int jn = min(TC, j1 - lo + 1);
+#pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
       const int j = j1 - jj;
-      // x_j = y_j / U_jj on the lower lane, broadcast to the pair
-      const double dr = sd[0][jj], di = sd[1][jj];
-      double qr = wr_[KL] * dr - wi_[KL] * di, qi = wr_[KL] * di + wi_[KL] * dr;
-      qr = __shfl_sync(0xffffffffu, qr, lane | 1);
-      qi = __shfl_sync(0xffffffffu, qi, lane | 1);
-      // rows j-KV+base+t -= U(row, j) x_j
+      const double2 dv = su[buf][jj][KV];
+      const double qr = wr_[KV] * dv.x - wi_[KV] * dv.y, qi = wr_[KV] * dv.y + wi_[KV] * dv.x;
+      // rows j-KV+t -= U(., j) x_j, written one slot up (the window slides)
 #pragma unroll
-      for (int t = 0; t < KL; ++t) {
-        const double br = su[buf][0][jj][base + t], bi = su[buf][1][jj][base + t];
-        wr_[t] -= br * qr - bi * qi;
-        wi_[t] -= br * qi + bi * qr;
+      for (int t = KV - 1; t >= 0; --t) {
+        if (t % 8 == 7) asm volatile("" ::: "memory");
+        const double2 u = su[buf][jj][t];
+        wr_[t + 1] = fma(-u.x, qr, fma(u.y, qi, wr_[t]));
+        wi_[t + 1] = fma(-u.x, qi, fma(-u.y, qr, wi_[t]));
       }
-      if (on && h) {
+      if (on) {
         const long long o = (long long)j * a.ldx + col;
         Xr[o] = qr;
         Xi[o] = qi;
       }
-      // slide one row: upper lane's last row crosses to the lower lane
-      const double cr = __shfl_sync(0xffffffffu, wr_[KL - 1], lane & ~1);
-      const double ci = __shfl_sync(0xffffffffu, wi_[KL - 1], lane & ~1);
+      wr_[0] = qr_[0];
+      wi_[0] = qi_[0];
 #pragma unroll
-      for (int t = NL - 1; t > 0; --t) {
-        wr_[t] = wr_[t - 1];
-        wi_[t] = wi_[t - 1];
+      for (int d = 0; d + 1 < QD; ++d) {
+        qr_[d] = qr_[d + 1];
+        qi_[d] = qi_[d + 1];
       }
-      if (h) {
-        wr_[0] = cr;
-        wi_[0] = ci;
-      } else {
-        wr_[0] = qr_[0];
-        wi_[0] = qi_[0];
-#pragma unroll
-        for (int d = 0; d + 1 < QD; ++d) {
-          qr_[d] = qr_[d + 1];
-          qi_[d] = qi_[d + 1];
-        }
-        ld(j - 2 - KV - (QD - 1), qr_[QD - 1], qi_[QD - 1]);
-      }
+      ld(j - 2 - KV - (QD - 1), qr_[QD - 1], qi_[QD - 1]);
     }
     __syncthreads();
   }
@@ -997,7 +987,7 @@ cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
   const int nw = std::min(SNW, ceil_div(ps.nrhs, 32));
   const dim3 grid(ps.P, ceil_div(ps.nrhs, 32 * nw), count);
   psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, 0, st>>>(ps);
-  psolve_bwd_fn(ps.kl)<<<grid, 64 * nw, 0, st>>>(ps);
+  psolve_bwd_fn(ps.kl)<<<grid, 32 * nw, 0, st>>>(ps);
   count_launch(2);
   return cudaGetLastError();
 }

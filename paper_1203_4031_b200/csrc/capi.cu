@@ -251,30 +251,51 @@ int fb_splitmix(fb_ctx* c, uint64_t seed, int64_t off_re, int64_t off_im, int n,
   return set_err(c, fb::splitmix_launch(seed, off_re, off_im, n, m, re, im, ld, c->stream), "splitmix");
 }
 
+// Coefficients evaluated as numpy does (kernel.py:117-123):
+//   sym : (w/2.0) * (r*exp(i theta) * x).real
+//   herm: ((w/4.0) * r) * exp(+-i theta), then times x
+static void acc_coeffs(int variant, double w, double r, double theta, int* mode, double* h, double* cr,
+                       double* ci) {
+  double cth = std::cos(theta), sth = std::sin(theta);
+  if (variant == 0) {
+    *mode = 0;
+    *h = w / 2.0;
+    *cr = r * cth;
+    *ci = r * sth;
+  } else {
+    *mode = 1;
+    double s = (w / 4.0) * r;
+    *h = 0.0;
+    *cr = s * cth;
+    *ci = s * (variant == 1 ? sth : -sth);
+  }
+}
+
 int fb_accumulate(fb_ctx* c, int variant, int n, int m, const double* xr, const double* xi, int64_t ldx,
                   double* qr, double* qi, int64_t ldq, double w, double r, double theta) {
   CTX_GUARD(c);
   if (variant < 0 || variant > 2) return FB_ERR_ARG;
-  // Coefficients evaluated as numpy does (kernel.py:117-123):
-  //   sym : (w/2.0) * (r*exp(i theta) * x).real
-  //   herm: ((w/4.0) * r) * exp(+-i theta), then times x
-  double cth = std::cos(theta), sth = std::sin(theta);
   int mode;
   double h, cr, ci;
-  if (variant == 0) {
-    mode = 0;
-    h = w / 2.0;
-    cr = r * cth;
-    ci = r * sth;
-  } else {
-    mode = 1;
-    double s = (w / 4.0) * r;
-    h = 0.0;
-    cr = s * cth;
-    ci = s * (variant == 1 ? sth : -sth);
-  }
+  acc_coeffs(variant, w, r, theta, &mode, &h, &cr, &ci);
   return set_err(c, fb::accumulate_launch(mode, n, m, xr, xi, ldx, qr, qi, ldq, h, cr, ci, c->stream),
                  "accumulate");
+}
+
+int fb_accumulate_terms(fb_ctx* c, int count, const int* variant, const double* w, double r, const double* theta,
+                        const double* const* xr, const double* const* xi, int n, int m, int64_t ldx, double* qr,
+                        double* qi, int64_t ldq) {
+  CTX_GUARD(c);
+  if (count < 0 || count > fb::kMaxAccTerms) return FB_ERR_ARG;
+  fb::AccTerms t{};
+  t.count = count;
+  for (int k = 0; k < count; ++k) {
+    if (variant[k] < 0 || variant[k] > 2 || (variant[k] == 0) != (variant[0] == 0)) return FB_ERR_ARG;
+    acc_coeffs(variant[k], w[k], r, theta[k], &t.mode[k], &t.h[k], &t.cr[k], &t.ci[k]);
+    t.xr[k] = xr[k];
+    t.xi[k] = xi[k];
+  }
+  return set_err(c, fb::accumulate_terms_launch(t, n, m, ldx, qr, qi, ldq, c->stream), "accumulate_terms");
 }
 
 int fb_gemm(fb_ctx* c, int cplx, char opa, char opb, int m, int n, int k, double ar, double ai,

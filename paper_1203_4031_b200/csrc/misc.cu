@@ -57,6 +57,36 @@ __global__ void accumulate_kernel(int mode, int n, int m, const double* __restri
   }
 }
 
+// All quadrature terms of one contour pass in one sweep over Q: each element
+// of Q is read once, updated term by term in the caller's order with exactly
+// accumulate_kernel's arithmetic (so the result equals the sequence of
+// per-point accumulations bit for bit), and written once.
+__global__ void accumulate_terms_kernel(AccTerms t, int n, int m, long long ldx, double* __restrict__ qr,
+                                        double* __restrict__ qi, long long ldq) {
+  long long total = (long long)n * m;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    const long long ox = i * ldx + j, oq = i * ldq + j;
+    double q_r = qr[oq], q_i = (t.mode[0] != 0 && qi) ? qi[oq] : 0.0;
+    for (int k = 0; k < t.count; ++k) {
+      const double a = t.xr[k][ox], b = t.xi[k][ox];
+      const double cr = t.cr[k], ci = t.ci[k];
+      if (t.mode[k] == 0) {
+        const double v = __dsub_rn(__dmul_rn(cr, a), __dmul_rn(ci, b));
+        q_r = __dsub_rn(q_r, __dmul_rn(t.h[k], v));
+      } else {
+        const double vr = __dsub_rn(__dmul_rn(cr, a), __dmul_rn(ci, b));
+        const double vi = __dadd_rn(__dmul_rn(cr, b), __dmul_rn(ci, a));
+        q_r = __dsub_rn(q_r, vr);
+        q_i = __dsub_rn(q_i, vi);
+      }
+    }
+    qr[oq] = q_r;
+    if (t.mode[0] != 0 && qi) qi[oq] = q_i;
+  }
+}
+
 __global__ void symmetrize_kernel(int m, double* __restrict__ re, double* __restrict__ im,
                                   long long ld) {
   long long total = (long long)m * m;
@@ -151,6 +181,17 @@ cudaError_t splitmix_launch(unsigned long long seed, long long off_re, long long
   if (n <= 0 || m <= 0) return cudaSuccess;
   count_launch();
   splitmix_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(seed, off_re, off_im, n, m, re, im, ld);
+  return cudaGetLastError();
+}
+
+cudaError_t accumulate_terms_launch(const AccTerms& t, int n, int m, long long ldx, double* qr, double* qi,
+                                    long long ldq, cudaStream_t st) {
+  if (n <= 0 || m <= 0 || t.count <= 0) return cudaSuccess;
+  if (t.count > kMaxAccTerms) return cudaErrorInvalidValue;
+  for (int k = 1; k < t.count; ++k)
+    if ((t.mode[k] != 0) != (t.mode[0] != 0)) return cudaErrorInvalidValue;
+  count_launch();
+  accumulate_terms_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(t, n, m, ldx, qr, qi, ldq);
   return cudaGetLastError();
 }
 

@@ -9,6 +9,17 @@ cudaError_t splitmix_launch(unsigned long long seed, long long off_re, long long
 cudaError_t accumulate_launch(int mode, int n, int m, const double* xr, const double* xi,
                               long long ldx, double* qr, double* qi, long long ldq, double h,
                               double cr, double ci, cudaStream_t st);
+// one contour pass's quadrature terms (<= kMaxAccTerms), applied in order
+constexpr int kMaxAccTerms = 64;
+struct AccTerms {
+  int count;
+  int mode[kMaxAccTerms];
+  double h[kMaxAccTerms], cr[kMaxAccTerms], ci[kMaxAccTerms];
+  const double* xr[kMaxAccTerms];
+  const double* xi[kMaxAccTerms];
+};
+cudaError_t accumulate_terms_launch(const AccTerms& t, int n, int m, long long ldx, double* qr, double* qi,
+                                    long long ldq, cudaStream_t st);
 cudaError_t symmetrize_launch(int m, double* re, double* im, long long ld, cudaStream_t st);
 size_t residual_scratch_bytes(int n, int m);
 cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, const double* bxr,

@@ -108,6 +108,7 @@ class DeviceDenseOps:
         self.factorizations = 0
         self._batches = []
         self._pass = {}          # (id(batch), idx, adjoint) -> Planar result of this pass
+        self._zmap = {}          # z -> (batch, idx) of resident factors
         self._xbuf = {}          # (id(batch), adjoint) -> pass result buffer, reused across passes
 
     # -- factorization -------------------------------------------------------------
@@ -156,6 +157,7 @@ class DeviceDenseOps:
         self._batches.append(fb_)
         for i, z in enumerate(zs[:fit]):
             out[z] = _DenseFactor(z, fb_, i, True)
+            self._zmap[z] = (fb_, i)
         return out
 
     def factorize(self, z):
@@ -200,6 +202,17 @@ class DeviceDenseOps:
                                                     X[1].data_ptr(), m, n * m), "zgetrs_batched")
                 for i in range(cnt):
                     self._pass[(id(fb_), i, adj)] = (X, i)
+
+    def pass_result(self, z, adjoint):
+        """Planar view of this pass's solve for shift z (None if not resident)."""
+        hit = self._zmap.get(complex(z))
+        if hit is None:
+            return None
+        got = self._pass.get((id(hit[0]), hit[1], int(adjoint)))
+        if got is None:
+            return None
+        X, i = got
+        return Planar(X[:, i], True, X.shape[2], X.shape[3], X.shape[3])
 
     def _solve(self, f, W: Planar, adjoint):
         if f.resident:
@@ -274,7 +287,15 @@ class B200DenseOps:
 
 
 def _shape(a):
+    if isinstance(a, Planar):
+        return (a.rows, a.cols)
     return tuple(a.shape) if hasattr(a, "shape") else np.asarray(a).shape
+
+
+def _dtype_name(a):
+    if isinstance(a, Planar):
+        return "complex128" if a.cplx else "float64"
+    return str(a.dtype)
 
 
 def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, device=None,
@@ -282,11 +303,11 @@ def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, devic
     options = options or SolverOptions()
     fpm = FeastParams.coerce(fpm) if fpm is not None else feastinit()
     uplo = (uplo or "F").upper()
-    if not _is_torch(a):
+    if not _is_torch(a) and not isinstance(a, Planar):
         a = np.asarray(a)
     shp = _shape(a)
     n = shp[0] if len(shp) >= 1 else 0
-    single = str(a.dtype).endswith(("float32", "complex64"))
+    single = _dtype_name(a).endswith(("float32", "complex64"))
     scalar = (np.complex64 if single else np.complex128) if hermitian else (np.float32 if single else np.float64)
     routine = _routine_name(hermitian, single, b is not None)
     cls = HermitianRci if hermitian else SymmetricRci
@@ -300,7 +321,7 @@ def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, devic
         kernel.abort(-104)
         return kernel.result
     if b is not None:
-        if not _is_torch(b):
+        if not _is_torch(b) and not isinstance(b, Planar):
             b = np.asarray(b)
         if _shape(b) != shp:
             kernel.abort(-106)
@@ -309,8 +330,9 @@ def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, devic
         return kernel.result
     dev = kernel.dev
     try:
-        A = _upload_full(dev, expand_uplo(a, uplo, hermitian), hermitian)
-        B = None if b is None else _upload_full(dev, expand_uplo(b, uplo, hermitian), hermitian)
+        A = _upload_full(dev, a if isinstance(a, Planar) else expand_uplo(a, uplo, hermitian), hermitian)
+        B = None if b is None else _upload_full(
+            dev, b if isinstance(b, Planar) else expand_uplo(b, uplo, hermitian), hermitian)
     except MemoryError:
         kernel.abort(-1)
         return kernel.result
@@ -329,6 +351,11 @@ def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, devic
 
 
 def _upload_full(dev, m, hermitian):
+    if isinstance(m, Planar):
+        # already device-resident planar (full storage): used as is, no copy
+        if m.cplx != hermitian or m.rows != m.cols:
+            raise ValueError("planar input must be square and complex iff hermitian")
+        return m
     if _is_torch(m):
         return dev.upload_torch(m, cplx=hermitian)
     return dev.upload(np.asarray(m), cplx=hermitian)
@@ -341,8 +368,9 @@ def _routine_name(hermitian, single, generalized):
 
 def feast_sy(a, emin, emax, m0, *, uplo="F", b=None, fpm=None, options=None, x0=None, device=None):
     """Real symmetric A x = lambda x (or A x = lambda B x) on [emin, emax]
-    (dense.py:166-173).  ``a``/``b`` may be numpy arrays or torch tensors
-    (device-resident inputs skip the host->device copy)."""
+    (dense.py:166-173).  ``a``/``b`` may be numpy arrays, torch tensors or
+    full-storage device ``Planar`` matrices (device-resident inputs skip the
+    host->device copy; a ``Planar`` is used in place)."""
     return _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, False, device)
 
 

@@ -240,6 +240,23 @@ class Device:
                                     _P(Q.re), _P(Q.im), Q.ld, float(w), float(r), float(theta))
         self.check(rc, "accumulate")
 
+    def accumulate_terms(self, terms, radius, Q: Planar):
+        """terms: [(variant, weight, theta, X: Planar)] in accumulation order."""
+        k = len(terms)
+        if k == 0:
+            return
+        ldx = terms[0][3].ld
+        if any(t[3].ld != ldx for t in terms):
+            raise ValueError("accumulate_terms: solve results must share one leading dimension")
+        var = (ctypes.c_int * k)(*[int(t[0]) for t in terms])
+        w = (ctypes.c_double * k)(*[float(t[1]) for t in terms])
+        th = (ctypes.c_double * k)(*[float(t[2]) for t in terms])
+        xr = (ctypes.c_void_p * k)(*[t[3].re for t in terms])
+        xi = (ctypes.c_void_p * k)(*[t[3].im for t in terms])
+        rc = self.lib.fb_accumulate_terms(self.h, k, var, w, float(radius), th, xr, xi, Q.rows, Q.cols, ldx,
+                                          _P(Q.re), _P(Q.im), Q.ld)
+        self.check(rc, "accumulate_terms")
+
     def symmetrize(self, M: Planar):
         self.check(self.lib.fb_symmetrize(self.h, M.rows, _P(M.re), _P(M.im), M.ld), "symmetrize")
 

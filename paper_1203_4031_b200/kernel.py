@@ -165,6 +165,8 @@ class _RciKernel:
         self._points = points          # contour indices served by this rank (None: all)
         self._q_reduce = q_reduce      # callable(Q planar) summing partial Q over ranks
         self._solve_pass = None        # callable(Y, hermitian): batched solves of a pass
+        self._pass_result = None       # callable(z, adjoint) -> Planar result of this pass, or None
+        self.solve_fused = False       # this pass's SOLVE tasks were answered by solve_pass
         scalar = np.dtype(dtype) if dtype is not None else (
             np.dtype(np.complex128) if self.hermitian else np.dtype(np.float64))
         self._single = scalar in (np.dtype(np.float32), np.dtype(np.complex64))
@@ -319,6 +321,22 @@ class _RciKernel:
         nm = self.n * self._m0_init
         self.dev.splitmix(self.seed, 0, nm, self.Y)
 
+    def _pass_terms(self, contour, points):
+        """[(variant, w, theta, X)] for every solve of this pass when the ops
+        hold all of them on the device (else None: per-point path)."""
+        if self._pass_result is None:
+            return None
+        terms = []
+        for k in points:
+            z = complex(contour.z[k])
+            for adj in ((False, True) if self.hermitian else (False,)):
+                X = self._pass_result(z, adj)
+                if X is None:
+                    return None
+                variant = (2 if adj else 1) if self.hermitian else 0
+                terms.append((variant, contour.weights[k], contour.theta[k], X))
+        return terms if 0 < len(terms) <= 64 else None
+
     def _accumulate(self, weight, radius, theta, adjoint=False):
         m0 = self.m0
         variant = (2 if adjoint else 1) if self.hermitian else 0
@@ -349,13 +367,27 @@ class _RciKernel:
             m0 = self.m0
             Q = self.Q.cols_view(0, m0)
             Q.zero_()
+            self.solve_fused = False
             if self._solve_pass is not None:
                 self._solve_pass(self.Y.cols_view(0, m0), self.hermitian)
+                terms = self._pass_terms(contour, points)
+                if terms is not None:
+                    # every point's quadrature term in one sweep over Q, same
+                    # order and arithmetic as the per-point accumulations below
+                    dev.accumulate_terms(terms, contour.radius, Q)
+                    self.solve_fused = True
             for k in points:
                 self.ze = complex(contour.z[k])
                 yield RciTask.FACTORIZE
                 if self.hermitian and not self.adjoint_capable:
                     yield RciTask.FACTORIZE_ADJOINT
+                if self.solve_fused:
+                    # the pass's solves and their accumulation are done; the
+                    # SOLVE tasks keep the RCI grammar (the pump skips them)
+                    yield RciTask.SOLVE
+                    if self.hermitian:
+                        yield RciTask.SOLVE_ADJOINT
+                    continue
                 self.W2.cols_view(0, m0).copy_from(self.Y.cols_view(0, m0))
                 yield RciTask.SOLVE
                 self._accumulate(contour.weights[k], contour.radius, contour.theta[k], False)
