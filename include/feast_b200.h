@@ -211,6 +211,15 @@ int fb_band_solve_batched(fb_ctx* ctx, int count, int n, int kl, int nrhs,
                           const double* fact_re, const double* fact_im, int64_t fact_stride,
                           const int* ipiv, int64_t ipiv_stride, const double* aux, int64_t aux_stride,
                           double* x_re, double* x_im, int64_t ldx, int64_t x_stride);
+/* Same solve with the right-hand sides read from Y (y_re/y_im at
+ * + b*y_stride; y_stride = 0: one block shared by every shift, e.g. the
+ * contour pass's Y; y_im == NULL: real Y) and the solutions written to X
+ * (_BandedOps.solve, banded.py:166-170, for all shifts of a pass at once). */
+int fb_band_solve_batched_rhs(fb_ctx* ctx, int count, int n, int kl, int nrhs,
+                              const double* fact_re, const double* fact_im, int64_t fact_stride,
+                              const int* ipiv, int64_t ipiv_stride, const double* aux, int64_t aux_stride,
+                              const double* y_re, const double* y_im, int64_t ldy, int64_t y_stride,
+                              double* x_re, double* x_im, int64_t ldx, int64_t x_stride);
 
 #ifdef __cplusplus
 }

@@ -55,6 +55,8 @@ SIGNATURES = {
     "fb_band_aux_doubles": (c_int64, [c_int, c_int]),
     "fb_band_factor_batched": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P, P, c_int64, P, P, c_int64,
                                        P, c_int64, P, c_int64, P]),
+    "fb_band_solve_batched_rhs": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
+                                          P, P, c_int64, c_int64, P, P, c_int64, c_int64]),
     "fb_band_solve_batched": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
                                       P, P, c_int64, c_int64]),
 }

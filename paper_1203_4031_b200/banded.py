@@ -209,15 +209,12 @@ class DeviceBandOps:
             if X is None or X.shape[3] != m:
                 X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
                 self._xbuf[id(bb)] = X
-            X[0].copy_(Y.plane(0).unsqueeze(0).expand(cnt, n, m))
-            if Y.cplx:
-                X[1].copy_(Y.plane(1).unsqueeze(0).expand(cnt, n, m))
-            else:
-                X[1].zero_()
             fr, fi, fs, piv, ps, aux, as_ = bb.args()
-            dev.check(dev.lib.fb_band_solve_batched(dev.h, cnt, n, self.kl, m, fr, fi, fs, piv, ps, aux, as_,
-                                                    X[0].data_ptr(), X[1].data_ptr(), m, n * m),
-                      "band_solve_batched")
+            # every shift reads the pass's Y directly (stride 0, real or planar)
+            dev.check(dev.lib.fb_band_solve_batched_rhs(dev.h, cnt, n, self.kl, m, fr, fi, fs, piv, ps, aux, as_,
+                                                        Y.re, Y.im, Y.ld, 0, X[0].data_ptr(), X[1].data_ptr(),
+                                                        m, n * m),
+                      "band_solve_batched_rhs")
             for i in range(cnt):
                 self._pass[(id(bb), i)] = (X, i)
 

@@ -26,6 +26,8 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
                               long long sa, int* info, cudaStream_t st);
 cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* wr, const double* wi, long long sw,
                              const int* ipiv, long long sp, const double* aux, long long sa, double* xr,
-                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st);
+                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st,
+                             const double* yr = nullptr, const double* yi = nullptr, long long ldy = 0,
+                             long long sy = 0);
 
 }  // namespace fb

@@ -525,7 +525,10 @@ __global__ void __launch_bounds__(RT) band_rfactor_kernel(RFArgs a) {
   }
 }
 
-// ---- interface solve: one CTA per (shift, 32-column chunk) ------------------------
+// ---- interface solve: one CTA per (shift, RS_NC-column chunk) ---------------------
+// The chain over the P-1 interfaces is sequential; narrow column chunks put
+// more CTAs on it (one (row, column) entry per thread) and shorten each step.
+constexpr int RS_NC = 8;
 struct RSArgs {
   int n, kl, P, nrhs;
   const double *sr, *si;
@@ -540,7 +543,7 @@ struct RSArgs {
 
 __global__ void __launch_bounds__(RT) band_rsolve_kernel(RSArgs a) {
   const int k = blockIdx.x, chunk = blockIdx.y, kl = a.kl, w = 2 * kl, tid = threadIdx.x;
-  const int c0 = chunk * 32, nc = min(32, a.nrhs - c0);
+  const int c0 = chunk * RS_NC, nc = min(RS_NC, a.nrhs - c0);
   const double* Sr = a.sr + k * a.ss;
   const double* Si = a.si + k * a.ss;
   const double* Dr = a.dr + k * a.sa;
@@ -681,14 +684,14 @@ __global__ void __launch_bounds__(WPB * 32) band_correct_kernel(CKArgs a) {
 // prefetch queue (the global load of a row entering the window was issued QD
 // steps earlier).  Forward (pivots + unit L) and backward (U) are separate
 // kernels so each keeps its own register window.
-constexpr int TC = 32;     // factor columns per staged chunk
+constexpr int TC = 32;     // rows per staged chunk (correction)
 constexpr int SNW = 3;     // warps per CTA (96 right-hand sides)
-constexpr int QD = 4;
 
 // One forward step with the row interchange (0 <-> P) folded in at compile
 // time: x0 = w[P]; the window slides by one as each multiply-add writes row
-// i+1's update into register i, so neither the interchange nor the slide
-// costs a move.  The caller dispatches on the warp-uniform P with a switch.
+// i+1's update into slot i.  The caller dispatches on the warp-uniform P with
+// a switch (17 straight-line bodies; measured faster than an in-place swap
+// followed by one shared body, whose register renaming costs more moves).
 template <int KL, int P>
 __device__ __forceinline__ void fwd_step(double (&wr)[KL + 1], double (&wi)[KL + 1], const double2* __restrict__ l,
                                          double& x0r, double& x0i) {
@@ -705,11 +708,18 @@ __device__ __forceinline__ void fwd_step(double (&wr)[KL + 1], double (&wi)[KL +
   }
 }
 
+// Sweeps stage SC rows per chunk: the factor columns of the chunk's rows and,
+// for every thread's column, the SC right-hand-side rows that will ENTER the
+// register window during the chunk, one chunk ahead by cp.async (no register
+// queue; the load of a row is issued ~SC steps of the whole CTA before use).
+constexpr int SC = 12;
+size_t sweep_xring_bytes(int nt) { return sizeof(double) * 2 * SC * 2 * (size_t)nt; }
+
 template <int KL>
 __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) {
   constexpr int KV = 2 * KL, LW = 3 * KL + 1;
-  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x;
-  const int col = blockIdx.y * blockDim.x + tid;
+  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, nt = blockDim.x;
+  const int col = blockIdx.y * nt + tid;
   const bool on = col < a.nrhs;
   const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
   const double* Wr = a.wr + k * a.sw;
@@ -721,47 +731,58 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
   const double* Fr = sep ? a.fr + k * a.sf : Xr;
   const double* Fi = sep ? (a.fi ? a.fi + k * a.sf : nullptr) : Xi;
   const long long ldf = sep ? a.ldf : a.ldx;
-  __shared__ double2 sl[2][TC][KL];  // multipliers (re, im) of column j
-  __shared__ int spv[2][TC];
-  auto stage = [&](int buf, int j0) {
-    for (int e = tid; e < TC * KL; e += blockDim.x) {
+  extern __shared__ double sx[];  // [2 buf][SC rows][2 planes][nt]
+  __shared__ double2 sl[2][SC][KL];  // multipliers (re, im) of column j
+  __shared__ int spv[2][SC];
+  const int xbase = lo + KL + 1;  // row entering the window at step lo
+  auto stage = [&](int buf, int c) {
+    const int j0 = lo + c * SC;
+    for (int e = tid; e < SC * KL; e += nt) {
       const int jj = e / KL, i = e % KL, j = j0 + jj;
       const bool ok = j < hi;
       const long long o = ok ? (long long)j * LW + KV + 1 + i : 0;
       cp_async8(&sl[buf][jj][i].x, Wr + o, ok);
       cp_async8(&sl[buf][jj][i].y, Wi + o, ok);
     }
-    for (int jj = tid; jj < TC; jj += blockDim.x) spv[buf][jj] = (j0 + jj < hi) ? ipiv[j0 + jj] - (j0 + jj) : 0;
+    for (int jj = tid; jj < SC; jj += nt) cp_async4(&spv[buf][jj], ipiv + min(j0 + jj, hi - 1), j0 + jj < hi);
+    double* xb = sx + (size_t)buf * SC * 2 * nt;
+#pragma unroll
+    for (int r = 0; r < SC; ++r) {
+      const int row = xbase + c * SC + r;
+      const bool ok = on && row < hi;
+      const long long o = ok ? (long long)row * ldf + col : 0;
+      cp_async8(xb + (r * 2) * nt + tid, Fr + o, ok);
+      cp_async8(xb + (r * 2 + 1) * nt + tid, Fi ? Fi + o : Fr + o, ok && Fi != nullptr);
+    }
     cp_async_commit();
   };
-  auto ld = [&](int r, double& vr, double& vi) {
-    vr = vi = 0.0;
-    if (on && r < hi) {
-      const long long o = (long long)r * ldf + col;
-      vr = __ldcs(Fr + o);
-      if (Fi) vi = __ldcs(Fi + o);
+  double wr_[KL + 1], wi_[KL + 1];
+#pragma unroll
+  for (int i = 0; i <= KL; ++i) {
+    wr_[i] = wi_[i] = 0.0;
+    if (on && lo + i < hi) {
+      const long long o = (long long)(lo + i) * ldf + col;
+      wr_[i] = Fr[o];
+      if (Fi) wi_[i] = Fi[o];
     }
-  };
-  double wr_[KL + 1], wi_[KL + 1], qr_[QD], qi_[QD];
-#pragma unroll
-  for (int i = 0; i <= KL; ++i) ld(lo + i, wr_[i], wi_[i]);
-#pragma unroll
-  for (int d = 0; d < QD; ++d) ld(lo + KL + 1 + d, qr_[d], qi_[d]);
-  stage(0, lo);
-  int buf = 0;
-  for (int j0 = lo; j0 < hi; j0 += TC, buf ^= 1) {
-    if (j0 + TC < hi) {
-      stage(buf ^ 1, j0 + TC);
+  }
+  const int nch = (hi - lo + SC - 1) / SC;
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      stage(buf ^ 1, c + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const int jn = min(TC, hi - j0);
+    const int j0 = lo + c * SC, jn = min(SC, hi - j0);
+    const double* xb = sx + (size_t)buf * SC * 2 * nt;
 #pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
       const int j = j0 + jj;
-      const int p = spv[buf][jj];
+      const int p = spv[buf][jj] - j;
       const double2* lcol = sl[buf][jj];
       double x0r, x0i;
 #define FB_FWD_CASE(I)                                                          \
@@ -780,75 +801,80 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
         Xr[o] = x0r;
         Xi[o] = x0i;
       }
-      wr_[KL] = qr_[0];
-      wi_[KL] = qi_[0];
-#pragma unroll
-      for (int d = 0; d + 1 < QD; ++d) {
-        qr_[d] = qr_[d + 1];
-        qi_[d] = qi_[d + 1];
-      }
-      ld(j + KL + 1 + QD, qr_[QD - 1], qi_[QD - 1]);
+      wr_[KL] = xb[(jj * 2) * nt + tid];
+      wi_[KL] = xb[(jj * 2 + 1) * nt + tid];
     }
     __syncthreads();
   }
 }
 
 // Backward sweep: one thread per right-hand side holds rows j-KV..j in
-// registers; the U column (re, im interleaved, 1/U_jj precomputed per chunk)
-// comes from shared memory.
+// registers; the U column (re, im interleaved, 1/U_jj computed per chunk)
+// and the rows entering the window come from shared memory.
 template <int KL>
 __global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) {
   constexpr int KV = 2 * KL, LW = 3 * KL + 1;
-  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x;
-  const int col = blockIdx.y * blockDim.x + tid;
+  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, nt = blockDim.x;
+  const int col = blockIdx.y * nt + tid;
   const bool on = col < a.nrhs;
   const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
   const double* Wr = a.wr + k * a.sw;
   const double* Wi = a.wi + k * a.sw;
   double* Xr = a.xr + k * a.sx;
   double* Xi = a.xi + k * a.sx;
-  __shared__ double2 su[2][TC][KV + 1];  // U column j (rows j-KV..j); slot KV <- 1/U_jj
-  auto stage = [&](int buf, int j1) {
-    for (int e = tid; e < TC * (KV + 1); e += blockDim.x) {
+  extern __shared__ double sx[];         // [2 buf][SC rows][2 planes][nt]
+  __shared__ double2 su[2][SC][KV + 1];  // U column j (rows j-KV..j); slot KV <- 1/U_jj
+  const int xtop = hi - 2 - KV;          // row entering the window at step hi-1
+  auto stage = [&](int buf, int c) {
+    const int j1 = hi - 1 - c * SC;
+    for (int e = tid; e < SC * (KV + 1); e += nt) {
       const int jj = e / (KV + 1), i = e % (KV + 1), j = j1 - jj;
       const bool ok = j >= lo;
       const long long o = ok ? (long long)j * LW + i : 0;
       cp_async8(&su[buf][jj][i].x, Wr + o, ok);
       cp_async8(&su[buf][jj][i].y, Wi + o, ok);
     }
+    double* xb = sx + (size_t)buf * SC * 2 * nt;
+#pragma unroll
+    for (int r = 0; r < SC; ++r) {
+      const int row = xtop - c * SC - r;
+      const bool ok = on && row >= lo;
+      const long long o = ok ? (long long)row * a.ldx + col : 0;
+      cp_async8(xb + (r * 2) * nt + tid, Xr + o, ok);
+      cp_async8(xb + (r * 2 + 1) * nt + tid, Xi + o, ok);
+    }
     cp_async_commit();
   };
-  auto ld = [&](int r, double& vr, double& vi) {
-    if (on && r >= lo && r < hi) {
+  double wr_[KV + 1], wi_[KV + 1];  // wr_[t] = row j-KV+t
+#pragma unroll
+  for (int t = 0; t <= KV; ++t) {
+    const int r = hi - 1 - KV + t;
+    wr_[t] = wi_[t] = 0.0;
+    if (on && r >= lo) {
       const long long o = (long long)r * a.ldx + col;
-      vr = __ldcs(Xr + o);
-      vi = __ldcs(Xi + o);
-    } else {
-      vr = vi = 0.0;
+      wr_[t] = Xr[o];
+      wi_[t] = Xi[o];
     }
-  };
-  double wr_[KV + 1], wi_[KV + 1], qr_[QD], qi_[QD];  // wr_[t] = row j-KV+t
-#pragma unroll
-  for (int t = 0; t <= KV; ++t) ld(hi - 1 - KV + t, wr_[t], wi_[t]);
-#pragma unroll
-  for (int d = 0; d < QD; ++d) ld(hi - 2 - KV - d, qr_[d], qi_[d]);
-  stage(0, hi - 1);
-  int buf = 0;
-  for (int j1 = hi - 1; j1 >= lo; j1 -= TC, buf ^= 1) {
-    if (j1 - TC >= lo) {
-      stage(buf ^ 1, j1 - TC);
+  }
+  const int nch = (hi - lo + SC - 1) / SC;
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      stage(buf ^ 1, c + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    for (int jj = tid; jj < TC; jj += blockDim.x) {
+    for (int jj = tid; jj < SC; jj += nt) {
       const double2 d = su[buf][jj][KV];
       const double den = d.x * d.x + d.y * d.y;
       su[buf][jj][KV] = den > 0.0 ? make_double2(d.x / den, -d.y / den) : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const int jn = min(TC, j1 - lo + 1);
+    const int j1 = hi - 1 - c * SC, jn = min(SC, j1 - lo + 1);
+    const double* xb = sx + (size_t)buf * SC * 2 * nt;
 #pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
       const int j = j1 - jj;
@@ -867,14 +893,8 @@ __global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) 
         Xr[o] = qr;
         Xi[o] = qi;
       }
-      wr_[0] = qr_[0];
-      wi_[0] = qi_[0];
-#pragma unroll
-      for (int d = 0; d + 1 < QD; ++d) {
-        qr_[d] = qr_[d + 1];
-        qi_[d] = qi_[d + 1];
-      }
-      ld(j - 2 - KV - (QD - 1), qr_[QD - 1], qi_[QD - 1]);
+      wr_[0] = xb[(jj * 2) * nt + tid];
+      wi_[0] = xb[(jj * 2 + 1) * nt + tid];
     }
     __syncthreads();
   }
@@ -986,8 +1006,16 @@ CkFn correct_fn(int kl) {
 cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
   const int nw = std::min(SNW, ceil_div(ps.nrhs, 32));
   const dim3 grid(ps.P, ceil_div(ps.nrhs, 32 * nw), count);
-  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, 0, st>>>(ps);
-  psolve_bwd_fn(ps.kl)<<<grid, 32 * nw, 0, st>>>(ps);
+  const size_t smem = sweep_xring_bytes(32 * nw);
+  static bool cfg[KLMAX + 1] = {};
+  if (!cfg[ps.kl]) {  // sized for the widest CTA (SNW warps)
+    const int mx = (int)sweep_xring_bytes(32 * SNW);
+    cudaFuncSetAttribute(psolve_fwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(psolve_bwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cfg[ps.kl] = true;
+  }
+  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, smem, st>>>(ps);
+  psolve_bwd_fn(ps.kl)<<<grid, 32 * nw, smem, st>>>(ps);
   count_launch(2);
   return cudaGetLastError();
 }
@@ -1089,15 +1117,17 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
 
 cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* wr, const double* wi, long long sw,
                              const int* ipiv, long long sp, const double* aux, long long sa, double* xr,
-                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st) {
+                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st,
+                             const double* yr, const double* yi, long long ldy, long long sy_) {
   if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
   if (!band_spike_ok(kl)) return cudaErrorInvalidValue;
   const int P = band_spike_parts(n, kl);
-  const int chunks = ceil_div(nrhs, 32);
+  const int chunks = ceil_div(nrhs, RS_NC);
   PSArgs ps{};
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = nrhs;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
   ps.xr = xr; ps.xi = xi; ps.ldx = ldx; ps.sx = sx;
+  ps.fr = yr; ps.fi = yi; ps.ldf = ldy; ps.sf = sy_;
   cudaError_t e;
   if ((e = psolve_launch(ps, count, st))) return e;
   if (P == 1) return cudaSuccess;

@@ -439,6 +439,21 @@ int fb_band_solve_batched(fb_ctx* c, int count, int n, int kl, int nrhs, const d
                  "band_solve_batched");
 }
 
+int fb_band_solve_batched_rhs(fb_ctx* c, int count, int n, int kl, int nrhs, const double* fr, const double* fi,
+                              int64_t fs, const int* ipiv, int64_t ps, const double* aux, int64_t as,
+                              const double* yr, const double* yi, int64_t ldy, int64_t ys, double* xr, double* xi,
+                              int64_t ldx, int64_t xs) {
+  CTX_GUARD(c);
+  if (count < 0 || count > 64 || n < 0 || nrhs < 0 || !fb::band_spike_ok(kl) || !fr || !fi || !ipiv || !aux ||
+      !xr || !xi || !yr)
+    return FB_ERR_ARG;
+  int r = ensure_scratch(c, sizeof(double) * fb::band_spike_solve_scratch_doubles(n, kl, nrhs, count));
+  if (r) return r;
+  return set_err(c, fb::band_spike_solve(count, n, kl, nrhs, fr, fi, fs, ipiv, ps, aux, as, xr, xi, ldx, xs,
+                                         (double*)c->scratch, c->stream, yr, yi, ldy, ys),
+                 "band_solve_batched_rhs");
+}
+
 // Debug only (not part of the ABI header): partition size target of the
 // SPIKE band path (tests force many partitions at small n); returns P.
 int fb_debug_band_part_target(int target, int n, int kl) {

@@ -69,6 +69,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pre
   int src = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int src = pred ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+}
 // 16-byte L2-only copy; bytes past src_bytes (0, 8 or 16) are zero-filled
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
