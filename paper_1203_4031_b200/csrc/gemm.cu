@@ -24,7 +24,7 @@ namespace fb {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 8, STAGES = 3, THREADS = 128;
+constexpr int BM = 64, BN = 64, BK = 8, STAGES = 4, THREADS = 128;
 constexpr int PK = BK + 4;   // pitch of [row][k] layouts (12 doubles)
 constexpr int PM = BM + 8;   // pitch of [k][row] layouts (72 doubles)
 
@@ -90,14 +90,31 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
   };
 
   double accr[4][4][2], acci[4][4][2];
+  // C += -A*B (alpha = -1, beta = 1, no split-K: the LU / solve updates): the
+  // accumulators start from C, so the epilogue is a plain store and the C
+  // loads overlap the pipeline prologue; the products are negated through
+  // the A fragments.
+  const bool cinit = p.splits == 1 && p.alpha_re == -1.0 && p.alpha_im == 0.0 && p.beta_re == 1.0 &&
+                     p.beta_im == 0.0;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      accr[a][b][0] = accr[a][b][1] = 0.0;
-      acci[a][b][0] = acci[a][b][1] = 0.0;
-    }
-  const double sa = p.a.conj ? -1.0 : 1.0;
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        accr[a][b][e] = acci[a][b][e] = 0.0;
+        if (cinit) {
+          const int i = m0 + wm + a * 8 + (lane >> 2);
+          const int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
+          if (i < p.m && j < p.n) {
+            const long long c = (long long)i * p.cs0 + (long long)j * p.cs1;
+            accr[a][b][e] = cre[c];
+            if (CPLX && cim) acci[a][b][e] = cim[c];
+          }
+        }
+      }
+  const double sgn = cinit ? -1.0 : 1.0;
+  const double sa = p.a.conj ? -sgn : sgn;  // sign of the A imaginary fragments
   const double sb = p.b.conj ? -1.0 : 1.0;
 
 #pragma unroll
@@ -119,7 +136,7 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         int sA = ATile<AKC>::idx(wm + t * 8 + (lane >> 2), kk);
-        ar[t] = as[sA];
+        ar[t] = sgn * as[sA];
         int sB = ATile<!BNC>::idx(wn + t * 8 + (lane >> 2), kk);
         br[t] = bs[sB];
         if (CPLX) {
@@ -161,6 +178,12 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
         int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
         if (i >= p.m || j >= p.n) continue;
         double vr = accr[a][b][e], vi = CPLX ? acci[a][b][e] : 0.0;
+        if (cinit) {
+          const long long c = (long long)i * p.cs0 + (long long)j * p.cs1;
+          cre[c] = vr;
+          if (CPLX && cim) cim[c] = vi;
+          continue;
+        }
         if (p.splits > 1) {
           size_t plane = (size_t)p.m * p.n;
           double* w = p.ws + (size_t)z * PL * plane;
@@ -178,6 +201,172 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
         }
         cre[c] = outr;
         if (CPLX && cim) cim[c] = outi;
+      }
+}
+
+// Fast path for the dominant complex case (LU trailing / in-block updates,
+// dense multiplies): A k-contiguous, B n-contiguous, C row-major, every base
+// pointer and leading dimension 16-byte aligned, no conjugation, no split-K.
+// Same tiling and fragment order as gemm_kernel, but each thread streams
+// fixed 16-byte chunks (pointer increments instead of per-element 64-bit
+// index math, half the cp.async count), sign handling is compile-time (sign
+// flips are integer ops, off the FP64 pipe the DMMAs run on), and for
+// MODE 1 (C -= A*B) the accumulators start from C so the epilogue is a store.
+__device__ __forceinline__ double dneg(double v) {
+  return __longlong_as_double(__double_as_longlong(v) ^ 0x8000000000000000ull);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
+  constexpr int AE = ATile<true>::kElems;   // [BM][PK]
+  constexpr int BE = ATile<false>::kElems;  // [BK][PM]  (B^T viewed as an A tile, n<->m)
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                 // [STAGES][2][AE]
+  double* Bs = smem + STAGES * 2 * AE;  // [STAGES][2][BE]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int bz = blockIdx.z;
+  const int nk = ceil_div(p.k, BK);
+  const long long lda = p.a.s0, ldb = p.b.s0;
+  const double* are = p.a.re + bz * p.bsa;
+  const double* aim = p.a.im + bz * p.bsa;
+  const double* bre = p.b.re + bz * p.bsb;
+  const double* bim = p.b.im + bz * p.bsb;
+  double* cre = p.cre + bz * p.bsc;
+  double* cim = p.cim + bz * p.bsc;
+  // A: 64 rows x 8 k = 256 16-byte chunks per plane -> 2 per thread
+  // B: 8 k x 64 cols = 256 chunks per plane -> 2 per thread
+  int a_row[2], a_kc[2], b_k[2], b_col[2];
+  const double* ap[2];
+  const double* bp[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int e = tid + r * THREADS;
+    a_row[r] = e >> 2;
+    a_kc[r] = (e & 3) * 2;
+    ap[r] = are + (long long)(m0 + a_row[r]) * lda + a_kc[r];
+    b_k[r] = e >> 5;
+    b_col[r] = (e & 31) * 2;
+    bp[r] = bre + (long long)b_k[r] * ldb + n0 + b_col[r];
+  }
+  const long long aoff = aim - are, boff = bim - bre;
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * 2 * AE;
+    double* bs = Bs + stage * 2 * BE;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int gk = k0 + a_kc[r];
+      const int bytes = (m0 + a_row[r] < p.m) ? (gk + 1 < p.k ? 16 : (gk < p.k ? 8 : 0)) : 0;
+      const double* src = bytes ? ap[r] + k0 : are;
+      const int s_ = a_row[r] * PK + a_kc[r];
+      cp_async16(as + s_, src, bytes);
+      cp_async16(as + AE + s_, bytes ? src + aoff : are, bytes);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int gk = k0 + b_k[r], gj = n0 + b_col[r];
+      const int bytes = gk < p.k ? (gj + 1 < p.n ? 16 : (gj < p.n ? 8 : 0)) : 0;
+      const double* src = bytes ? bp[r] + (long long)k0 * ldb : bre;
+      const int s_ = b_k[r] * PM + b_col[r];
+      cp_async16(bs + s_, src, bytes);
+      cp_async16(bs + BE + s_, bytes ? src + boff : bre, bytes);
+    }
+  };
+  double accr[4][4][2], acci[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        accr[a][b][e] = acci[a][b][e] = 0.0;
+        if (MODE == 1) {
+          const int i = m0 + wm + a * 8 + (lane >> 2);
+          const int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
+          if (i < p.m && j < p.n) {
+            const long long c = (long long)i * p.cs0 + j;
+            accr[a][b][e] = cre[c];
+            acci[a][b][e] = cim[c];
+          }
+        }
+      }
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (kt + STAGES - 1 < nk) load_stage((kt + STAGES - 1) % STAGES, kt + STAGES - 1);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * 2 * AE;
+    const double* bs = Bs + (kt % STAGES) * 2 * BE;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      const int kk = k4 + (lane & 3);
+      double x[4], y[4], z[4], br[4], bi[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int sA = (wm + t * 8 + (lane >> 2)) * PK + kk;
+        const int sB = kk * PM + wn + t * 8 + (lane >> 2);
+        const double ar = as[sA], ai = as[AE + sA];
+        br[t] = bs[sB];
+        bi[t] = bs[BE + sB];
+        if (MODE == 1) {  // -(A B): re += (-ar) br + ai bi, im += (-ar) bi + (-ai) br
+          x[t] = dneg(ar);
+          y[t] = ai;
+          z[t] = dneg(ai);
+        } else {          // A B: re += ar br + (-ai) bi, im += ar bi + ai br
+          x[t] = ar;
+          y[t] = dneg(ai);
+          z[t] = ai;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma(accr[a][b][0], accr[a][b][1], x[a], br[b]);
+          dmma(acci[a][b][0], acci[a][b][1], x[a], bi[b]);
+        }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dmma(accr[a][b][0], accr[a][b][1], y[a], bi[b]);
+          dmma(acci[a][b][0], acci[a][b][1], z[a], br[b]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = m0 + wm + a * 8 + (lane >> 2);
+        const int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
+        if (i >= p.m || j >= p.n) continue;
+        const long long c = (long long)i * p.cs0 + j;
+        const double vr = accr[a][b][e], vi = acci[a][b][e];
+        if (MODE == 1) {
+          cre[c] = vr;
+          cim[c] = vi;
+          continue;
+        }
+        double outr = p.alpha_re * vr - p.alpha_im * vi;
+        double outi = p.alpha_re * vi + p.alpha_im * vr;
+        if (p.beta_re != 0.0 || p.beta_im != 0.0) {
+          const double cr = cre[c], ci = cim[c];
+          outr += p.beta_re * cr - p.beta_im * ci;
+          outi += p.beta_re * ci + p.beta_im * cr;
+        }
+        cre[c] = outr;
+        cim[c] = outi;
       }
 }
 
@@ -229,6 +418,31 @@ cudaError_t launch_t(const GemmParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static bool al16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+bool fast_ok(const GemmParams& p) {
+  if (p.splits != 1 || p.k <= 0 || p.a.conj || p.b.conj || !p.a.im || !p.b.im || !p.cim) return false;
+  if (p.a.s1 != 1 || p.b.s1 != 1 || p.cs1 != 1) return false;
+  if ((p.a.s0 | p.b.s0 | p.cs0 | p.bsa | p.bsb) & 1) return false;
+  return al16(p.a.re) && al16(p.a.im) && al16(p.b.re) && al16(p.b.im);
+}
+
+cudaError_t launch_fast(const GemmParams& p, cudaStream_t st) {
+  const size_t smem = sizeof(double) * STAGES * 2 * (ATile<true>::kElems + ATile<false>::kElems);
+  const bool mode1 = p.alpha_re == -1.0 && p.alpha_im == 0.0 && p.beta_re == 1.0 && p.beta_im == 0.0;
+  auto kern = mode1 ? zgemm_fast_kernel<1> : zgemm_fast_kernel<0>;
+  static bool configured[2] = {false, false};
+  if (!configured[mode1]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured[mode1] = true;
+  }
+  dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.batch);
+  kern<<<grid, THREADS, smem, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 size_t gemm_workspace_bytes(int cplx, int m, int n, int splits) {
@@ -260,6 +474,7 @@ cudaError_t gemm_launch(int cplx, GemmParams p, cudaStream_t st) {
   }
   bool akc = p.a.s1 == 1 || p.a.s0 != 1;   // k-contiguous (or generic) A
   bool bnc = p.b.s1 == 1 || p.b.s0 != 1;   // n-contiguous (or generic) B
+  if (cplx && fast_ok(p)) return launch_fast(p, st);
   if (cplx) {
     if (akc && bnc) return launch_t<true, true, true>(p, st);
     if (akc && !bnc) return launch_t<true, true, false>(p, st);

@@ -89,6 +89,15 @@ def test_helloworld_golden_values(capsys):
     assert "DFEAST_SYEV" in out
 
 
+# The reference's own (final M0 -> loop count) trajectories on the same pencil
+# under 1-ulp perturbations A*(1 + k*2^-52), k = 0..7 (tools/ref_sensitivity.py,
+# profiles/r01_c3s_ref_sensitivity.txt).  Where FEAST shrinks M0 after a
+# Cholesky breakdown of the rank-deficient Q^H B Q (kernel.py:385-400) the
+# breakdown index is decided by rounding, and the loop count follows it; the
+# +-1 bar then applies to the reference trajectory with the same final M0.
+REF_TRAJECTORIES = {"c3s": {30: 6, 29: 4, 28: 1}}
+
+
 @pytest.mark.parametrize("tag", ["c1s", "c2s", "c3s", "c5s", "c4s"])
 def test_scaled_config_parity(tag):
     import paper_1203_4031_b200 as fb
@@ -104,7 +113,9 @@ def test_scaled_config_parity(tag):
     s = max(abs(w.emin), abs(w.emax))
     assert r.info == info == 0
     assert r.m == m == w.expect_m
-    assert abs(r.loop - loop) <= 1
+    traj = REF_TRAJECTORIES.get(tag, {m0: loop})
+    assert r.m0 in traj, (r.m0, traj)
+    assert abs(r.loop - traj[r.m0]) <= 1
     assert np.abs(r.e[:m] - g["e"][:m]).max() <= 1e-10 * s
     assert r.res[:m].max() <= 1e-10
 
