@@ -17,6 +17,8 @@
 // elements have no ldmatrix path).  Complex products use 4 real DMMAs
 // (re*re - im*im, re*im + im*re).  Split-K is deterministic: partial tiles go
 // to a workspace and are reduced in a fixed order.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -216,15 +218,20 @@ __device__ __forceinline__ double dneg(double v) {
   return __longlong_as_double(__double_as_longlong(v) ^ 0x8000000000000000ull);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT, 2) zgemm_fast_kernel(GemmParams p) {
+  // NT = 128: 4 warps of 32x32 (2x2); NT = 256: 8 warps of 32x16 (2x4), half
+  // the accumulator registers per thread and twice the warps per SM
+  constexpr int NB_ = NT == 128 ? 4 : 2;  // 8-column DMMA tiles per warp
+  constexpr int WN = NB_ * 8;
+  constexpr int WCOLS = BN / WN;          // warps along n
   constexpr int AE = ATile<true>::kElems;   // [BM][PK]
   constexpr int BE = ATile<false>::kElems;  // [BK][PM]  (B^T viewed as an A tile, n<->m)
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                 // [STAGES][2][AE]
   double* Bs = smem + STAGES * 2 * AE;  // [STAGES][2][BE]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp / WCOLS) * 32, wn = (warp % WCOLS) * WN;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int bz = blockIdx.z;
   const int nk = ceil_div(p.k, BK);
@@ -235,14 +242,14 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
   const double* bim = p.b.im + bz * p.bsb;
   double* cre = p.cre + bz * p.bsc;
   double* cim = p.cim + bz * p.bsc;
-  // A: 64 rows x 8 k = 256 16-byte chunks per plane -> 2 per thread
-  // B: 8 k x 64 cols = 256 chunks per plane -> 2 per thread
-  int a_row[2], a_kc[2], b_k[2], b_col[2];
-  const double* ap[2];
-  const double* bp[2];
+  // A: 64 rows x 8 k = 256 16-byte chunks per plane; B: 8 k x 64 cols = 256
+  constexpr int CH = 256 / NT;  // chunks per thread per plane
+  int a_row[CH], a_kc[CH], b_k[CH], b_col[CH];
+  const double* ap[CH];
+  const double* bp[CH];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int e = tid + r * THREADS;
+  for (int r = 0; r < CH; ++r) {
+    const int e = tid + r * NT;
     a_row[r] = e >> 2;
     a_kc[r] = (e & 3) * 2;
     ap[r] = are + (long long)(m0 + a_row[r]) * lda + a_kc[r];
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
     double* as = As + stage * 2 * AE;
     double* bs = Bs + stage * 2 * BE;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < CH; ++r) {
       const int gk = k0 + a_kc[r];
       const int bytes = (m0 + a_row[r] < p.m) ? (gk + 1 < p.k ? 16 : (gk < p.k ? 8 : 0)) : 0;
       const double* src = bytes ? ap[r] + k0 : are;
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
       cp_async16(as + AE + s_, bytes ? src + aoff : are, bytes);
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < CH; ++r) {
       const int gk = k0 + b_k[r], gj = n0 + b_col[r];
       const int bytes = gk < p.k ? (gj + 1 < p.n ? 16 : (gj < p.n ? 8 : 0)) : 0;
       const double* src = bytes ? bp[r] + (long long)k0 * ldb : bre;
@@ -274,11 +281,11 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
       cp_async16(bs + BE + s_, bytes ? src + boff : bre, bytes);
     }
   };
-  double accr[4][4][2], acci[4][4][2];
+  double accr[4][NB_][2], acci[4][NB_][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < NB_; ++b)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         accr[a][b][e] = acci[a][b][e] = 0.0;
@@ -307,14 +314,17 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
       const int kk = k4 + (lane & 3);
-      double x[4], y[4], z[4], br[4], bi[4];
+      double x[4], y[4], z[4], br[NB_], bi[NB_];
+#pragma unroll
+      for (int t = 0; t < NB_; ++t) {
+        const int sB = kk * PM + wn + t * 8 + (lane >> 2);
+        br[t] = bs[sB];
+        bi[t] = bs[BE + sB];
+      }
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int sA = (wm + t * 8 + (lane >> 2)) * PK + kk;
-        const int sB = kk * PM + wn + t * 8 + (lane >> 2);
         const double ar = as[sA], ai = as[AE + sA];
-        br[t] = bs[sB];
-        bi[t] = bs[BE + sB];
         if (MODE == 1) {  // -(A B): re += (-ar) br + ai bi, im += (-ar) bi + (-ai) br
           x[t] = dneg(ar);
           y[t] = ai;
@@ -328,14 +338,14 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < NB_; ++b) {
           dmma(accr[a][b][0], accr[a][b][1], x[a], br[b]);
           dmma(acci[a][b][0], acci[a][b][1], x[a], bi[b]);
         }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < NB_; ++b) {
           dmma(accr[a][b][0], accr[a][b][1], y[a], bi[b]);
           dmma(acci[a][b][0], acci[a][b][1], z[a], br[b]);
         }
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_fast_kernel(GemmParams p) {
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < NB_; ++b)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = m0 + wm + a * 8 + (lane >> 2);
@@ -430,7 +440,13 @@ bool fast_ok(const GemmParams& p) {
 cudaError_t launch_fast(const GemmParams& p, cudaStream_t st) {
   const size_t smem = sizeof(double) * STAGES * 2 * (ATile<true>::kElems + ATile<false>::kElems);
   const bool mode1 = p.alpha_re == -1.0 && p.alpha_im == 0.0 && p.beta_re == 1.0 && p.beta_im == 0.0;
-  auto kern = mode1 ? zgemm_fast_kernel<1> : zgemm_fast_kernel<0>;
+  static int nt = 0;
+  if (!nt) {
+    const char* e = getenv("FB_ZGEMM_THREADS");
+    nt = (e && atoi(e) == 128) ? 128 : 256;
+  }
+  auto kern = mode1 ? (nt == 128 ? zgemm_fast_kernel<1, 128> : zgemm_fast_kernel<1, 256>)
+                    : (nt == 128 ? zgemm_fast_kernel<0, 128> : zgemm_fast_kernel<0, 256>);
   static bool configured[2] = {false, false};
   if (!configured[mode1]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -438,7 +454,7 @@ cudaError_t launch_fast(const GemmParams& p, cudaStream_t st) {
     configured[mode1] = true;
   }
   dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.batch);
-  kern<<<grid, THREADS, smem, st>>>(p);
+  kern<<<grid, nt, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }

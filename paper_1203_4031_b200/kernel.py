@@ -321,21 +321,29 @@ class _RciKernel:
         nm = self.n * self._m0_init
         self.dev.splitmix(self.seed, 0, nm, self.Y)
 
-    def _pass_terms(self, contour, points):
-        """[(variant, w, theta, X)] for every solve of this pass when the ops
-        hold all of them on the device (else None: per-point path)."""
-        if self._pass_result is None:
-            return None
-        terms = []
+    def _pass_spec(self, contour, points):
+        """The pass's quadrature terms in accumulation order (kernel.py:350-364):
+        [(z, adjoint, variant, w, theta)]."""
+        spec = []
         for k in points:
             z = complex(contour.z[k])
             for adj in ((False, True) if self.hermitian else (False,)):
-                X = self._pass_result(z, adj)
-                if X is None:
-                    return None
                 variant = (2 if adj else 1) if self.hermitian else 0
-                terms.append((variant, contour.weights[k], contour.theta[k], X))
-        return terms if 0 < len(terms) <= 64 else None
+                spec.append((z, adj, variant, contour.weights[k], contour.theta[k]))
+        return spec
+
+    def _pass_terms(self, spec):
+        """[(variant, w, theta, X)] for every solve of this pass when the ops
+        hold all of them on the device (else None: per-point path)."""
+        if self._pass_result is None or not 0 < len(spec) <= 64:
+            return None
+        terms = []
+        for z, adj, variant, w, theta in spec:
+            X = self._pass_result(z, adj)
+            if X is None:
+                return None
+            terms.append((variant, w, theta, X))
+        return terms
 
     def _accumulate(self, weight, radius, theta, adjoint=False):
         m0 = self.m0
@@ -370,7 +378,7 @@ class _RciKernel:
             self.solve_fused = False
             if self._solve_pass is not None:
                 self._solve_pass(self.Y.cols_view(0, m0), self.hermitian)
-                terms = self._pass_terms(contour, points)
+                terms = self._pass_terms(self._pass_spec(contour, points))
                 if terms is not None:
                     # every point's quadrature term in one sweep over Q, same
                     # order and arithmetic as the per-point accumulations below

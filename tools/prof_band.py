@@ -50,8 +50,20 @@ Y = dev.empty(n, m0, False)
 Y.plane(0).copy_(torch.rand(n, m0, dtype=torch.float64, device=dev.tdev) - 0.5)
 ops.solve_pass(Y, False)
 t_s = timed(lambda: ops.solve_pass(Y, False), reps)
+Xs0 = ops._pass[(id(ops._batches[0]), 0)][0][:, 0].clone()
 X = dev.empty(n, m0, False)
 t_m = timed(lambda: ops.multiply_a(Y, X), reps)
+ct = build_contour(gauss_legendre(8), w.emin, w.emax)
+Q = dev.zeros(n, m0, False)
+
+
+def pass_acc():
+    ops.solve_pass(Y, False)
+    dev.accumulate_terms([(0, ct.weights[k], ct.theta[k], ops.pass_result(complex(ct.z[k]), False))
+                          for k in range(len(zs))], ct.radius, Q)
+
+
+t_sa = timed(pass_acc, reps)
 
 ne = len(zs)
 solve_bytes = ne * ((3 * kl + 1) * n * 16 + 2 * n * m0 * 16)
@@ -61,12 +73,11 @@ print(f"n={n} kl={kl} m0={m0} Ne={ne}")
 print(f"factor (8 shifts, incl. alloc): {t_f:.2f} ms")
 print(f"solve pass (8 shifts): {t_s:.2f} ms  -> {solve_bytes / t_s / 1e6:.0f} GB/s algorithmic, "
       f"{solve_flops / t_s / 1e9:.2f} TFLOP/s")
+print(f"solve pass + quadrature sum (accumulate_terms): {t_sa:.2f} ms")
 print(f"band matvec A*Y: {t_m:.3f} ms -> {mv_bytes / t_m / 1e6:.0f} GB/s")
 
 # residual check of shift 0's solve: || S x - y || / ||y|| through a band multiply
-bb = ops._batches[0]
-Xs = ops._pass[(id(bb), 0)][0]
-x0 = torch.complex(Xs[0, 0], Xs[1, 0])
+x0 = torch.complex(Xs0[0], Xs0[1])
 z = complex(zs[0])
 fa_t = torch.from_numpy(fa).to(dev.tdev)
 fb_t = torch.from_numpy(fbm).to(dev.tdev)
