@@ -36,7 +36,15 @@ namespace fb {
 namespace {
 
 constexpr int PW = 32;                 // sub-panel width (= diagonal block size of dinv)
-constexpr int NB = 128;                // outer block (trailing-update K)
+static int outer_nb() {                // outer block (trailing-update K), FB_LU_NB overrides
+  static int nb = 0;
+  if (!nb) {
+    const char* e = getenv("FB_LU_NB");
+    nb = e ? atoi(e) : 128;
+    if (nb < 32 || nb % 32) nb = 128;
+  }
+  return nb;
+}
 constexpr int LIST = 1 + 2 * 2 * PW;   // per-block swap list: cnt, dst[2PW], src[2PW]
 
 // S_b = z_b B - A (B == nullptr: identity); item b = blockIdx.y.
@@ -249,6 +257,7 @@ static cudaError_t swap_list_launch(const LuBatch& f, int ca, int cb, int cc, in
 cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t st, const LuStreams* ls) {
   cudaError_t e;
   if (n <= 0 || f.count <= 0) return cudaSuccess;
+  const int NB = outer_nb();
   const int B = f.count;
   const long long ld = f.ld, slu = f.slu, sd = f.sdinv;
   double* re = f.re;

@@ -757,7 +757,12 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
   count_launch();
   if (rows <= rpc_cluster || (g_cluster_ok && rows <= max_cluster * rpc_cluster)) {
     int G = std::max(1, std::min(max_cluster, ceil_div(rows, rpc_cluster)));
-    if (rows > 2 * PW) G = std::max(G, std::min(max_cluster, ceil_div(rows, 192)));
+    static int rmin = 0;
+    if (!rmin) {
+      const char* e = getenv("FB_PANEL_RPC");
+      rmin = e ? std::max(64, std::min(rpc_cluster, atoi(e))) : 192;
+    }
+    if (rows > 2 * PW) G = std::max(G, std::min(max_cluster, ceil_div(rows, rmin)));
     G = std::max(1, std::min(G, rows / PW));
     int rpc = ceil_div(rows, G);
     G = ceil_div(rows, rpc);

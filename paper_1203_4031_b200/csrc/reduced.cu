@@ -125,9 +125,13 @@ __device__ void tridiag_bisect_invit(int m, const double* d, const double* e, do
     while (kend < m && eps[kend] - eps[kend - 1] <= ortol) ++kend;
     double* W = Wk + (size_t)k * 6 * m;
     double *u0 = W, *u1 = W + m, *u2 = W + 2 * m, *lm = W + 3 * m, *sw = W + 4 * m, *y = W + 5 * m;
+    double lam = 0.0;
     for (int j = k; j < kend; ++j) {
-      // perturb coincident eigenvalues inside a cluster so the factors differ
-      const double lam = eps[j] + (double)(j - k) * 10.0 * ulp * tnorm;
+      // separate (nearly) coincident eigenvalues by 10 ulp of the eigenvalue
+      // itself, as LAPACK dstein does: a norm-relative step would move the
+      // small Ritz values of a graded (ill-conditioned B_Q) pencil far off
+      const double pert = 10.0 * ulp * fabs(eps[j]);
+      lam = (j > k && eps[j] - lam < pert) ? lam + pert : eps[j];
       // LU with partial pivoting of T - lam I (U has two superdiagonals)
       double c0 = d[0] - lam, c1 = m > 1 ? e[0] : 0.0, c2 = 0.0;
       for (int i = 0; i + 1 < m; ++i) {

@@ -111,9 +111,11 @@ def main():
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     s = max(abs(emin), abs(emax))
-    rep = {"info": int(r.info), "m": int(r.m), "loop": int(r.loop), "seconds": dt,
+    rep = {"info": int(r.info), "m": int(r.m), "m0_final": int(r.m0), "loop": int(r.loop), "seconds": dt,
            "it_per_s": (r.loop + 1) / dt, "factorizations": int(getattr(r, "factorizations", -1)),
            "max_res": float(np.max(r.res[:r.m])) if r.m else None, "epsout": float(r.epsout)}
+    rep["e_all"] = [float(v) for v in r.e[:r.m0]]
+    rep["res_all"] = [float(v) for v in r.res[:r.m0]]
     if "inertia_count" in report:
         rep["count_inertia"] = report["inertia_count"]
     X = r.x[:, :r.m] if r.m else None
