@@ -205,18 +205,19 @@ class DeviceBandOps:
         dev, n, m = self.dev, self.n, Y.cols
         for bb in self._batches:
             cnt = bb.count
+            mp = m + (m & 1)   # even leading dimension: 16-byte correction GEMM rows
             X = self._xbuf.get(id(bb))
-            if X is None or X.shape[3] != m:
-                X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+            if X is None or X.shape[3] != mp:
+                X = dev.torch.empty((2, cnt, n, mp), dtype=dev.torch.float64, device=dev.tdev)
                 self._xbuf[id(bb)] = X
             fr, fi, fs, piv, ps, aux, as_ = bb.args()
             # every shift reads the pass's Y directly (stride 0, real or planar)
             dev.check(dev.lib.fb_band_solve_batched_rhs(dev.h, cnt, n, self.kl, m, fr, fi, fs, piv, ps, aux, as_,
                                                         Y.re, Y.im, Y.ld, 0, X[0].data_ptr(), X[1].data_ptr(),
-                                                        m, n * m),
+                                                        mp, n * mp),
                       "band_solve_batched_rhs")
             for i in range(cnt):
-                self._pass[(id(bb), i)] = (X, i)
+                self._pass[(id(bb), i)] = (X, i, m)
 
     def pass_result(self, z, adjoint):
         """Planar view of this pass's solve for shift z (A^H: the conj(z) factor)."""
@@ -227,13 +228,13 @@ class DeviceBandOps:
         got = self._pass.get((id(hit[0]), hit[1]))
         if got is None:
             return None
-        X, i = got
-        return Planar(X[:, i], True, X.shape[2], X.shape[3], X.shape[3])
+        X, i, m = got
+        return Planar(X[:, i], True, X.shape[2], m, X.shape[3])
 
     def _solve_batched(self, f, W: Planar):
         hit = self._pass.get((id(f.batch), f.idx))
         if hit is not None:
-            X, i = hit
+            X, i, _ = hit
             W.plane(0).copy_(X[0, i][:, :W.cols])
             W.plane(1).copy_(X[1, i][:, :W.cols])
             return

@@ -35,6 +35,7 @@
 
 #include "band.cuh"
 #include "common.cuh"
+#include "gemm.cuh"
 
 namespace fb {
 
@@ -48,7 +49,13 @@ struct Zs {
   double r[64], i[64];
 };
 
-__host__ __device__ __forceinline__ int part_lo(int j, int n, int P) { return (int)((long long)j * n / P); }
+// Partitions of equal size sz = ceil(n / P) (the last one shorter; P is chosen
+// so that it still holds > 2kl rows): equal strides let the spike correction
+// run as one strided-batch ZGEMM over the partitions.
+__host__ __device__ __forceinline__ int part_sz(int n, int P) { return (n + P - 1) / P; }
+__host__ __device__ __forceinline__ int part_lo(int j, int n, int P) {
+  return (int)min((long long)n, (long long)j * part_sz(n, P));
+}
 
 // S[r][c] of z*FB - FA inside partition [lo, hi) (zero outside it or the band),
 // with the rounding of band_shift_kernel (numpy order, banded.py:158-163)
@@ -676,6 +683,40 @@ __global__ void __launch_bounds__(WPB * 32) band_correct_kernel(CKArgs a) {
   }
 }
 
+// ---- tips of partition j in spike-column order: T_j = [x_{j+1}^t ; x_{j-1}^b] ----------
+// (zero where the neighbour does not exist), so that the correction of every
+// partition is one product X_j -= [V_j W_j] T_j.  Item k = blockIdx.y.
+struct TGArgs {
+  int kl, P, nrhs;
+  const double *yr, *yi;
+  long long sy;
+  double *tr, *ti;
+  long long st;
+};
+__global__ void band_tips_kernel(TGArgs a) {
+  const int k = blockIdx.y, w = 2 * a.kl;
+  const long long tot = (long long)a.P * w * a.nrhs;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(e % a.nrhs);
+    const long long rq = e / a.nrhs;
+    const int q = (int)(rq % w), j = (int)(rq / w);
+    double vr = 0.0, vi = 0.0;
+    long long o = -1;
+    if (q < a.kl) {
+      if (j + 1 < a.P) o = ((long long)j * w + a.kl + q) * a.nrhs + c;        // y_j[kl + q]
+    } else if (j > 0) {
+      o = ((long long)(j - 1) * w + (q - a.kl)) * a.nrhs + c;                  // y_{j-1}[q - kl]
+    }
+    if (o >= 0) {
+      vr = a.yr[k * a.sy + o];
+      vi = a.yi[k * a.sy + o];
+    }
+    a.tr[k * a.st + e] = vr;
+    a.ti[k * a.st + e] = vi;
+  }
+}
+
 // ---- staged partition solves: one CTA per (partition, column block, shift) -------
 // All warps of a CTA share the factor columns, staged through shared memory in
 // chunks of TC columns by cp.async (double-buffered) with re/im interleaved so
@@ -1034,6 +1075,8 @@ int band_spike_parts(int n, int kl) {
   const int minsz = std::max(2 * kl + 1, std::min(64, g_part_target));
   int P = (n + g_part_target - 1) / g_part_target;
   P = std::min(P, std::max(1, n / std::max(1, minsz)));
+  // every partition, the shorter last one included, keeps >= minsz rows
+  while (P > 1 && n - (P - 1) * part_sz(n, P) < minsz) --P;
   return std::max(1, P);
 }
 
@@ -1046,7 +1089,8 @@ size_t band_spike_aux_doubles(int n, int kl) {
 
 size_t band_spike_solve_scratch_doubles(int n, int kl, int nrhs, int count) {
   const int P = band_spike_parts(n, kl);
-  return (size_t)count * (P > 1 ? P - 1 : 0) * 2 * kl * nrhs * 2 + 64;
+  // interface values [count][P-1][2kl][nrhs] + per-partition tips [count][P][2kl][nrhs], re | im
+  return (size_t)count * ((P > 1 ? P - 1 : 0) + P) * 2 * kl * nrhs * 2 + 64;
 }
 
 // aux pointers of item base
@@ -1142,16 +1186,43 @@ cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* w
   band_rsolve_kernel<<<dim3(count, chunks), RT, 0, st>>>(rs);
   count_launch();
   if ((e = cudaGetLastError())) return e;
-  CKArgs ck{};
-  ck.n = n; ck.kl = kl; ck.P = P; ck.nrhs = nrhs;
-  ck.sr = sr; ck.si = si; ck.ss = sa; ck.yr = rs.yr; ck.yi = rs.yi; ck.sy = sy;
-  ck.xr = xr; ck.xi = xi; ck.ldx = ldx; ck.sx = sx;
-  {
+  if (getenv("FB_BAND_CORRECT_SIMT")) {
+    CKArgs ck{};
+    ck.n = n; ck.kl = kl; ck.P = P; ck.nrhs = nrhs;
+    ck.sr = sr; ck.si = si; ck.ss = sa; ck.yr = rs.yr; ck.yi = rs.yi; ck.sy = sy;
+    ck.xr = xr; ck.xi = xi; ck.ldx = ldx; ck.sx = sx;
     const int nw = std::min(SNW, ceil_div(nrhs, 32));
     correct_fn(kl)<<<dim3(P, ceil_div(nrhs, 32 * nw), count), 32 * nw, 0, st>>>(ck);
+    count_launch();
+    return cudaGetLastError();
   }
+  // correction on the FP64 tensor pipe: per shift, X_j -= [V_j W_j] T_j for all
+  // partitions as one strided-batch ZGEMM (K = 2kl) plus one for the shorter last
+  const long long w = 2 * kl, stt = (long long)P * w * nrhs;
+  TGArgs tg{};
+  tg.kl = kl; tg.P = P; tg.nrhs = nrhs; tg.yr = rs.yr; tg.yi = rs.yi; tg.sy = sy;
+  tg.tr = scratch + 2 * count * sy; tg.ti = tg.tr + count * stt; tg.st = stt;
+  band_tips_kernel<<<dim3((int)std::min<long long>(ceil_div(stt, 256), 4 * kSMs), count), 256, 0, st>>>(tg);
   count_launch();
-  return cudaGetLastError();
+  if ((e = cudaGetLastError())) return e;
+  const int sz = part_sz(n, P), last = n - (P - 1) * sz;
+  for (int k = 0; k < count; ++k) {
+    const double* ar = sr + k * sa;
+    const double* ai = si + k * sa;
+    const double* br = tg.tr + k * stt;
+    const double* bi = tg.ti + k * stt;
+    double* cr = xr + k * sx;
+    double* ci = xi + k * sx;
+    if ((e = gemm(1, sz, nrhs, (int)w, op_n(ar, ai, w), op_n(br, bi, nrhs), cr, ci, ldx, -1.0, 0.0, 1.0, 0.0, st,
+                  nullptr, 1, P - 1, (long long)sz * w, w * nrhs, (long long)sz * ldx)))
+      return e;
+    const long long lo = (long long)(P - 1) * sz;
+    if ((e = gemm(1, last, nrhs, (int)w, op_n(ar + lo * w, ai + lo * w, w),
+                  op_n(br + (P - 1) * w * nrhs, bi + (P - 1) * w * nrhs, nrhs), cr + lo * ldx, ci + lo * ldx, ldx,
+                  -1.0, 0.0, 1.0, 0.0, st)))
+      return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace fb

@@ -213,18 +213,19 @@ int fb_zgetrs(fb_ctx* c, int n, int nrhs, const double* re, const double* im, in
   if (n < 0 || nrhs < 0 || !xr || !xi) return FB_ERR_ARG;
   if (n == 0 || nrhs == 0) return FB_OK;
   // in place: the right-hand sides go through the scratch first
-  const size_t plane = (size_t)n * (size_t)nrhs;
+  const int tld = fb::zgetrs_tmp_ld(nrhs);
+  const size_t plane = (size_t)n * (size_t)tld;
   int r = ensure_scratch(c, sizeof(double) * 4 * plane);
   if (r) return r;
   double* tr = (double*)c->scratch;
   double* ti = tr + plane;
-  cudaError_t e = cudaMemcpy2DAsync(tr, nrhs * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, c->stream);
+  cudaError_t e = cudaMemcpy2DAsync(tr, tld * 8, xr, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, c->stream);
   if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(ti, nrhs * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, c->stream);
+    e = cudaMemcpy2DAsync(ti, tld * 8, xi, ldx * 8, nrhs * 8, n, cudaMemcpyDeviceToDevice, c->stream);
   if (e != cudaSuccess) return set_err(c, e, "zgetrs copy");
   fb::LuBatch f{1, const_cast<double*>(re), const_cast<double*>(im), ld, 0, const_cast<int*>(piv), 0,
                 nullptr, const_cast<double*>(dinv), 0};
-  return set_err(c, fb::zgetrs_batched(n, nrhs, f, adjoint, tr, ti, nrhs, 0, xr, xi, ldx, 0, tr + 2 * plane,
+  return set_err(c, fb::zgetrs_batched(n, nrhs, f, adjoint, tr, ti, tld, 0, xr, xi, ldx, 0, tr + 2 * plane,
                                        c->stream),
                  "zgetrs");
 }
@@ -236,7 +237,7 @@ int fb_zgetrs_batched(fb_ctx* c, int count, int n, int nrhs, const double* re, c
   CTX_GUARD(c);
   if (n < 0 || nrhs < 0 || count < 0 || !xr || !xi || !br || !bi) return FB_ERR_ARG;
   if (n == 0 || nrhs == 0 || count == 0) return FB_OK;
-  int r = ensure_scratch(c, sizeof(double) * 2 * (size_t)count * n * nrhs);
+  int r = ensure_scratch(c, sizeof(double) * 2 * (size_t)count * n * fb::zgetrs_tmp_ld(nrhs));
   if (r) return r;
   fb::LuBatch f{count, const_cast<double*>(re), const_cast<double*>(im), ld, lu_stride, const_cast<int*>(piv),
                 piv_stride, nullptr, const_cast<double*>(dinv), dinv_stride};

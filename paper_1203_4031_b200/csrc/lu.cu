@@ -393,23 +393,26 @@ cudaError_t zgetrs_batched(int n, int nrhs, const LuBatch& f, int adjoint, const
       return e;
     return sweep_launch(1, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, xr, xi, ldx, sx, st);
   }
-  // A^H = U^H L^H P: U^H and L^H sweeps on a copy, then X_b <- P_b^T (scatter)
-  const long long st_ = (long long)n * nrhs;
+  // A^H = U^H L^H P: U^H and L^H sweeps on a copy, then X_b <- P_b^T (scatter).
+  // The copy's leading dimension is even so the sweeps take the 16-byte path
+  // even when M0 has shrunk to an odd column count.
+  const int tld = zgetrs_tmp_ld(nrhs);
+  const long long st_ = (long long)n * tld;
   double* tr = tmp;
   double* ti = tmp + (size_t)B * st_;
   for (int b = 0; b < B; ++b) {
-    if ((e = cudaMemcpy2DAsync(tr + b * st_, nrhs * 8, rr + b * srhs, ldr * 8, nrhs * 8, n,
+    if ((e = cudaMemcpy2DAsync(tr + b * st_, tld * 8, rr + b * srhs, ldr * 8, nrhs * 8, n,
                                cudaMemcpyDeviceToDevice, st)))
       return e;
-    if ((e = cudaMemcpy2DAsync(ti + b * st_, nrhs * 8, ri + b * srhs, ldr * 8, nrhs * 8, n,
+    if ((e = cudaMemcpy2DAsync(ti + b * st_, tld * 8, ri + b * srhs, ldr * 8, nrhs * 8, n,
                                cudaMemcpyDeviceToDevice, st)))
       return e;
   }
-  if ((e = sweep_launch(2, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, tr, ti, nrhs, st_, st)))
+  if ((e = sweep_launch(2, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, tr, ti, tld, st_, st)))
     return e;
-  if ((e = sweep_launch(3, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, tr, ti, nrhs, st_, st)))
+  if ((e = sweep_launch(3, n, nrhs, B, f.re, f.im, f.ld, f.slu, f.dinv, gm, f.sdinv, tr, ti, tld, st_, st)))
     return e;
-  return permute_rows_launch(n, nrhs, B, perm, 2 * f.sdinv, 0, tr, ti, nrhs, st_, xr, xi, ldx, sx, st);
+  return permute_rows_launch(n, nrhs, B, perm, 2 * f.sdinv, 0, tr, ti, tld, st_, xr, xi, ldx, sx, st);
 }
 
 }  // namespace fb

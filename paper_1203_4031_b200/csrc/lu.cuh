@@ -37,6 +37,9 @@ cudaError_t permute_rows_launch(int n, int m, int count, const int* perm, long l
                                 const double* ir, const double* ii, long long ldi, long long sin_, double* orr,
                                 double* oi, long long ldo, long long sout, cudaStream_t st);
 cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t st, const LuStreams* ls);
+// leading dimension of zgetrs_batched's adjoint copy (even: 16-byte sweeps);
+// tmp holds 2 * count * n * zgetrs_tmp_ld(nrhs) doubles
+inline int zgetrs_tmp_ld(int nrhs) { return nrhs + (nrhs & 1); }
 cudaError_t zgetrs_batched(int n, int nrhs, const LuBatch& f, int adjoint, const double* rr, const double* ri,
                            long long ldr, long long srhs, double* xr, double* xi, long long ldx, long long sx,
                            double* tmp, cudaStream_t st);

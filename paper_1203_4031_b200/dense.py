@@ -192,16 +192,19 @@ class DeviceDenseOps:
         for fb_ in self._batches:
             cnt = fb_.count
             for adj in ((0, 1) if hermitian else (0,)):
+                # even leading dimension: the sweeps' 16-byte path also when M0
+                # has shrunk to an odd column count (kernel.py:385-400)
+                mp = m + (m & 1)
                 X = self._xbuf.get((id(fb_), adj))
-                if X is None or X.shape[3] != m:
-                    X = dev.torch.empty((2, cnt, n, m), dtype=dev.torch.float64, device=dev.tdev)
+                if X is None or X.shape[3] != mp:
+                    X = dev.torch.empty((2, cnt, n, mp), dtype=dev.torch.float64, device=dev.tdev)
                     self._xbuf[(id(fb_), adj)] = X
                 re, im, ld, slu, piv, spiv, dinv, sdinv = fb_.args()
                 dev.check(dev.lib.fb_zgetrs_batched(dev.h, cnt, n, m, re, im, ld, slu, piv, spiv, dinv, sdinv,
                                                     adj, W.re, W.im, W.ld, 0, X[0].data_ptr(),
-                                                    X[1].data_ptr(), m, n * m), "zgetrs_batched")
+                                                    X[1].data_ptr(), mp, n * mp), "zgetrs_batched")
                 for i in range(cnt):
-                    self._pass[(id(fb_), i, adj)] = (X, i)
+                    self._pass[(id(fb_), i, adj)] = (X, i, m)
 
     def pass_result(self, z, adjoint):
         """Planar view of this pass's solve for shift z (None if not resident)."""
@@ -211,14 +214,14 @@ class DeviceDenseOps:
         got = self._pass.get((id(hit[0]), hit[1], int(adjoint)))
         if got is None:
             return None
-        X, i = got
-        return Planar(X[:, i], True, X.shape[2], X.shape[3], X.shape[3])
+        X, i, m = got
+        return Planar(X[:, i], True, X.shape[2], m, X.shape[3])
 
     def _solve(self, f, W: Planar, adjoint):
         if f.resident:
             hit = self._pass.get((id(f.batch), f.idx, int(adjoint)))
             if hit is not None:
-                X, i = hit
+                X, i, _ = hit
                 W.plane(0).copy_(X[0, i][:, :W.cols])
                 W.plane(1).copy_(X[1, i][:, :W.cols])
                 return
