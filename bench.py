@@ -46,26 +46,53 @@ def _dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region, in-process
+    through NVML (no nvidia-smi subprocesses competing with the launching
+    thread); falls back to nvidia-smi when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index):
         self.index = index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            dev = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(index)).split(",")[index]) \
+                if os.environ.get("CUDA_VISIBLE_DEVICES") else index
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in self.BITS]
 
     def _loop(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
+                if self._nvml is not None:
+                    self.samples.append(self._sample_nvml())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -81,14 +108,15 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def cpu_reference_solve(w, threads):
@@ -180,13 +208,17 @@ def run_gpu(args):
     lu_events = []
     DeviceDenseOps.lu_event_sink = lu_events
     with ClockSampler(local) as clk:
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev0.record()
-        for _ in range(args.steps):
+        step_ev[0].record()
+        for i in range(args.steps):
             r = solve_once(A_d, B_d)
             its += r.loop + 1
             loops.append(r.loop)
+            step_ev[i + 1].record()
         ev1.record()
         barrier()
+    step_ms = [round(step_ev[i].elapsed_time(step_ev[i + 1]), 2) for i in range(args.steps)]
     DeviceDenseOps.lu_event_sink = None
     launches = dev.launches() - launches0
     t = ev0.elapsed_time(ev1) / 1e3
@@ -240,7 +272,7 @@ def run_gpu(args):
             "config": {"workload": "c2_dfeast_sygv N=4096 M0=160 Ne=8 (BASELINE configs[1])",
                        "global_batch": 1, "seq_len": n, "parallelism": f"contour-points x{world}",
                        "l2": "working set (A, B, 8 factors = 2.4 GB) larger than L2",
-                       "m_found": int(r.m), "loops": loops, "info": int(r.info)},
+                       "m_found": int(r.m), "loops": loops, "info": int(r.info), "step_ms": step_ms},
             "lu_tflops": lu_tf, "lu_ms": lu_ms,
             "roofline": {"bound": "tensor", "achieved": lu_tf, "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
                          "frac": lu_tf / FP64_DMMA_PEAK, "traffic": None,

@@ -55,6 +55,57 @@ def expand_band(ab, kl: int, uplo: str, hermitian: bool) -> np.ndarray:
     return out
 
 
+def expand_band_device(dev, ab, kl: int, uplo: str, hermitian: bool, kl_to: int) -> Planar:
+    """expand_band + pad_band on the device: only the in-pattern rows of the
+    LAPACK band ``ab`` cross PCIe (kl+1 rows for 'L'/'U'), the full-band
+    (2*kl_to+1) x n layout is assembled by device copies (the mirrored
+    triangle conjugated for Hermitian input) -- the same values as the host
+    functions, bit for bit (banded.py:21-47, 181-187)."""
+    torch = dev.torch
+    ab = np.asarray(ab)
+    n = ab.shape[1]
+    uplo = uplo.upper()
+    off = kl_to - kl
+    out = dev.zeros(2 * kl_to + 1, n, hermitian)
+    planes = [out.plane(0)] + ([out.plane(1)] if hermitian else [])
+    # LAPACK band rows: 'F' 2kl+1 rows (diagonal in row kl); 'L' diagonal in
+    # row 0, subdiagonals below; 'U' superdiagonals above the diagonal in row kl
+    rows = list(range(2 * kl + 1)) if uplo == "F" else list(range(kl + 1))
+    src = np.ascontiguousarray(ab[rows[0]:rows[-1] + 1])
+    if hermitian:
+        st = torch.from_numpy(src.astype(np.complex128, copy=False)).to(dev.tdev)
+        sp = [st.real, st.imag]
+    else:
+        st = torch.from_numpy(np.ascontiguousarray(src.real if np.iscomplexobj(src) else src,
+                                                   dtype=np.float64)).to(dev.tdev)
+        sp = [st]
+    r0 = rows[0]
+
+    def row(k, p):
+        return sp[p][k - r0]
+
+    for p, P in enumerate(planes):
+        sign = -1.0 if (hermitian and p == 1) else 1.0
+        if uplo == "F":
+            P[off + kl].copy_(row(kl, p))
+            for d in range(1, kl + 1):
+                P[off + kl - d, d:].copy_(row(kl - d, p)[d:])
+                P[off + kl + d, :n - d].copy_(row(kl + d, p)[:n - d])
+        elif uplo == "L":
+            P[off + kl].copy_(row(0, p))
+            for d in range(1, kl + 1):
+                low = row(d, p)[:n - d]
+                P[off + kl + d, :n - d].copy_(low)
+                P[off + kl - d, d:].copy_(low if sign > 0 else -low)
+        else:
+            P[off + kl].copy_(row(kl, p))
+            for d in range(1, kl + 1):
+                up = row(kl - d, p)[d:]
+                P[off + kl - d, d:].copy_(up)
+                P[off + kl + d, :n - d].copy_(up if sign > 0 else -up)
+    return out
+
+
 def pad_band(fb, kl_from: int, kl_to: int):
     if kl_from == kl_to:
         return fb
@@ -351,15 +402,10 @@ def _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, hermi
     if kernel.done:
         return kernel.result
     kl = max(kla, klb if b is not None else 0)
-    wdt = np.complex128 if hermitian else np.float64
-    fa = pad_band(expand_band(a, kla, uplo, hermitian).astype(wdt, copy=False), kla, kl)
-    fbm = None
-    if b is not None:
-        fbm = pad_band(expand_band(b, klb, uplo, hermitian).astype(wdt, copy=False), klb, kl)
     dev = kernel.dev
     try:
-        FA = dev.upload(fa, cplx=hermitian)
-        FB = None if fbm is None else dev.upload(fbm, cplx=hermitian)
+        FA = expand_band_device(dev, a, kla, uplo, hermitian, kl)
+        FB = None if b is None else expand_band_device(dev, b, klb, uplo, hermitian, kl)
     except MemoryError:
         kernel.abort(-1)
         return kernel.result

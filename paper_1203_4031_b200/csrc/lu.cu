@@ -4,8 +4,8 @@
 // Restates feastlib's dense backend (dense.py:30-88, _DenseOps dense.py:91-117)
 // as a blocked algorithm for sm_100a:
 //   * shift formation S_e = z_e B - A (dense.py:97-103), planar complex;
-//   * right-looking blocked LU, outer block NB = 128 (trailing update is one
-//     DMMA ZGEMM with K = 128), inner sub-panels of PW = 32 columns factored by
+//   * right-looking blocked LU, outer block NB = 256 (trailing update is one
+//     DMMA ZGEMM with K = 256), inner sub-panels of PW = 32 columns factored by
 //     panel.cu (cluster/DSMEM exchange, one pivot per column);
 //   * the panel kernel also emits the 32x32 unit-lower / upper diagonal-block
 //     inverses (every triangular solve downstream is then a DMMA GEMM) and the
@@ -40,8 +40,8 @@ static int outer_nb() {                // outer block (trailing-update K), FB_LU
   static int nb = 0;
   if (!nb) {
     const char* e = getenv("FB_LU_NB");
-    nb = e ? atoi(e) : 128;
-    if (nb < 32 || nb % 32) nb = 128;
+    nb = e ? atoi(e) : 256;  // 256: +3 % over 128 at N = 4096 and 8192 (profiles/r01_lu_nb_rpc_sweep.txt)
+    if (nb < 32 || nb % 32) nb = 256;
   }
   return nb;
 }

@@ -760,7 +760,7 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     static int rmin = 0;
     if (!rmin) {
       const char* e = getenv("FB_PANEL_RPC");
-      rmin = e ? std::max(64, std::min(rpc_cluster, atoi(e))) : 192;
+      rmin = e ? std::max(64, std::min(rpc_cluster, atoi(e))) : 384;  // fewest CTAs: SMs stay with the GEMM
     }
     if (rows > 2 * PW) G = std::max(G, std::min(max_cluster, ceil_div(rows, rmin)));
     G = std::max(1, std::min(G, rows / PW));

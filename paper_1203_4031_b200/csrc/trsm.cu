@@ -43,10 +43,14 @@ namespace fb {
 namespace {
 
 constexpr int BS = 32;                 // block rows (= PW of the factorization)
-constexpr int CW = 32;                 // right-hand-side columns per chunk
-constexpr int TT = 128;                // threads: 4 warps in a 2x2 grid of 16x16 sub-tiles
-constexpr int PA = 36;                 // tile pitch (= 4 mod 16: conflict-free fragments, both orientations)
-constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 tile in shared memory
+constexpr int CW = 32;                 // right-hand-side columns per chunk (64: 1.4x slower on C2, fewer CTAs per SM)
+constexpr int WC = CW / 16;            // warps along the columns (16x16 sub-tile each)
+constexpr int TT = 32 * 2 * WC;        // threads: 4 warps in a 2x2 grid of 16x16 sub-tiles
+constexpr int GT = 128;                // threads of the gmat kernel
+constexpr int PA = 36;                 // operator tile pitch (= 4 mod 16: conflict-free fragments, both orientations)
+constexpr int XP = CW + 4;             // X tile pitch (= 4 mod 16)
+constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 operator tile in shared memory
+constexpr int XTILE = 2 * BS * XP;     // doubles per planar 32 x CW X tile
 constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): G re/im, D re/im
 
 struct SweepArgs {
@@ -78,28 +82,28 @@ __device__ __forceinline__ int blk_at(const SweepArgs& a, int t) {
 }
 
 // --- cp.async tile loader ---------------------------------------------------------
-// Natural copy of the planar block [r0, r0 + 32) x [c0, c0 + 32) of a row-major
-// matrix (row stride ld) into a pitch-PA tile; rows >= nr / cols >= nc read 0.
-template <bool VEC>
+// Natural copy of the planar block [r0, r0 + 32) x [c0, c0 + NC) of a row-major
+// matrix (row stride ld) into a pitch-P tile; rows >= nr / cols >= nc read 0.
+template <bool VEC, int NC = BS, int P = PA>
 __device__ __forceinline__ void cp_block(const double* re, const double* im, long long ld, int r0, int c0,
                                          int nr, int nc, double* s) {
   if (VEC) {
-    for (int e = threadIdx.x; e < BS * BS / 2; e += TT) {
-      const int r = e >> 4, c = (e & 15) * 2;
+    for (int e = threadIdx.x; e < BS * NC / 2; e += TT) {
+      const int r = e / (NC / 2), c = (e % (NC / 2)) * 2;
       const int gr = r0 + r, gc = c0 + c;
       const int valid = gr < nr ? max(0, min(2, nc - gc)) : 0;
       const long long o = valid ? (long long)gr * ld + gc : 0;
-      cp_async16(s + r * PA + c, re + o, valid * 8);
-      cp_async16(s + BS * PA + r * PA + c, im + o, valid * 8);
+      cp_async16(s + r * P + c, re + o, valid * 8);
+      cp_async16(s + BS * P + r * P + c, im + o, valid * 8);
     }
   } else {
-    for (int e = threadIdx.x; e < BS * BS; e += TT) {
-      const int r = e >> 5, c = e & 31;
+    for (int e = threadIdx.x; e < BS * NC; e += TT) {
+      const int r = e / NC, c = e % NC;
       const int gr = r0 + r, gc = c0 + c;
       const bool ok = gr < nr && gc < nc;
       const long long o = ok ? (long long)gr * ld + gc : 0;
-      cp_async8(s + r * PA + c, re + o, ok);
-      cp_async8(s + BS * PA + r * PA + c, im + o, ok);
+      cp_async8(s + r * P + c, re + o, ok);
+      cp_async8(s + BS * P + r * P + c, im + o, ok);
     }
   }
 }
@@ -125,14 +129,17 @@ __device__ __forceinline__ void acc_zero(Acc& c) {
       for (int e = 0; e < 2; ++e) c.r[mt][nt][e] = c.i[mt][nt][e] = 0.0;
 }
 
-// acc += (sr*Re A + i*si*Im A) (32x32) * B (32x32 tile of X); A is read as
-// A[r][k] = S[r*PA + k] (TR = false) or S[k*PA + r] (TR = true)
+// acc += (sr*Re A + i*si*Im A) (32x32) * B (32 x CW tile of X); A is read as
+// A[r][k] = S[r*PA + k] (TR = false) or S[k*PA + r] (TR = true).  live = false:
+// the warp's 16 columns lie past nrhs (warp-uniform skip, no barriers inside).
 template <bool TR>
-__device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* B, double sr, double si) {
+__device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* B, double sr, double si,
+                                         bool live) {
+  if (!live) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int wr = w >> 1, wc = w & 1;
+  const int wr = w / WC, wc = w % WC;
   const double* Ai = A + BS * PA;
-  const double* Bi = B + BS * PA;
+  const double* Bi = B + BS * XP;
 #pragma unroll
   for (int k0 = 0; k0 < BS; k0 += 4) {
     const int k = k0 + (lane & 3);
@@ -148,8 +155,8 @@ __device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* 
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int col = wc * 16 + nt * 8 + (lane >> 2);
-      br[nt] = B[k * PA + col];
-      bi[nt] = Bi[k * PA + col];
+      br[nt] = B[k * XP + col];
+      bi[nt] = Bi[k * XP + col];
     }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -173,7 +180,7 @@ __device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* 
 template <bool VEC>
 __device__ __forceinline__ void acc_load(const SweepArgs& a, int b, int c0, Acc& c) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int wr = w >> 1, wc = w & 1;
+  const int wr = w / WC, wc = w % WC;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int gr = b * BS + wr * 16 + mt * 8 + (lane >> 2);
@@ -201,7 +208,7 @@ __device__ __forceinline__ void acc_load(const SweepArgs& a, int b, int c0, Acc&
 template <bool VEC>
 __device__ __forceinline__ void acc_store(const SweepArgs& a, int b, int c0, const Acc& c) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int wr = w >> 1, wc = w & 1;
+  const int wr = w / WC, wc = w % WC;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int gr = b * BS + wr * 16 + mt * 8 + (lane >> 2);
@@ -235,15 +242,15 @@ __device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b, int w
 template <bool VEC>
 __device__ __forceinline__ void cp_x(const SweepArgs& a, int b, int c0, double* s) {
   if (VEC) {
-    cp_block<true>(a.xre, a.xim, a.ldx, b * BS, c0, a.n, a.nrhs, s);
+    cp_block<true, CW, XP>(a.xre, a.xim, a.ldx, b * BS, c0, a.n, a.nrhs, s);
   } else {
-    for (int e = threadIdx.x; e < BS * BS; e += TT) {
-      const int r = e >> 5, c = e & 31;
+    for (int e = threadIdx.x; e < BS * CW; e += TT) {
+      const int r = e / CW, c = e % CW;
       const int gr = b * BS + r, gc = c0 + c;
       const bool ok = gr < a.n && gc < a.nrhs;
       const long long o = (long long)gr * a.ldx + gc;
-      s[r * PA + c] = ok ? __ldcg(a.xre + o) : 0.0;
-      s[BS * PA + r * PA + c] = ok ? __ldcg(a.xim + o) : 0.0;
+      s[r * XP + c] = ok ? __ldcg(a.xre + o) : 0.0;
+      s[BS * XP + r * XP + c] = ok ? __ldcg(a.xim + o) : 0.0;
     }
   }
 }
@@ -296,10 +303,11 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
   const int S = G >= C ? G / C + (g % C < G % C ? 1 : 0) : 1;
   const int sub = G >= C ? g / C : 0;
   const double conj_i = TR ? -1.0 : 1.0;  // Im sign of the streamed M tiles
-  double* Xt = s;             // X_{b(t)} chunk (B operand of every product this step)
-  double* Xn = s + TILE;      // X_{b(t+1)} chunk (look-ahead)
-  double* T0 = s + 2 * TILE;  // operator stage 0
-  double* T1 = s + 3 * TILE;  // operator stage 1
+  double* Xt = s;                      // X_{b(t)} chunk (B operand of every product this step)
+  double* Xn = s + XTILE;              // X_{b(t+1)} chunk (look-ahead)
+  double* T0 = s + 2 * XTILE;          // operator stage 0
+  double* T1 = s + 2 * XTILE + TILE;   // operator stage 1
+  const int wcol = ((threadIdx.x >> 5) % WC) * 16;  // this warp's first column inside a chunk
   auto upd = [&](int blk, int c) { return a.upd + (size_t)blk * C + c; };
   auto fin = [&](int blk, int c) { return a.fin + (size_t)blk * C + c; };
   const int c_first = G >= C ? g % C : g, c_step = G >= C ? C : G;
@@ -315,7 +323,7 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
       __syncthreads();
       Acc acc;
       acc_zero(acc);
-      tile_mma<false>(acc, T0, Xt, 1.0, 1.0);
+      tile_mma<false>(acc, T0, Xt, 1.0, 1.0, c * CW + wcol < a.nrhs);
       acc_store<VEC>(a, b0, c * CW, acc);
       __syncthreads();
       publish(fin(b0, c), 1);
@@ -336,6 +344,7 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
     if (!do_ahead && qb >= qe) continue;
     for (int c = c_first; c < C; c += c_step) {
       const int c0 = c * CW;
+      const bool live = c0 + wcol < a.nrhs;
       if (threadIdx.x == 0) wait_ge(fin(bt, c), 1);
       if (do_ahead && threadIdx.x == 32) wait_ge(upd(blk_at(a, t + 1), c), t);
       __syncthreads();
@@ -350,8 +359,8 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
         __syncthreads();
         Acc acc;
         acc_zero(acc);
-        tile_mma<false>(acc, T0, Xn, 1.0, 1.0);
-        tile_mma<false>(acc, T1, Xt, -1.0, -1.0);
+        tile_mma<false>(acc, T0, Xn, 1.0, 1.0, live);
+        tile_mma<false>(acc, T1, Xt, -1.0, -1.0, live);
         acc_store<VEC>(a, bn, c0, acc);
         __syncthreads();
         publish(fin(bn, c), 1);
@@ -378,7 +387,7 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
             cp_async_wait<0>();
           }
           __syncthreads();
-          tile_mma<TR>(cur, Tq, Xt, -1.0, -conj_i);
+          tile_mma<TR>(cur, Tq, Xt, -1.0, -conj_i, live);
           acc_store<VEC>(a, rb, c0, cur);
           __syncthreads();
         }
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
 
 // Per (block, variant): D_v (the variant's diagonal inverse, conj-transposed for
 // the adjoint sweeps) and G_v = D_v * M(b, prev(b)).
-__global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
+__global__ void __launch_bounds__(GT) gmat_kernel(SweepArgs a0) {
   __shared__ double Dr[BS * 33], Di[BS * 33], Mr[BS * 33], Mi[BS * 33];
   SweepArgs a = a0;
   offset_item(a, blockIdx.z);
@@ -414,7 +423,7 @@ __global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
   const double* dr = a.dinv + (size_t)b * 4 * BS * BS + (upper ? 2 : 0) * BS * BS;
   const double* di = dr + BS * BS;
   double* out = const_cast<double*>(a.gmat) + ((size_t)variant * a.nblk + b) * GM_BLK;
-  for (int e = threadIdx.x; e < BS * BS; e += TT) {
+  for (int e = threadIdx.x; e < BS * BS; e += GT) {
     const int r = e / BS, k = e % BS;
     const double vr = trans ? dr[k * BS + r] : dr[e];
     const double vi = trans ? -di[k * BS + r] : di[e];
@@ -426,11 +435,11 @@ __global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
   const bool fwd = variant == 0 || variant == 2;
   const int prev = fwd ? b - 1 : b + 1;
   if (prev < 0 || prev >= a.nblk) {
-    for (int e = threadIdx.x; e < BS * BS; e += TT) out[e] = out[BS * BS + e] = 0.0;
+    for (int e = threadIdx.x; e < BS * BS; e += GT) out[e] = out[BS * BS + e] = 0.0;
     return;
   }
   const int i0 = b * BS, p0 = prev * BS;
-  for (int e = threadIdx.x; e < BS * BS; e += TT) {
+  for (int e = threadIdx.x; e < BS * BS; e += GT) {
     const int r = e / BS, k = e % BS;
     const int gr = i0 + r, gk = p0 + k;
     double vr = 0.0, vi = 0.0;
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
     Mi[r * 33 + k] = vi;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < BS * BS; e += TT) {
+  for (int e = threadIdx.x; e < BS * BS; e += GT) {
     const int r = e / BS, c = e % BS;
     double sr = 0.0, si = 0.0;
     for (int k = 0; k < BS; ++k) {
@@ -461,7 +470,7 @@ __global__ void __launch_bounds__(TT) gmat_kernel(SweepArgs a0) {
   }
 }
 
-size_t sweep_smem() { return sizeof(double) * 4 * TILE; }
+size_t sweep_smem() { return sizeof(double) * (2 * XTILE + 2 * TILE); }
 
 }  // namespace
 
@@ -472,7 +481,7 @@ cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, 
   SweepArgs a{};
   a.n = n; a.nblk = ceil_div(n, BS); a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.slu = slu; a.sdinv = sdinv; a.sx = 0;
-  gmat_kernel<<<dim3(a.nblk, 4, count), TT, 0, st>>>(a);
+  gmat_kernel<<<dim3(a.nblk, 4, count), GT, 0, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }

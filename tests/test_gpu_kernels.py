@@ -302,3 +302,29 @@ def test_band_matvec(dev, unit_golden, n, kl):
     dev.check(dev.lib.fb_band_matvec(dev.h, n, kl, x.shape[1], _c(FB.re), _c(FB.im), FB.ld, _c(X.re),
                                      _c(X.im), X.ld, _c(Y.re), _c(Y.im), Y.ld), "band_matvec")
     assert np.abs(dev.download(Y) - g[f"bmv_y_{tag}"]).max() <= 1e-13 * n
+
+
+@pytest.mark.parametrize("uplo", ["F", "L", "U"])
+@pytest.mark.parametrize("herm", [False, True])
+@pytest.mark.parametrize("kl,kl_to", [(1, 1), (3, 3), (1, 4), (4, 6)])
+def test_expand_band_device_bitexact(dev, uplo, herm, kl, kl_to):
+    """Device band expansion == host expand_band + pad_band bit for bit, with
+    the out-of-pattern slots of the LAPACK band poisoned by NaN (never read,
+    banded.py:21-47; test_banded.py:145-164)."""
+    from paper_1203_4031_b200.banded import band_required_rows, expand_band, expand_band_device, pad_band
+    rng = np.random.default_rng(kl * 10 + kl_to + (7 if herm else 0))
+    n = 23
+    rows = band_required_rows(kl, uplo)
+    ab = rng.standard_normal((rows, n)) + (1j * rng.standard_normal((rows, n)) if herm else 0)
+    for d in range(1, kl + 1):   # poison the slots outside the band pattern
+        if uplo == "F":
+            ab[kl - d, :d] = np.nan
+            ab[kl + d, n - d:] = np.nan
+        elif uplo == "L":
+            ab[d, n - d:] = np.nan
+        else:
+            ab[kl - d, :d] = np.nan
+    want = pad_band(expand_band(ab, kl, uplo, herm), kl, kl_to)
+    got = expand_band_device(dev, ab, kl, uplo, herm, kl_to)
+    g = got.plane(0).cpu().numpy() + (1j * got.plane(1).cpu().numpy() if herm else 0)
+    assert np.array_equal(g, want)
