@@ -8,6 +8,7 @@ PLANAR: a float64 tensor of shape (2, rows, ld) (plane 0 = real part).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -191,6 +192,19 @@ class Device:
         out = np.empty(tuple(t.shape), dtype=npdt)
         src = t.view(-1).view(torch.uint8)
         dst = out.reshape(-1).view(np.uint8)
+        pool = self._copy_pool()
+        nth = pool._max_workers
+
+        def host_copy(pbuf, poff, pn):
+            # first touch of the fresh destination pages dominates: split the
+            # pinned -> pageable copy over threads (numpy releases the GIL)
+            step = -(-pn // nth)
+            hb = pbuf[:pn].numpy()
+            futs = [pool.submit(np.copyto, dst[poff + a:poff + min(pn, a + step)], hb[a:min(pn, a + step)])
+                    for a in range(0, pn, step)]
+            for f in futs:
+                f.result()
+
         prev = None
         for k, off in enumerate(range(0, nbytes, self._BOUNCE)):
             n = min(self._BOUNCE, nbytes - off)
@@ -200,12 +214,19 @@ class Device:
             if prev is not None:
                 pbuf, pev, poff, pn = prev
                 pev.synchronize()
-                dst[poff:poff + pn] = pbuf[:pn].numpy()
+                host_copy(pbuf, poff, pn)
             prev = (buf, ev, off, n)
         pbuf, pev, poff, pn = prev
         pev.synchronize()
-        dst[poff:poff + pn] = pbuf[:pn].numpy()
+        host_copy(pbuf, poff, pn)
         return out
+
+    def _copy_pool(self):
+        if getattr(self, "_pool", None) is None:
+            import concurrent.futures
+            self._pool = concurrent.futures.ThreadPoolExecutor(
+                max_workers=max(1, min(8, len(os.sched_getaffinity(0)))))
+        return self._pool
 
     def download(self, p: Planar, as_complex=None):
         """Planar -> numpy (complex128 when the view is complex)."""
