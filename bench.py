@@ -262,6 +262,17 @@ def run_gpu(args):
                          "+ LAPACK zgetrf/zgetrs, OpenBLAS threads=cores)",
                "m_found": int(rr.m), "loops": int(rr.loop), "seconds": dt}
 
+    # DRAM bytes of one batched LU call (all its kernels) from the committed ncu
+    # capture of the same workload (tools/prof_final.sh -> profiles/), or null
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_lu_traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("n") == n and tj.get("count") == w.ne:
+            traffic = tj["dram_bytes_per_call"]
+    except (OSError, ValueError, KeyError):
+        pass
+
     if rank == 0:
         clocks = clk.summary()
         line = {
@@ -275,7 +286,8 @@ def run_gpu(args):
                        "m_found": int(r.m), "loops": loops, "info": int(r.info), "step_ms": step_ms},
             "lu_tflops": lu_tf, "lu_ms": lu_ms,
             "roofline": {"bound": "tensor", "achieved": lu_tf, "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
-                         "frac": lu_tf / FP64_DMMA_PEAK, "traffic": None,
+                         "frac": lu_tf / FP64_DMMA_PEAK, "traffic": traffic,
+                         "traffic_unit": "bytes per fb_zgetrf_batched call (Ne shifts), ncu dram read+write",
                          "kernel": "fb_zgetrf_batched (Ne shifted complex LUs per call, (8/3)N^3 flop each)",
                          "peak_source": "measured DMMA m8n8k4 f64 microbenchmark (tools/fp64_peak.cu); "
                                         "MEASURED_PEAKS.json has no FP64 entry"},
