@@ -130,12 +130,16 @@ __device__ __forceinline__ void acc_zero(Acc& c) {
       for (int e = 0; e < 2; ++e) c.r[mt][nt][e] = c.i[mt][nt][e] = 0.0;
 }
 
-// acc += (sr*Re A + i*si*Im A) (32x32) * B (32 x CW tile of X); A is read as
-// A[r][k] = S[r*PA + k] (TR = false) or S[k*PA + r] (TR = true).  live = false:
-// the warp's 16 columns lie past nrhs (warp-uniform skip, no barriers inside).
-template <bool TR>
-__device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* B, double sr, double si,
-                                         bool live) {
+// acc += (SR*Re A + i*SI*Im A) (32x32) * B (32 x CW tile of X); A is read as
+// A[r][k] = S[r*PA + k] (TR = false) or S[k*PA + r] (TR = true).  The signs
+// are compile-time and applied as integer sign-bit flips, so the FP64 pipe
+// that issues the DMMAs carries no extra multiplies.  live = false: the
+// warp's 16 columns lie past nrhs (warp-uniform skip, no barriers inside).
+__device__ __forceinline__ double sgnflip(double v) {
+  return __longlong_as_double(__double_as_longlong(v) ^ 0x8000000000000000ll);
+}
+template <bool TR, int SR, int SI>
+__device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* B, bool live) {
   if (!live) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wr = w / WC, wc = w % WC;
@@ -149,9 +153,10 @@ __device__ __forceinline__ void tile_mma(Acc& c, const double* A, const double* 
     for (int mt = 0; mt < 2; ++mt) {
       const int r = wr * 16 + mt * 8 + (lane >> 2);
       const int o = TR ? k * PA + r : r * PA + k;
-      ar[mt] = sr * A[o];
-      ai[mt] = si * Ai[o];
-      nai[mt] = -ai[mt];
+      const double xr = A[o], xi = Ai[o];
+      ar[mt] = SR > 0 ? xr : sgnflip(xr);
+      ai[mt] = SI > 0 ? xi : sgnflip(xi);
+      nai[mt] = SI > 0 ? sgnflip(xi) : xi;
     }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -303,7 +308,6 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
   // chunk group of this CTA: one chunk if G >= C, else chunks g, g + G, ...
   const int S = G >= C ? G / C + (g % C < G % C ? 1 : 0) : 1;
   const int sub = G >= C ? g / C : 0;
-  const double conj_i = TR ? -1.0 : 1.0;  // Im sign of the streamed M tiles
   double* Xt = s;                      // X_{b(t)} chunk (B operand of every product this step)
   double* Xn = s + XTILE;              // X_{b(t+1)} chunk (look-ahead)
   double* T0 = s + 2 * XTILE;          // operator stage 0
@@ -324,7 +328,7 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
       __syncthreads();
       Acc acc;
       acc_zero(acc);
-      tile_mma<false>(acc, T0, Xt, 1.0, 1.0, c * CW + wcol < a.nrhs);
+      tile_mma<false, 1, 1>(acc, T0, Xt, c * CW + wcol < a.nrhs);
       acc_store<VEC>(a, b0, c * CW, acc);
       __syncthreads();
       publish(fin(b0, c), 1);
@@ -362,8 +366,8 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
         __syncthreads();
         Acc acc;
         acc_zero(acc);
-        tile_mma<false>(acc, T0, Xn, 1.0, 1.0, live);
-        tile_mma<false>(acc, T1, Xt, -1.0, -1.0, live);
+        tile_mma<false, 1, 1>(acc, T0, Xn, live);
+        tile_mma<false, -1, -1>(acc, T1, Xt, live);
         acc_store<VEC>(a, bn, c0, acc);
         __syncthreads();
         publish(fin(bn, c), 1);
@@ -390,7 +394,7 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
             cp_async_wait<0>();
           }
           __syncthreads();
-          tile_mma<TR>(cur, Tq, Xt, -1.0, -conj_i, live);
+          tile_mma<TR, -1, (TR ? 1 : -1)>(cur, Tq, Xt, live);
           acc_store<VEC>(a, rb, c0, cur);
           __syncthreads();
         }
