@@ -31,6 +31,7 @@ _LAZY = {
     "B200DenseOps": "dense", "DeviceDenseOps": "dense", "feast_sb": "banded",
     "feast_hb": "banded", "B200BandOps": "banded", "DeviceBandOps": "banded",
     "feast_sy_distributed": "distributed", "feast_he_distributed": "distributed",
+    "feast_sy_intervals": "distributed", "feast_he_intervals": "distributed",
 }
 
 
@@ -47,6 +48,7 @@ __all__ = [
     "DeviceBandOps", "DeviceDenseOps", "EigenResult", "FeastParams", "HermitianRci",
     "QuadratureRule", "RciTask", "ReducedSolverError", "SingularMatrixError", "SolverOptions",
     "SymmetricRci", "build_contour", "check_problem", "feast_hb", "feast_he", "feast_sb",
-    "feast_sy", "feastinit", "gauss_legendre", "info_classification", "info_description",
+    "feast_sy", "feast_sy_distributed", "feast_he_distributed", "feast_sy_intervals",
+    "feast_he_intervals", "feastinit", "gauss_legendre", "info_classification", "info_description",
     "run_rci", "validate_params",
 ]

@@ -97,3 +97,45 @@ def test_partial_q_allreduce_matches_serial_sum(herm):
     if herm:
         got = got[0] + 1j * got[1]
     assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("world,nint", [(1, 1), (1, 3), (2, 1), (3, 2), (8, 2), (8, 3), (2, 5), (8, 8)])
+def test_split_ranks(world, nint):
+    from paper_1203_4031_b200.distributed import split_ranks
+    blocks = split_ranks(world, nint)
+    assert len(blocks) == nint and all(blocks)
+    if world >= nint:   # disjoint contiguous blocks covering every rank, balanced
+        assert sorted(r for b in blocks for r in b) == list(range(world))
+        assert max(map(len, blocks)) - min(map(len, blocks)) <= 1
+    else:               # one rank per interval, round robin
+        assert [b[0] for b in blocks] == [i % world for i in range(nint)]
+
+
+def _interval_worker(rank, world, port, nint, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1203_4031_b200.distributed import feast_intervals, split_ranks
+
+    def solve(i, sub):
+        # stands in for feast_*_distributed on the sub-communicator: a collective
+        # inside the sub-group (all its ranks must take part, no other rank)
+        t = torch.tensor([float(rank + 1)])
+        if sub is not None:
+            dist.all_reduce(t, group=sub)
+        return {"interval": i, "sum": float(t.item())}
+
+    res = feast_intervals(solve, nint)
+    blocks = split_ranks(world, nint)
+    want = [{"interval": i, "sum": float(sum(r + 1 for r in b))} for i, b in enumerate(blocks)]
+    out[rank] = int(res == want)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nint", [(2, 1), (3, 2), (4, 2), (2, 3)])
+def test_feast_intervals_subgroups(world, nint):
+    """First-level parallelism (fpm(9) analogue): every interval solved on its
+    own rank sub-group, every rank gets every interval's result."""
+    out = mp.Manager().dict()
+    mp.spawn(_interval_worker, args=(world, _free_port(), nint, out), nprocs=world, join=True)
+    assert [out[r] for r in range(world)] == [1] * world

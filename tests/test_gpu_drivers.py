@@ -253,3 +253,21 @@ def test_reference_ops_protocol_adapter(rng):
     r = fb.run_rci(k, B200DenseOps(a), fb.SolverOptions())
     assert r.info == 0 and r.m == 8
     assert np.abs(r.e[:8] - ev[10:18]).max() <= 1e-10
+
+
+def test_intervals_match_separate_solves():
+    """First-level parallelism on one GPU (no process group): the intervals
+    are solved one after the other and equal independent feast_sy calls."""
+    import paper_1203_4031_b200 as fb
+    rng = np.random.default_rng(91)
+    n = 200
+    g = rng.standard_normal((n, n))
+    a = (g + g.T) / (2 * np.sqrt(n))
+    ev = np.linalg.eigvalsh(a)
+    iv = [(0.5 * (ev[79] + ev[80]), 0.5 * (ev[89] + ev[90])), (0.5 * (ev[99] + ev[100]), 0.5 * (ev[111] + ev[112]))]
+    rs = fb.feast_sy_intervals(a, iv, 20)
+    for (lo, hi), r in zip(iv, rs):
+        one = fb.feast_sy(a, lo, hi, 20)
+        assert r.info == one.info == 0 and r.m == one.m
+        assert np.array_equal(r.e[:r.m], one.e[:one.m])
+    assert [r.m for r in rs] == [10, 12]
