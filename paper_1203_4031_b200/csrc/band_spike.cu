@@ -753,8 +753,9 @@ __device__ __forceinline__ void fwd_step(double (&wr)[KL + 1], double (&wi)[KL +
 // for every thread's column, the SC right-hand-side rows that will ENTER the
 // register window during the chunk, one chunk ahead by cp.async (no register
 // queue; the load of a row is issued ~SC steps of the whole CTA before use).
-constexpr int SC = 12;
-size_t sweep_xring_bytes(int nt) { return sizeof(double) * 2 * SC * 2 * (size_t)nt; }
+constexpr int SC = 12;   // forward sweep (4 CTAs per SM)
+constexpr int SCB = 24;  // backward sweep: register-bound at 2 CTAs per SM, so longer chunks halve its barriers
+size_t sweep_xring_bytes(int nt, int sc = SC) { return sizeof(double) * 2 * sc * 2 * (size_t)nt; }
 
 template <int KL>
 __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) {
@@ -863,22 +864,22 @@ __global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) 
   const double* Wi = a.wi + k * a.sw;
   double* Xr = a.xr + k * a.sx;
   double* Xi = a.xi + k * a.sx;
-  extern __shared__ double sx[];         // [2 buf][SC rows][2 planes][nt]
-  __shared__ double2 su[2][SC][KV + 1];  // U column j (rows j-KV..j); slot KV <- 1/U_jj
+  extern __shared__ double sx[];         // [2 buf][SCB rows][2 planes][nt]
+  __shared__ double2 su[2][SCB][KV + 1];  // U column j (rows j-KV..j); slot KV <- 1/U_jj
   const int xtop = hi - 2 - KV;          // row entering the window at step hi-1
   auto stage = [&](int buf, int c) {
-    const int j1 = hi - 1 - c * SC;
-    for (int e = tid; e < SC * (KV + 1); e += nt) {
+    const int j1 = hi - 1 - c * SCB;
+    for (int e = tid; e < SCB * (KV + 1); e += nt) {
       const int jj = e / (KV + 1), i = e % (KV + 1), j = j1 - jj;
       const bool ok = j >= lo;
       const long long o = ok ? (long long)j * LW + i : 0;
       cp_async8(&su[buf][jj][i].x, Wr + o, ok);
       cp_async8(&su[buf][jj][i].y, Wi + o, ok);
     }
-    double* xb = sx + (size_t)buf * SC * 2 * nt;
+    double* xb = sx + (size_t)buf * SCB * 2 * nt;
 #pragma unroll
-    for (int r = 0; r < SC; ++r) {
-      const int row = xtop - c * SC - r;
+    for (int r = 0; r < SCB; ++r) {
+      const int row = xtop - c * SCB - r;
       const bool ok = on && row >= lo;
       const long long o = ok ? (long long)row * a.ldx + col : 0;
       cp_async8(xb + (r * 2) * nt + tid, Xr + o, ok);
@@ -897,7 +898,7 @@ __global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) 
       wi_[t] = Xi[o];
     }
   }
-  const int nch = (hi - lo + SC - 1) / SC;
+  const int nch = (hi - lo + SCB - 1) / SCB;
   stage(0, 0);
   for (int c = 0; c < nch; ++c) {
     const int buf = c & 1;
@@ -908,14 +909,14 @@ __global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) 
       cp_async_wait<0>();
     }
     __syncthreads();
-    for (int jj = tid; jj < SC; jj += nt) {
+    for (int jj = tid; jj < SCB; jj += nt) {
       const double2 d = su[buf][jj][KV];
       const double den = d.x * d.x + d.y * d.y;
       su[buf][jj][KV] = den > 0.0 ? make_double2(d.x / den, -d.y / den) : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    const int j1 = hi - 1 - c * SC, jn = min(SC, j1 - lo + 1);
-    const double* xb = sx + (size_t)buf * SC * 2 * nt;
+    const int j1 = hi - 1 - c * SCB, jn = min(SCB, j1 - lo + 1);
+    const double* xb = sx + (size_t)buf * SCB * 2 * nt;
 #pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
       const int j = j1 - jj;
@@ -1047,16 +1048,16 @@ CkFn correct_fn(int kl) {
 cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
   const int nw = std::min(SNW, ceil_div(ps.nrhs, 32));
   const dim3 grid(ps.P, ceil_div(ps.nrhs, 32 * nw), count);
-  const size_t smem = sweep_xring_bytes(32 * nw);
   static bool cfg[KLMAX + 1] = {};
   if (!cfg[ps.kl]) {  // sized for the widest CTA (SNW warps)
-    const int mx = (int)sweep_xring_bytes(32 * SNW);
-    cudaFuncSetAttribute(psolve_fwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(psolve_bwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(psolve_fwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sweep_xring_bytes(32 * SNW, SC));
+    cudaFuncSetAttribute(psolve_bwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sweep_xring_bytes(32 * SNW, SCB));
     cfg[ps.kl] = true;
   }
-  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, smem, st>>>(ps);
-  psolve_bwd_fn(ps.kl)<<<grid, 32 * nw, smem, st>>>(ps);
+  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, sweep_xring_bytes(32 * nw, SC), st>>>(ps);
+  psolve_bwd_fn(ps.kl)<<<grid, 32 * nw, sweep_xring_bytes(32 * nw, SCB), st>>>(ps);
   count_launch(2);
   return cudaGetLastError();
 }
