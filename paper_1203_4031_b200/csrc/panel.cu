@@ -757,11 +757,12 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
   count_launch();
   if (rows <= rpc_cluster || (g_cluster_ok && rows <= max_cluster * rpc_cluster)) {
     int G = std::max(1, std::min(max_cluster, ceil_div(rows, rpc_cluster)));
-    static int rmin = 0;
-    if (!rmin) {
-      const char* e = getenv("FB_PANEL_RPC");
-      rmin = e ? std::max(64, std::min(rpc_cluster, atoi(e))) : 384;  // fewest CTAs: SMs stay with the GEMM
-    }
+    // rows per CTA: a batch of shifts leaves the SMs to the concurrent trailing
+    // GEMMs (384: fewest CTAs, +1-3 % at 8 shifts); a lone shift is panel-latency
+    // bound and wants the shortest per-CTA column work (192: 28.2 vs 31.1 ms
+    // for one N = 4096 LU)
+    static const int rforce = getenv("FB_PANEL_RPC") ? std::max(64, std::min(rpc_cluster, atoi(getenv("FB_PANEL_RPC")))) : 0;
+    const int rmin = rforce ? rforce : (count >= 4 ? 384 : 192);
     if (rows > 2 * PW) G = std::max(G, std::min(max_cluster, ceil_div(rows, rmin)));
     G = std::max(1, std::min(G, rows / PW));
     int rpc = ceil_div(rows, G);
