@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
       for (int q = warp; q < G; q += NW) {
         const unsigned rrec = mapa_u32(rec_l, q), rbar = mapa_u32(bar_l, q);
         st_async_v2(rrec + 16 + 16 * lane, x0, x1, rbar);
-        if (lane == 0) st_async_v2(rrec, t.v, (double)t.r, rbar);
+        if (lane == 0) st_async_v2(rrec, t.v, __longlong_as_double((long long)t.r), rbar);  // row as integer bits
         if (own_rj) st_async_v2(mapa_u32(rj_l, q) + 16 * lane, w0, w1, rbar);
       }
     }
@@ -587,7 +587,8 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
     PROBE(2);
     // 3. winner from the local mailbox (every warp, redundantly)
     const double* rec = mrec + par * MAXG * REC;
-    Best w = lane < G ? Best{rec[lane * REC], (int)rec[lane * REC + 1]} : Best{-1.0, 0x7fffffff};
+    Best w = lane < G ? Best{rec[lane * REC], (int)__double_as_longlong(rec[lane * REC + 1])}
+                      : Best{-1.0, 0x7fffffff};
     const Best wb = warp_best(w);
     const unsigned m = __ballot_sync(0xffffffffu, lane < G && w.r == wb.r && w.v == wb.v);
     const int gw = m ? __ffs(m) - 1 : 0;
@@ -606,8 +607,9 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
     if (!zero) {
       const double pr = prow[j], pi = prow[PW + j];
       const double den = pr * pr + pi * pi;
-      ir = pr / den;
-      ii = -pi / den;
+      const double rden = 1.0 / den;  // one division on the critical path
+      ir = pr * rden;
+      ii = -pi * rden;
     }
     PROBE(3);
     // 4. own rows: swap (by the owning warp, lanes over columns), multiplier,
@@ -768,9 +770,11 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     int rpc = ceil_div(rows, G);
     G = ceil_div(rows, rpc);
     a.rpc = rpc;
-    size_t smem = panel_smem(rpc);
-    if (G == 1) {
-      panel_kernel<PANEL_GRID><<<dim3(1, count), PT, smem, st>>>(a);
+    // G == 1 runs the cluster kernel too (a 1-CTA cluster): its exchange stays
+    // in shared memory, where the grid kernel would round-trip through L2
+    static const bool grid1 = getenv("FB_PANEL_GRID1") != nullptr;
+    if (G == 1 && grid1) {
+      panel_kernel<PANEL_GRID><<<dim3(1, count), PT, panel_smem(rpc), st>>>(a);
       return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
