@@ -68,7 +68,15 @@ def test_full_config_parity(tag):
         assert r.info in infos, (r.m0, r.info, infos)
         assert min(loops) - 1 <= r.loop <= max(loops) + 1, (r.m0, r.loop, traj)
     assert np.abs(r.e[:m] - g["e"][:m]).max() <= 1e-10 * s
-    assert r.res[:m].max() <= 1e-10
+    if r.info == 0:
+        assert r.res[:m].max() <= 1e-10
+    else:
+        # info 2 (loop budget spent, FEAST makes no convergence claim) occurs
+        # only on trajectories where the reference also ends with info 2
+        # (checked above); a spurious Ritz value wandering through the
+        # interval can leave one genuine pair a few 1e-10 off
+        # (profiles/r01_c3_shrink_sensitivity.txt)
+        assert r.res[:m].max() <= 1e-9
     if m0_ref == w.m0:
         assert r.m0 == w.m0
     else:
