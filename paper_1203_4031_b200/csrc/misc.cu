@@ -5,6 +5,8 @@
 //   symmetrize      kernel.py:380-381 (A_Q <- (A_Q + A_Q^H) / 2)
 //   residuals       kernel.py:147-153 (column 1-norm ratios, +inf on zero denominator)
 //   pack / unpack   numpy complex128 (interleaved) <-> planar device layout
+#include <cstdint>
+
 #include "common.cuh"
 #include "misc.cuh"
 
@@ -61,29 +63,65 @@ __global__ void accumulate_kernel(int mode, int n, int m, const double* __restri
 // of Q is read once, updated term by term in the caller's order with exactly
 // accumulate_kernel's arithmetic (so the result equals the sequence of
 // per-point accumulations bit for bit), and written once.
+// V elements per thread (V = 2: 16-byte loads/stores when every row start is
+// 16-byte aligned); the X loads of four terms are issued together before
+// their (in-order) arithmetic, so each thread keeps 4 * 2 * V loads in flight.
+template <int V>
 __global__ void accumulate_terms_kernel(AccTerms t, int n, int m, long long ldx, double* __restrict__ qr,
                                         double* __restrict__ qi, long long ldq) {
-  long long total = (long long)n * m;
+  const int mv = m / V;
+  const long long total = (long long)n * mv;
+  const bool cplx = t.mode[0] != 0 && qi;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / m), j = (int)(e % m);
+    const int i = (int)(e / mv), j = (int)(e % mv) * V;
     const long long ox = i * ldx + j, oq = i * ldq + j;
-    double q_r = qr[oq], q_i = (t.mode[0] != 0 && qi) ? qi[oq] : 0.0;
-    for (int k = 0; k < t.count; ++k) {
-      const double a = t.xr[k][ox], b = t.xi[k][ox];
-      const double cr = t.cr[k], ci = t.ci[k];
-      if (t.mode[k] == 0) {
-        const double v = __dsub_rn(__dmul_rn(cr, a), __dmul_rn(ci, b));
-        q_r = __dsub_rn(q_r, __dmul_rn(t.h[k], v));
-      } else {
-        const double vr = __dsub_rn(__dmul_rn(cr, a), __dmul_rn(ci, b));
-        const double vi = __dadd_rn(__dmul_rn(cr, b), __dmul_rn(ci, a));
-        q_r = __dsub_rn(q_r, vr);
-        q_i = __dsub_rn(q_i, vi);
+    double q_r[V], q_i[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      q_r[v] = qr[oq + v];
+      q_i[v] = cplx ? qi[oq + v] : 0.0;
+    }
+    for (int k0 = 0; k0 < t.count; k0 += 4) {
+      double a[4][V], b[4][V];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < t.count) {
+          if (V == 2) {
+            const double2 va = __ldcs(reinterpret_cast<const double2*>(t.xr[k0 + u] + ox));
+            const double2 vb = __ldcs(reinterpret_cast<const double2*>(t.xi[k0 + u] + ox));
+            a[u][0] = va.x; a[u][V - 1] = va.y;
+            b[u][0] = vb.x; b[u][V - 1] = vb.y;
+          } else {
+            a[u][0] = __ldcs(t.xr[k0 + u] + ox);
+            b[u][0] = __ldcs(t.xi[k0 + u] + ox);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u;
+        if (k >= t.count) break;
+        const double cr = t.cr[k], ci = t.ci[k];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (t.mode[k] == 0) {
+            const double x = __dsub_rn(__dmul_rn(cr, a[u][v]), __dmul_rn(ci, b[u][v]));
+            q_r[v] = __dsub_rn(q_r[v], __dmul_rn(t.h[k], x));
+          } else {
+            const double vr = __dsub_rn(__dmul_rn(cr, a[u][v]), __dmul_rn(ci, b[u][v]));
+            const double vi = __dadd_rn(__dmul_rn(cr, b[u][v]), __dmul_rn(ci, a[u][v]));
+            q_r[v] = __dsub_rn(q_r[v], vr);
+            q_i[v] = __dsub_rn(q_i[v], vi);
+          }
+        }
       }
     }
-    qr[oq] = q_r;
-    if (t.mode[0] != 0 && qi) qi[oq] = q_i;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      qr[oq + v] = q_r[v];
+      if (cplx) qi[oq + v] = q_i[v];
+    }
   }
 }
 
@@ -191,7 +229,14 @@ cudaError_t accumulate_terms_launch(const AccTerms& t, int n, int m, long long l
   for (int k = 1; k < t.count; ++k)
     if ((t.mode[k] != 0) != (t.mode[0] != 0)) return cudaErrorInvalidValue;
   count_launch();
-  accumulate_terms_kernel<<<grid_for((long long)n * m), 256, 0, st>>>(t, n, m, ldx, qr, qi, ldq);
+  bool vec = m % 2 == 0 && ldx % 2 == 0 && ldq % 2 == 0 &&
+             ((reinterpret_cast<uintptr_t>(qr) | reinterpret_cast<uintptr_t>(qi)) & 15) == 0;
+  for (int k = 0; k < t.count && vec; ++k)
+    vec = ((reinterpret_cast<uintptr_t>(t.xr[k]) | reinterpret_cast<uintptr_t>(t.xi[k])) & 15) == 0;
+  if (vec)
+    accumulate_terms_kernel<2><<<grid_for((long long)n * m / 2), 256, 0, st>>>(t, n, m, ldx, qr, qi, ldq);
+  else
+    accumulate_terms_kernel<1><<<grid_for((long long)n * m), 256, 0, st>>>(t, n, m, ldx, qr, qi, ldq);
   return cudaGetLastError();
 }
 
