@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstdint>
 #include <mutex>
@@ -493,10 +494,40 @@ cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, 
   return cudaGetLastError();
 }
 
+static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
+                                    long long ld, long long slu, const double* dinv, const double* gmat,
+                                    long long sdinv, double* xre, double* xim, long long ldx, long long sx,
+                                    cudaStream_t st);
+
+// The right-hand sides of all items are read and rewritten by every step
+// (right-looking accumulators), so the batch is swept in groups whose
+// accumulators fit in L2 (FB_SWEEP_L2MB, default 64 MB): past that the
+// accumulator traffic spills to HBM (C3: 321 MB of X for 16 shifts).
 cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                          long long ld, long long slu, const double* dinv, const double* gmat, long long sdinv,
                          double* xre, double* xim, long long ldx, long long sx, cudaStream_t st) {
   if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
+  static const double budget = 1048576.0 * (getenv("FB_SWEEP_L2MB") ? atof(getenv("FB_SWEEP_L2MB")) : 64.0);
+  const double item = 16.0 * (double)n * (double)nrhs;
+  int group = count;
+  if (count * item > 1.5 * budget) {  // C2's 84 MB stays one launch; C3's 321 MB goes in 3-shift groups
+    const int per = std::max(1, (int)(budget / item));
+    group = ceil_div(count, ceil_div(count, per));  // balanced
+  }
+  for (int b0 = 0; b0 < count; b0 += group) {
+    const int cnt = std::min(group, count - b0);
+    cudaError_t e = sweep_launch_one(variant, n, nrhs, cnt, lre + b0 * slu, lim + b0 * slu, ld, slu,
+                                     dinv + b0 * sdinv, gmat + b0 * sdinv, sdinv, xre + b0 * sx, xim + b0 * sx,
+                                     ldx, sx, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
+                                    long long ld, long long slu, const double* dinv, const double* gmat,
+                                    long long sdinv, double* xre, double* xim, long long ldx, long long sx,
+                                    cudaStream_t st) {
   SweepArgs a{};
   a.n = n; a.nrhs = nrhs; a.nblk = ceil_div(n, BS); a.variant = variant;
   a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
