@@ -754,7 +754,7 @@ __device__ __forceinline__ void fwd_step(double (&wr)[KL + 1], double (&wi)[KL +
 // register window during the chunk, one chunk ahead by cp.async (no register
 // queue; the load of a row is issued ~SC steps of the whole CTA before use).
 constexpr int SC = 12;   // forward sweep (4 CTAs per SM)
-constexpr int SCB = 24;  // backward sweep: register-bound at 2 CTAs per SM, so longer chunks halve its barriers
+constexpr int SCB = 12;  // backward sweep chunk (4 CTAs per SM at <= 168 registers)
 size_t sweep_xring_bytes(int nt, int sc = SC) { return sizeof(double) * 2 * sc * 2 * (size_t)nt; }
 
 template <int KL>
@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
 // registers; the U column (re, im interleaved, 1/U_jj computed per chunk)
 // and the rows entering the window come from shared memory.
 template <int KL>
-__global__ void __launch_bounds__(SNW * 32, 2) band_psolve_bwd_kernel(PSArgs a) {
+__global__ void __launch_bounds__(SNW * 32, 4) band_psolve_bwd_kernel(PSArgs a) {
   constexpr int KV = 2 * KL, LW = 3 * KL + 1;
   const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, nt = blockDim.x;
   const int col = blockIdx.y * nt + tid;
