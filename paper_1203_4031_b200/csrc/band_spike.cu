@@ -118,7 +118,25 @@ __global__ void __launch_bounds__(WPB * 32) band_pfactor_kernel(PFArgs a) {
   }
   int rb = 0, cb = 0;  // slots of row j / column j
   int ju = lo, bad = 0;
+  // Entries entering the window at step j (row j+RW at columns j+1+c, column
+  // j+CW at rows j+1+i) depend only on A, B and z: they are fetched QF steps
+  // ahead into a register queue so the global latency is off the column chain.
+  constexpr int QF = 4;
+  struct Ent {
+    double r0, i0, r1, i1, cr, ci;
+  };
+  auto fetch = [&](int jj) {
+    Ent e{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (lane < CW) S(jj + RW, jj + 1 + lane, e.r0, e.i0);
+    if (lane + 32 < CW) S(jj + RW, jj + 1 + lane + 32, e.r1, e.i1);
+    if (lane < kl) S(jj + 1 + lane, jj + CW, e.cr, e.ci);
+    return e;
+  };
+  Ent q[QF];
+#pragma unroll
+  for (int d = 0; d < QF; ++d) q[d] = fetch(lo + d);
   for (int j = lo; j < hi; ++j) {
+    const Ent nxt = fetch(j + QF);
     __syncwarp();
     const int km = min(kl, hi - 1 - j);
     auto RS = [&](int i) { const int s = rb + i; return s >= RW ? s - RW : s; };
@@ -200,20 +218,18 @@ __global__ void __launch_bounds__(WPB * 32) band_pfactor_kernel(PFArgs a) {
     }
     __syncwarp();
     // slide: row j+kl+1 takes row j's slot, column j+2kl+1 takes column j's slot
-    const int rn = j + RW, cn = j + CW;
     for (int c = lane; c < CW; c += 32) {
-      double vr, vi;
-      S(rn, j + 1 + c, vr, vi);
-      const int cs = CS(1 + c) * RW;  // c = kv wraps onto column j's slot (= column cn)
-      xr[cs + RS(0)] = vr;
-      xi[cs + RS(0)] = vi;
+      const int cs = CS(1 + c) * RW;  // c = kv wraps onto column j's slot (= column j+CW)
+      xr[cs + RS(0)] = c < 32 ? q[0].r0 : q[0].r1;
+      xi[cs + RS(0)] = c < 32 ? q[0].i0 : q[0].i1;
     }
-    for (int i = lane; i < kl; i += 32) {
-      double vr, vi;
-      S(j + 1 + i, cn, vr, vi);
-      xr[c0 + RS(1 + i)] = vr;
-      xi[c0 + RS(1 + i)] = vi;
+    if (lane < kl) {
+      xr[c0 + RS(1 + lane)] = q[0].cr;
+      xi[c0 + RS(1 + lane)] = q[0].ci;
     }
+#pragma unroll
+    for (int d = 0; d + 1 < QF; ++d) q[d] = q[d + 1];
+    q[QF - 1] = nxt;
     rb = RS(1);
     cb = CS(1);
   }
