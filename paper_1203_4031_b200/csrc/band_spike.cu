@@ -421,13 +421,44 @@ __global__ void __launch_bounds__(RT) band_rfactor_kernel(RFArgs a) {
   __shared__ double ar[M2][2 * M2 + 1], ai[M2][2 * M2 + 1];  // [D' | I] -> [I | D'^-1]
   __shared__ double pinv[KLMAX][M2 + 1], pinvi[KLMAX][M2 + 1];  // top kl rows of the previous D'^-1
   __shared__ int s_piv;
-  auto sp = [&](int row, int col, double& vr, double& vi) {  // spike buffer entry
-    const long long o = (long long)row * w + col;
-    vr = Sr[o];
-    vi = Si[o];
+  // Interface i reads the spike rows [hi_i - kl, hi_i + kl) (all 2kl columns)
+  // and the top rows of partition i, i.e. the lower half of interface i-1's
+  // window: a ring of three windows in dynamic shared memory, the next one
+  // staged by cp.async while the current interface is factored.
+  extern __shared__ __align__(16) double swnd[];  // [3][2 planes][2kl rows][2kl cols]
+  const int wsz = 2 * w * w;
+  auto stage_win = [&](int ii) {
+    if (ii + 1 < a.P) {
+      const int h = part_lo(ii + 1, a.n, a.P);
+      double* dst = swnd + (size_t)(ii % 3) * wsz;
+      for (int e = tid; e < w * w; e += RT) {
+        const int rr = e / w, c = e % w;
+        const long long o = (long long)(h - kl + rr) * w + c;
+        cp_async8(dst + e, Sr + o, true);
+        cp_async8(dst + w * w + e, Si + o, true);
+      }
+    }
+    cp_async_commit();
   };
+  int cur_i = 0;
+  auto sp = [&](int row, int col, double& vr, double& vi) {  // spike buffer entry (windows i-1, i)
+    const int h = part_lo(cur_i + 1, a.n, a.P);
+    int ii = cur_i, rr = row - (h - kl);
+    if (rr < 0) {  // top rows of partition cur_i: lower half of window cur_i - 1
+      ii = cur_i - 1;
+      rr = row - (part_lo(cur_i, a.n, a.P) - kl);
+    }
+    const double* src = swnd + (size_t)(ii % 3) * wsz;
+    vr = src[rr * w + col];
+    vi = src[w * w + rr * w + col];
+  };
+  stage_win(0);
   for (int i = 0; i + 1 < a.P; ++i) {
     const int hi_i = part_lo(i + 1, a.n, a.P);  // first row of partition i+1
+    cur_i = i;
+    stage_win(i + 1);
+    cp_async_wait<1>();
+    __syncthreads();
     // D_i
     for (int e = tid; e < w * w; e += RT) {
       const int r = e / w, c = e % w;
@@ -1171,7 +1202,16 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   rf.n = n; rf.kl = kl; rf.P = P;
   rf.sr = sr; rf.si = si; rf.ss = sa;
   rf.dr = dr; rf.di = di; rf.fr = fr; rf.fi = fi; rf.sa = sa; rf.info = info;
-  band_rfactor_kernel<<<count, RT, 0, st>>>(rf);
+  {
+    const size_t rsm = sizeof(double) * 3 * 2 * (size_t)(2 * kl) * (2 * kl);
+    static bool rcfg = false;
+    if (!rcfg) {
+      cudaFuncSetAttribute(band_rfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double) * 3 * 2 * (2 * KLMAX) * (2 * KLMAX)));
+      rcfg = true;
+    }
+    band_rfactor_kernel<<<count, RT, rsm, st>>>(rf);
+  }
   count_launch();
   return cudaGetLastError();
 }
