@@ -200,6 +200,11 @@ def run_gpu(args):
     for _ in range(args.warmup):
         r = solve_once(A_d, B_d)
     # -- device-resident timed region -------------------------------------
+    # the host issues ~1300 launches per step: keep Python's cyclic GC from
+    # pausing the launching thread inside the timed regions
+    import gc
+    gc.collect()
+    gc.disable()
     barrier()
     launches0 = dev.launches()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -250,6 +255,7 @@ def run_gpu(args):
         tt = torch.tensor([t_e2e], device=dev.tdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
+    gc.enable()
     h2d = 2 * n * n * 8
     d2h = n * m0 * 8 + 2 * m0 * 8
 
