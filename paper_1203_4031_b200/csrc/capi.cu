@@ -13,6 +13,8 @@
 
 namespace fb {
 void panel_profile_read(unsigned long long* out);
+void panel_wall_read(unsigned long long* out4);
+double panel_events_read_ms(int* count);
 void reduced_profile_read(unsigned long long* out);
 void reduced_cluster_profile_read(unsigned long long* out);
 }
@@ -467,6 +469,16 @@ int fb_debug_panel_profile(unsigned long long* out8) {
   fb::panel_profile_read(out8);
   return FB_OK;
 }
+
+// Debug only: CTA 0 of the cluster panels, summed over launches: wall ns
+// (globaltimer), SM cycles (clock64), launch count.
+int fb_debug_panel_wall(unsigned long long* out4) {
+  fb::panel_wall_read(out4);
+  return FB_OK;
+}
+
+// Debug only (FB_PANEL_EVENTS=1): summed event time around the panel launches.
+double fb_debug_panel_events(int* count) { return fb::panel_events_read_ms(count); }
 
 int fb_debug_reduced_profile(unsigned long long* out8) {
   // single-CTA counters, or the cluster kernel's when it ran

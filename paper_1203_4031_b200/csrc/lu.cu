@@ -24,6 +24,8 @@
 // (_driver.py:46-54): each factorization is computed exactly as it would be
 // alone, so results do not depend on the batch composition.
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -179,6 +181,28 @@ __global__ void fill_int_kernel(int* p, int v, int count) {
 
 }  // namespace
 
+// FB_PANEL_EVENTS (debug): CUDA events around every panel launch
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_pev;
+static bool panel_events_on() {
+  static const bool on = getenv("FB_PANEL_EVENTS") != nullptr;
+  return on;
+}
+static void panel_events_push(cudaEvent_t a, cudaEvent_t b) { g_pev.emplace_back(a, b); }
+double panel_events_read_ms(int* count) {
+  double tot = 0.0;
+  for (auto& p : g_pev) {
+    cudaEventSynchronize(p.second);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.first, p.second);
+    tot += ms;
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  *count = (int)g_pev.size();
+  g_pev.clear();
+  return tot;
+}
+
 size_t zgetrf_scratch_bytes(int n, int count) {
   (void)n;
   return panel_scratch_bytes() * (size_t)count;
@@ -236,6 +260,11 @@ static cudaError_t swap_list_launch(const LuBatch& f, int ca, int cb, int cc, in
                                     cudaStream_t st) {
   const int ncols = std::max(0, cb - ca) + std::max(0, cd - cc);
   if (ncols <= 0) return cudaSuccess;
+  static bool sw_cfg = false;
+  if (!sw_cfg) {
+    if (carveout_max()) cudaFuncSetAttribute(swap_list_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    sw_cfg = true;
+  }
   swap_list_kernel<<<dim3(ceil_div(ncols, SW_COLS), f.count), 256, 0, st>>>(
       f.re, f.im, f.ld, f.slu, ca, std::max(ca, cb), cc, std::max(cc, cd), list, 2 * f.sdinv);
   count_launch();
@@ -286,7 +315,17 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
       pa.re = re; pa.im = im; pa.ld = ld; pa.n = n; pa.c0 = c0; pa.pw = pw;
       pa.piv = f.piv; pa.info = f.info; pa.linv = L(blk); pa.uinv = U(blk); pa.list = list;
       pa.slu = slu; pa.spiv = f.spiv; pa.sdinv = sd;
-      if ((r = panel_launch(pa, B, scratch, q))) return r;
+      if (panel_events_on()) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, q);
+        if ((r = panel_launch(pa, B, scratch, q))) return r;
+        cudaEventRecord(e1, q);
+        panel_events_push(e0, e1);
+      } else if ((r = panel_launch(pa, B, scratch, q))) {
+        return r;
+      }
       if ((r = swap_list_launch(f, k, c0, c0 + pw, k + nb, list, q))) return r;
       const int rest = k + nb - (c0 + pw);
       if (rest > 0) {
@@ -370,6 +409,7 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
   perm_kernel<<<B, 256, psmem, st>>>(n, lists, const_cast<int*>(factor_perm(f.dinv, n)), 2 * sd);
   count_launch();
   if ((e = cudaGetLastError())) return e;
+  if ((e = uinv_batched_launch(n, B, re, im, ld, slu, f.dinv, sd, st))) return e;
   return gmat_launch(n, B, re, im, ld, slu, f.dinv, sd, const_cast<double*>(factor_gmat(f.dinv, n)), st);
 }
 

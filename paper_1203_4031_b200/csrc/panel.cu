@@ -65,41 +65,67 @@ __device__ __forceinline__ Best warp_best(Best b) {
 }
 
 // Column `c` of the inverse of the unit-lower (LOWER) or upper diagonal block
-// held in rows 0..pw-1 of the CTA's panel (two partial sums break the FMA chain).
+// held in rows 0..pw-1 of the CTA's panel.  Rows are produced in blocks of 8
+// (from the top for LOWER, from the bottom for the upper block): the terms of
+// the rows already finished are summed for all 8 rows of a block at once
+// (8 independent accumulators), so only the short in-block recurrence is a
+// dependent chain.  This sits on the panel's critical path (the next GEMM
+// needs the inverse): the row-at-a-time form cost ~35 us per panel.
 template <bool LOWER>
 __device__ void tri_inverse(const PanelArgs& a, const double* sre, const double* sim, int c) {
+  constexpr int RB = 8;
   double xr[PW], xi[PW];
 #pragma unroll
-  for (int s = 0; s < PW; ++s) {
-    const int i = LOWER ? s : PW - 1 - s;
-    double sr0 = (i == c) ? 1.0 : 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
-    if (i < a.pw) {
+  for (int blk = 0; blk < PW / RB; ++blk) {
+    double ar[RB], ai[RB];
+    // rows of this block: i(rr) = LOWER ? blk*RB + rr : PW-1 - (blk*RB + rr)
 #pragma unroll
-      for (int k = 0; k < PW; k += 2) {
-        const bool in0 = LOWER ? (k < i) : (k > i && k < a.pw);
-        const bool in1 = LOWER ? (k + 1 < i) : (k + 1 > i && k + 1 < a.pw);
-        if (in0) {
-          double ur = sre[i * SP + k], ui = sim[i * SP + k];
-          sr0 -= ur * xr[k] - ui * xi[k];
-          si0 -= ur * xi[k] + ui * xr[k];
-        }
-        if (in1) {
-          double ur = sre[i * SP + k + 1], ui = sim[i * SP + k + 1];
-          sr1 -= ur * xr[k + 1] - ui * xi[k + 1];
-          si1 -= ur * xi[k + 1] + ui * xr[k + 1];
+    for (int rr = 0; rr < RB; ++rr) {
+      const int i = LOWER ? blk * RB + rr : PW - 1 - (blk * RB + rr);
+      ar[rr] = (i == c) ? 1.0 : 0.0;
+      ai[rr] = 0.0;
+    }
+    // contributions of the rows finished in earlier blocks (independent per row)
+#pragma unroll
+    for (int q = 0; q < blk * RB; ++q) {
+      const int k = LOWER ? q : PW - 1 - q;
+      const bool kin = LOWER ? true : (k < a.pw);
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr) {
+        const int i = LOWER ? blk * RB + rr : PW - 1 - (blk * RB + rr);
+        if (kin && i < a.pw) {
+          const double ur = sre[i * SP + k], ui = sim[i * SP + k];
+          ar[rr] -= ur * xr[k] - ui * xi[k];
+          ai[rr] -= ur * xi[k] + ui * xr[k];
         }
       }
     }
-    double sr = sr0 + sr1, si = si0 + si1;
-    if (!LOWER && i < a.pw) {
-      double dr = sre[i * SP + i], di = sim[i * SP + i];
-      double den = dr * dr + di * di;
-      double qr = (sr * dr + si * di) / den, qi = (si * dr - sr * di) / den;
-      sr = qr;
-      si = qi;
+    // in-block recurrence
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int i = LOWER ? blk * RB + rr : PW - 1 - (blk * RB + rr);
+      double sr = ar[rr], si = ai[rr];
+      if (i < a.pw) {
+#pragma unroll
+        for (int q = 0; q < rr; ++q) {
+          const int k = LOWER ? blk * RB + q : PW - 1 - (blk * RB + q);
+          if (LOWER || k < a.pw) {
+            const double ur = sre[i * SP + k], ui = sim[i * SP + k];
+            sr -= ur * xr[k] - ui * xi[k];
+            si -= ur * xi[k] + ui * xr[k];
+          }
+        }
+        if (!LOWER) {
+          const double dr = sre[i * SP + i], di = sim[i * SP + i];
+          const double den = dr * dr + di * di;
+          const double qr = (sr * dr + si * di) / den, qi = (si * dr - sr * di) / den;
+          sr = qr;
+          si = qi;
+        }
+      }
+      xr[i] = sr;
+      xi[i] = si;
     }
-    xr[i] = sr;
-    xi[i] = si;
   }
   double* out = LOWER ? a.linv : a.uinv;
 #pragma unroll
@@ -154,15 +180,118 @@ __device__ void panel_finish(const PanelArgs& a, const double* sre, const double
       a.list[1 + q] = s_row[q];
       a.list[1 + 2 * PW + q] = s_content[q];
     }
-  } else if (warp == 1) {
+  }
+#ifndef FB_PANEL_NO_INV
+#ifndef FB_PANEL_NO_LINV
+  else if (warp == 1) {
     tri_inverse<true>(a, sre, sim, lane);
-  } else if (warp == 2) {
-    tri_inverse<false>(a, sre, sim, lane);
+  }
+#endif
+  // the upper-block inverses are only needed by the solves: computed for all
+  // blocks at once after the factorization (uinv_batched_launch), off the
+  // panel's critical path (~30 us per panel here)
+#endif
+}
+
+
+// Inverses of the upper 32x32 diagonal blocks of a finished factorization, one
+// warp per (block, item): column `lane` by back substitution, rows in blocks
+// of 8 as tri_inverse.  Off the critical path (after the last panel).
+__global__ void uinv_kernel(int n, const double* __restrict__ re, const double* __restrict__ im, long long ld,
+                            long long slu, double* __restrict__ dinv, long long sdinv) {
+  constexpr int RB = 8;
+  const int lane = threadIdx.x & 31;
+  const int blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b = blockIdx.y;
+  const int nblk = (n + PW - 1) / PW;
+  if (blk >= nblk) return;
+  const int c0 = blk * PW, pw = min(PW, n - c0);
+  re += b * slu + (long long)c0 * ld + c0;
+  im += b * slu + (long long)c0 * ld + c0;
+  double* out = dinv + b * sdinv + (size_t)blk * 4 * PW * PW + 2 * PW * PW;
+  const int c = lane;
+  double xr[PW], xi[PW];
+#pragma unroll
+  for (int bb = 0; bb < PW / RB; ++bb) {
+    double ar[RB], ai[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int i = PW - 1 - (bb * RB + rr);
+      ar[rr] = (i == c) ? 1.0 : 0.0;
+      ai[rr] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < bb * RB; ++q) {
+      const int k = PW - 1 - q;
+      if (k < pw) {
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          const int i = PW - 1 - (bb * RB + rr);
+          if (i < pw) {
+            const double ur = __ldg(re + (long long)i * ld + k), ui = __ldg(im + (long long)i * ld + k);
+            ar[rr] -= ur * xr[k] - ui * xi[k];
+            ai[rr] -= ur * xi[k] + ui * xr[k];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int i = PW - 1 - (bb * RB + rr);
+      double sr = ar[rr], si = ai[rr];
+      if (i < pw) {
+#pragma unroll
+        for (int q = 0; q < rr; ++q) {
+          const int k = PW - 1 - (bb * RB + q);
+          if (k < pw) {
+            const double ur = __ldg(re + (long long)i * ld + k), ui = __ldg(im + (long long)i * ld + k);
+            sr -= ur * xr[k] - ui * xi[k];
+            si -= ur * xi[k] + ui * xr[k];
+          }
+        }
+        const double dr = __ldg(re + (long long)i * ld + i), di = __ldg(im + (long long)i * ld + i);
+        const double den = dr * dr + di * di;
+        const double qr = (sr * dr + si * di) / den, qi = (si * dr - sr * di) / den;
+        sr = qr;
+        si = qi;
+      }
+      xr[i] = sr;
+      xi[i] = si;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PW; ++i) {
+    out[i * PW + c] = xr[i];
+    out[PW * PW + i * PW + c] = xi[i];
   }
 }
 
+}  // namespace
+
+cudaError_t uinv_batched_launch(int n, int count, const double* re, const double* im, long long ld,
+                                long long slu, double* dinv, long long sdinv, cudaStream_t st) {
+  const int nblk = (n + PW - 1) / PW;
+  uinv_kernel<<<dim3((nblk + 3) / 4, count), 128, 0, st>>>(n, re, im, ld, slu, dinv, sdinv);
+  count_launch();
+  return cudaGetLastError();
+}
+
+namespace {
+
 // Phase timers of CTA 0 / thread 0 (read with fb_debug_panel_profile; tools/).
 __device__ unsigned long long g_panel_prof[8];
+__device__ unsigned long long g_panel_wall[4];  // CTA 0: sum of (globaltimer ns, clock64 cycles) over launches; [3]: sum of all-CTA spans
+__device__ unsigned long long g_pstart[1024], g_pend[1024];  // per panel (item 0): first CTA start, last CTA end
+[[maybe_unused]] __device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Phase probes and per-launch timing are compiled in only with
+// -DFB_PANEL_PROFILE: their same-address global atomics serialise in L2 and the
+// kernel cannot retire before they drain (~45 us per 32-column panel,
+// tools/panel_bench.cu).
+#ifdef FB_PANEL_PROFILE
 #define PROBE_START long long _t_last = clock64()
 #define PROBE(k)                                          \
   do {                                                    \
@@ -172,6 +301,14 @@ __device__ unsigned long long g_panel_prof[8];
       _t_last = _now;                                     \
     }                                                     \
   } while (0)
+#define PROF_ONLY(x) x
+#else
+#define PROBE_START
+#define PROBE(k) \
+  do {           \
+  } while (0)
+#define PROF_ONLY(x)
+#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a0) {
@@ -476,6 +613,7 @@ __global__ void __launch_bounds__(PT) panel_kernel(PanelArgs a0) {
 // thread reduces the (local) mailbox itself, so a column costs one
 // __syncthreads, one barrier.cluster and no remote reads.
 __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
+  if (a0.pw < 0) return;  // launch-cost probe (tools/panel_bench.cu)
   PanelArgs a = a0;
   {
     const long long item = a.b0 + blockIdx.y;
@@ -490,7 +628,9 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
     a.xrowr += item * a.sxs;
     a.xu += item * a.sxs;
   }
-  const long long _t_kernel0 = clock64();
+  PROF_ONLY(const long long _t_kernel0 = clock64(); const unsigned long long _g_kernel0 = gtimer();
+            if (threadIdx.x == 0 && blockIdx.y == 0 && a.b0 == 0 && a.c0 / PW < 1024)
+                atomicMin(&g_pstart[a.c0 / PW], _g_kernel0);)
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -524,7 +664,7 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  if (g == 0 && tid == 0) atomicAdd(&g_panel_prof[6], (unsigned long long)(clock64() - _t_kernel0));
+  PROF_ONLY(if (g == 0 && tid == 0) atomicAdd(&g_panel_prof[6], (unsigned long long)(clock64() - _t_kernel0));)
 
   for (int j = 0; j < a.pw; ++j) {
     PROBE_START;
@@ -687,9 +827,24 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
   }
   cl.sync();  // remote writers done before anyone exits
   __syncthreads();
-  const long long _t_fin0 = clock64();
+#ifdef FB_PANEL_EXIT_INVAL
+  if (tid == 0) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[0])) : "memory");
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[1])) : "memory");
+  }
+#endif
+#ifdef FB_PANEL_EXIT_FENCE
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
+  PROF_ONLY(const long long _t_fin0 = clock64();)
   panel_finish(a, sre, sim, s_piv, g, rbeg, cnt);
-  if (g == 0 && tid == 0) atomicAdd(&g_panel_prof[7], (unsigned long long)(clock64() - _t_fin0));
+  PROF_ONLY(if (tid == 0 && blockIdx.y == 0 && a.b0 == 0 && a.c0 / PW < 1024) atomicMax(&g_pend[a.c0 / PW], gtimer());
+            if (g == 0 && tid == 0) {
+              atomicAdd(&g_panel_prof[7], (unsigned long long)(clock64() - _t_fin0));
+              atomicAdd(&g_panel_wall[0], gtimer() - _g_kernel0);
+              atomicAdd(&g_panel_wall[1], (unsigned long long)(clock64() - _t_kernel0));
+              atomicAdd(&g_panel_wall[2], 1ull);
+            })
 }
 
 size_t panel_cluster_smem(int rpc) {
@@ -705,6 +860,30 @@ size_t panel_smem(int rpc) {
 }
 
 }  // namespace
+
+void panel_span_raw(unsigned long long* s0, unsigned long long* e0) {
+  cudaMemcpyFromSymbol(s0, g_pstart, 8);
+  cudaMemcpyFromSymbol(e0, g_pend, 8);
+}
+
+void panel_wall_read(unsigned long long* out4) {
+  static unsigned long long st[1024], en[1024];
+  cudaMemcpyFromSymbol(st, g_pstart, sizeof(st));
+  cudaMemcpyFromSymbol(en, g_pend, sizeof(en));
+  cudaMemcpyFromSymbol(out4, g_panel_wall, sizeof(unsigned long long) * 4);
+  unsigned long long sum = 0;
+  for (int i = 0; i < 1024; ++i)
+    if (en[i] > st[i] && st[i] != ~0ull) sum += en[i] - st[i];
+  out4[3] = sum;   // sum over panels of (last CTA end - first CTA start), item 0
+  for (int i = 0; i < 1024; ++i) {
+    st[i] = ~0ull;
+    en[i] = 0ull;
+  }
+  cudaMemcpyToSymbol(g_pstart, st, sizeof(st));
+  cudaMemcpyToSymbol(g_pend, en, sizeof(en));
+  unsigned long long z[4] = {0};
+  cudaMemcpyToSymbol(g_panel_wall, z, sizeof(z));
+}
 
 void panel_profile_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_panel_prof, sizeof(unsigned long long) * 8);
@@ -734,6 +913,10 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
+    if (carveout_max()) {
+      cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

@@ -28,5 +28,8 @@ struct PanelArgs {
 
 size_t panel_scratch_bytes();
 cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st);
+// upper diagonal-block inverses of a finished batched factorization (into dinv)
+cudaError_t uinv_batched_launch(int n, int count, const double* re, const double* im, long long ld,
+                                long long slu, double* dinv, long long sdinv, cudaStream_t st);
 
 }  // namespace fb
