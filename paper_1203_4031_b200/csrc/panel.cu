@@ -135,8 +135,77 @@ __device__ void tri_inverse(const PanelArgs& a, const double* sre, const double*
   }
 }
 
+// Inverse X of the unit-lower 32x32 diagonal block (rows 0..31 of the CTA's
+// panel) by all PT threads in 8x8 blocks: the four diagonal blocks by forward
+// substitution (one column per thread, chains of <= 7), then the off-diagonal
+// blocks by distance d = 1..3, X_ij = -X_ii (sum_m L_im X_mj), one entry per
+// thread -- 7 barriers instead of one warp's 32-row recurrence.  w: 64 rows of
+// pitch SP of free shared memory (X in rows 0..31, the partial products T in
+// rows 32..63).
+__device__ void linv_blocked(const PanelArgs& a, const double* Lr, const double* Li, double* wr, double* wi) {
+  constexpr int B8 = 8;
+  const int tid = threadIdx.x;
+  double* Tr = wr + PW * SP;
+  double* Ti = wi + PW * SP;
+  for (int e = tid; e < PW * PW; e += PT) {
+    const int r = e / PW, c = e % PW;
+    wr[r * SP + c] = 0.0;
+    wi[r * SP + c] = 0.0;
+  }
+  __syncthreads();
+  if (tid < PW) {  // diagonal blocks: column c of block b = c / 8
+    const int c = tid, b0 = (c / B8) * B8;
+    wr[c * SP + c] = 1.0;
+    for (int r = c + 1; r < b0 + B8; ++r) {
+      double sr = 0.0, si = 0.0;
+      for (int k = c; k < r; ++k) {
+        const double lr = Lr[r * SP + k], li = Li[r * SP + k], xr = wr[k * SP + c], xi = wi[k * SP + c];
+        sr -= lr * xr - li * xi;
+        si -= lr * xi + li * xr;
+      }
+      wr[r * SP + c] = sr;
+      wi[r * SP + c] = si;
+    }
+  }
+  __syncthreads();
+  for (int d = 1; d < PW / B8; ++d) {
+    const int nblk = PW / B8 - d;  // blocks (j + d, j), j < nblk
+    // T = sum_{k = 8j}^{8(j+d)-1} L[r][k] X[k][c]   (r in block j+d, c in block j)
+    for (int e = tid; e < nblk * B8 * B8; e += PT) {
+      const int j = e / (B8 * B8), r = (j + d) * B8 + (e / B8) % B8, c = j * B8 + e % B8;
+      double sr = 0.0, si = 0.0;
+      for (int k = j * B8; k < (j + d) * B8; ++k) {
+        const double lr = Lr[r * SP + k], li = Li[r * SP + k], xr = wr[k * SP + c], xi = wi[k * SP + c];
+        sr += lr * xr - li * xi;
+        si += lr * xi + li * xr;
+      }
+      Tr[r * SP + c] = sr;
+      Ti[r * SP + c] = si;
+    }
+    __syncthreads();
+    // X[r][c] = -sum_{k = 8(j+d)}^{r} X[r][k] T[k][c]
+    for (int e = tid; e < nblk * B8 * B8; e += PT) {
+      const int j = e / (B8 * B8), r = (j + d) * B8 + (e / B8) % B8, c = j * B8 + e % B8;
+      double sr = 0.0, si = 0.0;
+      for (int k = (j + d) * B8; k <= r; ++k) {
+        const double xr = wr[r * SP + k], xi = wi[r * SP + k], tr = Tr[k * SP + c], ti = Ti[k * SP + c];
+        sr -= xr * tr - xi * ti;
+        si -= xr * ti + xi * tr;
+      }
+      wr[r * SP + c] = sr;
+      wi[r * SP + c] = si;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < PW * PW; e += PT) {
+    const int r = e / PW, c = e % PW;
+    a.linv[e] = wr[r * SP + c];
+    a.linv[PW * PW + e] = wi[r * SP + c];
+  }
+}
+
 // Write the panel back, then (CTA 0) the interchange list and the diagonal-block inverses.
-__device__ void panel_finish(const PanelArgs& a, const double* sre, const double* sim, const int* s_piv,
+__device__ void panel_finish(const PanelArgs& a, double* sre, double* sim, const int* s_piv,
                              int g, int rbeg, int cnt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < cnt * a.pw; e += PT) {
@@ -183,7 +252,12 @@ __device__ void panel_finish(const PanelArgs& a, const double* sre, const double
   }
 #ifndef FB_PANEL_NO_INV
 #ifndef FB_PANEL_NO_LINV
-  else if (warp == 1) {
+  // unit-lower inverse: blocked over the whole CTA when rows 32..95 of the
+  // panel buffer are free scratch (written back above), else one warp
+  if (a.pw == PW && cnt >= 3 * PW) {
+    __syncthreads();
+    linv_blocked(a, sre, sim, sre + PW * SP, sim + PW * SP);
+  } else if (warp == 1) {
     tri_inverse<true>(a, sre, sim, lane);
   }
 #endif
