@@ -17,12 +17,6 @@
 
 #include <cstdlib>
 namespace fb {
-// FB_CARVEOUT_MAX=1: every LU kernel asks for the maximum shared-memory
-// carveout, so consecutive kernels never force an L1/shared reconfiguration
-inline bool carveout_max() {
-  static const bool on = getenv("FB_CARVEOUT_MAX") != nullptr;
-  return on;
-}
 
 
 constexpr int kSMs = 148;

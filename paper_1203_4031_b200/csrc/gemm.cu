@@ -413,7 +413,6 @@ cudaError_t launch_t(const GemmParams& p, cudaStream_t st) {
   static bool configured = false;  // attribute set once per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (carveout_max()) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -451,7 +450,6 @@ cudaError_t launch_fast(const GemmParams& p, cudaStream_t st) {
   static bool configured[2] = {false, false};
   if (!configured[mode1]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (carveout_max()) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     configured[mode1] = true;
   }

@@ -260,11 +260,6 @@ static cudaError_t swap_list_launch(const LuBatch& f, int ca, int cb, int cc, in
                                     cudaStream_t st) {
   const int ncols = std::max(0, cb - ca) + std::max(0, cd - cc);
   if (ncols <= 0) return cudaSuccess;
-  static bool sw_cfg = false;
-  if (!sw_cfg) {
-    if (carveout_max()) cudaFuncSetAttribute(swap_list_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    sw_cfg = true;
-  }
   swap_list_kernel<<<dim3(ceil_div(ncols, SW_COLS), f.count), 256, 0, st>>>(
       f.re, f.im, f.ld, f.slu, ca, std::max(ca, cb), cc, std::max(cc, cd), list, 2 * f.sdinv);
   count_launch();

@@ -250,8 +250,6 @@ __device__ void panel_finish(const PanelArgs& a, double* sre, double* sim, const
       a.list[1 + 2 * PW + q] = s_content[q];
     }
   }
-#ifndef FB_PANEL_NO_INV
-#ifndef FB_PANEL_NO_LINV
   // unit-lower inverse: blocked over the whole CTA when rows 32..95 of the
   // panel buffer are free scratch (written back above), else one warp
   if (a.pw == PW && cnt >= 3 * PW) {
@@ -260,11 +258,9 @@ __device__ void panel_finish(const PanelArgs& a, double* sre, double* sim, const
   } else if (warp == 1) {
     tri_inverse<true>(a, sre, sim, lane);
   }
-#endif
   // the upper-block inverses are only needed by the solves: computed for all
   // blocks at once after the factorization (uinv_batched_launch), off the
   // panel's critical path (~30 us per panel here)
-#endif
 }
 
 
@@ -901,15 +897,7 @@ __global__ void __launch_bounds__(PT) panel_cluster_kernel(PanelArgs a0) {
   }
   cl.sync();  // remote writers done before anyone exits
   __syncthreads();
-#ifdef FB_PANEL_EXIT_INVAL
-  if (tid == 0) {
-    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[0])) : "memory");
-    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&mbar[1])) : "memory");
-  }
-#endif
-#ifdef FB_PANEL_EXIT_FENCE
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-#endif
+
   PROF_ONLY(const long long _t_fin0 = clock64();)
   panel_finish(a, sre, sim, s_piv, g, rbeg, cnt);
   PROF_ONLY(if (tid == 0 && blockIdx.y == 0 && a.b0 == 0 && a.c0 / PW < 1024) atomicMax(&g_pend[a.c0 / PW], gtimer());
@@ -987,10 +975,6 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
-    if (carveout_max()) {
-      cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
