@@ -271,3 +271,31 @@ def test_intervals_match_separate_solves():
         assert r.info == one.info == 0 and r.m == one.m
         assert np.array_equal(r.e[:r.m], one.e[:one.m])
     assert [r.m for r in rs] == [10, 12]
+
+
+def test_non_resident_factors_host_tier(monkeypatch):
+    """Shifts that do not fit the factor cache are factorized into the shared
+    slot; with the host tier they are copied back from pinned host memory on
+    later passes instead of refactorized -- same results either way."""
+    import paper_1203_4031_b200 as fb
+    rng = np.random.default_rng(77)
+    n = 320
+    g = rng.standard_normal((n, n))
+    a = (g + g.T) / (2 * np.sqrt(n))
+    h = rng.standard_normal((n, n))
+    b = np.eye(n) + 0.1 * h @ h.T / n
+    ev = np.sort(np.linalg.eigvals(np.linalg.solve(b, a)).real)
+    i0 = int(np.searchsorted(ev, 0.0))
+    lo, hi = 0.5 * (ev[i0 - 7] + ev[i0 - 6]), 0.5 * (ev[i0 + 6] + ev[i0 + 7])
+    full = fb.feast_sy(a, lo, hi, 22, b=b)
+    per_mb = (16 * n * n + 4 * n) / 2**20 + 0.6      # ~one factor (+ its side store)
+    monkeypatch.setenv("FB_FACTOR_CACHE_MB", str(2 * per_mb))
+    host = fb.feast_sy(a, lo, hi, 22, b=b)
+    monkeypatch.setenv("FB_HOST_FACTORS", "0")
+    refac = fb.feast_sy(a, lo, hi, 22, b=b)
+    assert full.info == host.info == refac.info == 0
+    assert full.m == host.m == refac.m == 13
+    assert host.factorizations == 8 and refac.factorizations > 8
+    s = max(abs(lo), abs(hi))
+    assert np.abs(host.e[:host.m] - full.e[:full.m]).max() <= 1e-12 * s
+    assert np.array_equal(host.e[:host.m], refac.e[:refac.m])
