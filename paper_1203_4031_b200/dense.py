@@ -90,7 +90,7 @@ class DeviceDenseOps:
       that are factorized into one shared slot when solved (config 5 at
       N = 32768 holds ~8 of its 16 factors on one B200).  A factor built in
       the slot is kept in pinned host memory while the host has room
-      (``host_bytes``, default 70 % of available RAM; FB_HOST_FACTORS=0 turns
+      (80 % of the available RAM, at least 24 GB left free; FB_HOST_FACTORS=0 turns
       it off), so later passes copy it back over PCIe (~0.35 s for 17 GB)
       instead of refactorizing it (~3 s at N = 32768).
     """
@@ -188,7 +188,8 @@ class DeviceDenseOps:
             return 0
         try:
             import psutil
-            return int(0.7 * psutil.virtual_memory().available)
+            avail = psutil.virtual_memory().available
+            return int(max(0, min(0.8 * avail, avail - 24 * 2**30)))
         except Exception:
             return 0
 
