@@ -221,6 +221,40 @@ int fb_band_solve_batched_rhs(fb_ctx* ctx, int count, int n, int kl, int nrhs,
                               const double* y_re, const double* y_im, int64_t ldy, int64_t y_stride,
                               double* x_re, double* x_im, int64_t ldx, int64_t x_stride);
 
+/* ---- CSR backend (feast_scsr / feast_hcsr, sparse.py:430-517) ---------- */
+/* Y = M X for a full-pattern CSR matrix M (0-based int64 indptr[n+1] /
+ * indices[nnz], values planar: val_im NULL for real M) and a row-major
+ * n x m block X (x_im NULL: real).  Replaces _csr_block_matvec
+ * (sparse.py:156-169) behind _SparseOps.multiply_a / multiply_b
+ * (sparse.py:454-462).  y_im is required when M or X is complex. */
+int fb_csr_matvec(fb_ctx* ctx, int n, int m, const int64_t* indptr, const int64_t* indices,
+                  const double* val_re, const double* val_im,
+                  const double* x_re, const double* x_im, int64_t ldx,
+                  double* y_re, double* y_im, int64_t ldy);
+/* dst(i, :) = src(perm[i], :) for i < n (row gather; src_im and dst_im both
+ * NULL for real blocks).  Carries right-hand sides into and out of the
+ * bandwidth-reducing order of the CSR direct solver (the role of
+ * _SparseSymbolic.perm, sparse.py:209-212 and 292, 312-313). */
+int fb_permute_rows(fb_ctx* ctx, int n, int m, const int64_t* perm,
+                    const double* src_re, const double* src_im, int64_t lds,
+                    double* dst_re, double* dst_im, int64_t ldd);
+/* Lockstep diagonal-preconditioned BiCGStab over all m columns of B
+ * (_bicgstab + _IterativeFactor._solve_with, sparse.py:354-427): solves
+ * S X = B with S the full CSR (indptr/indices 0-based int64, planar complex
+ * values s_re/s_im) and d its diagonal (zeros replaced by 1).  b (real when
+ * b_im NULL) and x are row-major planar blocks; ldx must equal ld.
+ * phase 0 initialises (x = 0, r = rhat = b, per-column |b|); phase 1 runs
+ * `iters` more iterations and then writes istate[2m] = columns still
+ * iterating, istate[2m+1] = first failure code (0 none; -1 rho = 0,
+ * -2 rhat.v = 0, -3 t.t = 0, -4 maxiter reached: the reference's
+ * SingularMatrixError cases).  istate holds 2m+2 ints; work holds
+ * fb_bicgstab_workspace_doubles(n, m, ld) doubles. */
+int64_t fb_bicgstab_workspace_doubles(int n, int m, int64_t ld);
+int fb_bicgstab(fb_ctx* ctx, int phase, int n, int m, const int64_t* indptr, const int64_t* indices,
+                const double* s_re, const double* s_im, const double* d_re, const double* d_im,
+                const double* b_re, const double* b_im, int64_t ldb, double* x_re, double* x_im, int64_t ldx,
+                double tol, int maxiter, int iters, double* work, int64_t ld, int* istate);
+
 #ifdef __cplusplus
 }
 #endif

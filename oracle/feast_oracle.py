@@ -22,6 +22,7 @@ __all__ = [
     "reduced_eig", "column_residuals", "finalize_order", "OracleResult",
     "oracle_feast", "RefDenseOps", "RefBandOps", "LapackDenseOps",
     "LapackBandOps", "oracle_feast_sy", "oracle_feast_he", "oracle_feast_sb",
+    "CsrDirectOps", "CsrIterativeOps", "oracle_feast_csr",
 ]
 
 # params.py:11 — supported Gauss-Legendre orders
@@ -800,3 +801,120 @@ def oracle_feast_sb(ab, kla, emin, emax, m0, *, b=None, klb=None, uplo="F",
     ops = (LapackBandOps if lapack else RefBandOps)(fa, fb, kl)
     return oracle_feast(ops, fa.shape[1], m0, emin, emax, hermitian=hermitian,
                         fpm=fpm, seed=seed, x0=x0, reduced=reduced)
+
+
+# --------------------------------------------------------------------------
+# CSR backend (sparse.py:316-462)
+# --------------------------------------------------------------------------
+
+class CsrDirectOps(LapackDenseOps):
+    """_SparseOps(solver='direct') (sparse.py:430-462).  The reference's sparse
+    LU (minimum-degree order, no pivoting, sparse.py:172-313) is an exact
+    factorization of z*B - A, so its solves are answered here by zgetrf/zgetrs
+    on the dense shifted matrix; A*x / B*x are the same products."""
+
+
+class CsrIterativeOps(RefDenseOps):
+    """_SparseOps(solver='iterative'): union pattern of A and B (B = I when
+    absent) with aligned data (sparse.py:316-351), shifted data per z and
+    conj(z) (sparse.py:394-409), and the diagonal-preconditioned BiCGStab of
+    sparse.py:354-391 per right-hand-side column (sparse.py:411-427)."""
+
+    def __init__(self, a, b=None, tol=1e-3):
+        super().__init__(a, b)
+        n = a.shape[0]
+        mask = a != 0
+        mask |= (np.eye(n, dtype=bool) if b is None else b != 0)
+        self.rows, self.cols = np.nonzero(mask)          # row-major = sorted keys
+        self.indptr = np.concatenate([[0], np.cumsum(np.bincount(self.rows, minlength=n))])
+        self.a_data = a[self.rows, self.cols].astype(np.complex128)
+        bd = np.eye(n) if b is None else b
+        self.b_data = bd[self.rows, self.cols].astype(np.complex128)
+        self.tol = tol
+
+    def _matvec(self, data, x):
+        y = np.zeros(len(self.indptr) - 1, dtype=np.complex128)
+        contrib = data * x[self.cols]
+        nz = np.flatnonzero(np.diff(self.indptr) > 0)
+        y[nz] = np.add.reduceat(contrib, self.indptr[nz])
+        return y
+
+    def _operator(self, z):
+        data = z * self.b_data - self.a_data
+        diag = np.zeros(len(self.indptr) - 1, dtype=np.complex128)
+        on = self.rows == self.cols
+        diag[self.rows[on]] = data[on]
+        diag[diag == 0] = 1.0
+        return data, diag
+
+    def factorize(self, z):
+        return self._operator(z), self._operator(complex(z).conjugate())
+
+    def _bicgstab(self, data, diag, b):
+        """sparse.py:354-391, one column."""
+        maxiter = max(8 * len(diag), 200)
+        x = np.zeros_like(b)
+        r = b.copy()
+        bnorm = np.linalg.norm(b)
+        if bnorm == 0:
+            return x
+        rhat = r.copy()
+        rho = alpha = omega = 1.0 + 0j
+        v = np.zeros_like(b)
+        p = np.zeros_like(b)
+        for _ in range(maxiter):
+            rho1 = np.vdot(rhat, r)
+            if rho1 == 0:
+                raise SingularPivot(-1)
+            beta = (rho1 / rho) * (alpha / omega)
+            p = r + beta * (p - omega * v)
+            phat = p / diag
+            v = self._matvec(data, phat)
+            denom = np.vdot(rhat, v)
+            if denom == 0:
+                raise SingularPivot(-1)
+            alpha = rho1 / denom
+            s = r - alpha * v
+            if np.linalg.norm(s) <= self.tol * bnorm:
+                return x + alpha * phat
+            shat = s / diag
+            t = self._matvec(data, shat)
+            tt = np.vdot(t, t)
+            if tt == 0:
+                raise SingularPivot(-1)
+            omega = np.vdot(t, s) / tt
+            x = x + alpha * phat + omega * shat
+            r = s - omega * t
+            if np.linalg.norm(r) <= self.tol * bnorm:
+                return x
+            rho = rho1
+        raise SingularPivot(-1)
+
+    def _solve(self, op, rhs):
+        data, diag = op
+        rhs = np.asarray(rhs, dtype=np.complex128)
+        out = np.empty_like(rhs)
+        for k in range(rhs.shape[1]):
+            out[:, k] = self._bicgstab(data, diag, rhs[:, k].copy())
+        return out
+
+    def solve(self, f, rhs):
+        return self._solve(f[0], rhs)
+
+    def solve_adjoint(self, f, rhs):
+        return self._solve(f[1], rhs)
+
+
+def oracle_feast_csr(a, emin, emax, m0, *, b=None, hermitian=False, solver="direct", iter_tol=1e-3,
+                     fpm=None, seed=42):
+    """feast_scsr / feast_hcsr (sparse.py:465-517) on full dense copies a, b of
+    the expanded CSR matrices."""
+    dt = np.complex128 if hermitian else np.float64
+    a = np.asarray(a, dtype=dt)
+    b = None if b is None else np.asarray(b, dtype=dt)
+    ops = CsrDirectOps(a, b) if solver == "direct" else CsrIterativeOps(a, b, iter_tol)
+    try:
+        return oracle_feast(ops, a.shape[0], m0, emin, emax, hermitian=hermitian, fpm=fpm, seed=seed)
+    except SingularPivot:        # _driver.py:88-91: inner-solver failure -> info -2
+        n = a.shape[0]
+        return OracleResult(np.zeros(m0), np.zeros((n, m0), dtype=dt), 0, np.zeros(m0), 1.0, 0, -2, m0)

@@ -50,5 +50,5 @@ __all__ = [
     "SymmetricRci", "build_contour", "check_problem", "feast_hb", "feast_he", "feast_sb",
     "feast_sy", "feast_sy_distributed", "feast_he_distributed", "feast_sy_intervals",
     "feast_he_intervals", "feastinit", "gauss_legendre", "info_classification", "info_description",
-    "run_rci", "validate_params",
+    "run_rci", "validate_params", "CsrMatrix", "csr_matvec", "feast_scsr", "feast_hcsr", "DeviceCsrOps",
 ]

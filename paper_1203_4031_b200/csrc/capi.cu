@@ -7,6 +7,7 @@
 #include "../../include/feast_b200.h"
 #include "band.cuh"
 #include "common.cuh"
+#include "csr.cuh"
 #include "gemm.cuh"
 #include "lu.cuh"
 #include "misc.cuh"
@@ -490,6 +491,52 @@ int fb_debug_reduced_profile(unsigned long long* out8) {
   if (any)
     for (int k = 0; k < 8; ++k) out8[k] = c8[k];
   return FB_OK;
+}
+
+
+// ---- CSR backend -------------------------------------------------------------------------------
+
+int fb_csr_matvec(fb_ctx* c, int n, int m, const int64_t* indptr, const int64_t* indices, const double* vr,
+                  const double* vi, const double* xr, const double* xi, int64_t ldx, double* yr, double* yi,
+                  int64_t ldy) {
+  CTX_GUARD(c);
+  if (n < 0 || m < 0 || !indptr || !xr || !yr) return FB_ERR_ARG;
+  if ((vi || xi) && !yi) return FB_ERR_ARG;
+  return set_err(c,
+                 fb::csr_spmm_launch(n, m, reinterpret_cast<const long long*>(indptr),
+                                     reinterpret_cast<const long long*>(indices), vr, vi, xr, xi, ldx, yr, yi, ldy,
+                                     c->stream),
+                 "csr_matvec");
+}
+
+int fb_permute_rows(fb_ctx* c, int n, int m, const int64_t* perm, const double* sr, const double* si, int64_t lds,
+                    double* dr, double* di, int64_t ldd) {
+  CTX_GUARD(c);
+  if (n < 0 || m < 0 || !perm || !sr || !dr || (!si) != (!di)) return FB_ERR_ARG;
+  return set_err(c,
+                 fb::gather_rows_launch(n, m, reinterpret_cast<const long long*>(perm), sr, si, lds, dr, di, ldd,
+                                         c->stream),
+                 "permute_rows");
+}
+
+int64_t fb_bicgstab_workspace_doubles(int n, int m, int64_t ld) {
+  if (n < 0 || m < 0 || ld < m) return -1;
+  return (int64_t)fb::bicgstab_workspace_doubles(n, m, ld);
+}
+
+int fb_bicgstab(fb_ctx* c, int phase, int n, int m, const int64_t* indptr, const int64_t* indices, const double* sr,
+                const double* si, const double* dr, const double* di, const double* br, const double* bi,
+                int64_t ldb, double* xr, double* xi, int64_t ldx, double tol, int maxiter, int iters, double* work,
+                int64_t ld, int* istate) {
+  CTX_GUARD(c);
+  if (n <= 0 || m <= 0 || !indptr || !indices || !sr || !si || !dr || !di || !br || !xr || !xi || !work ||
+      !istate || ldx != ld || ld < m || (phase != 0 && phase != 1) || iters < 0)
+    return FB_ERR_ARG;
+  return set_err(c,
+                 fb::bicgstab_launch(phase, n, m, reinterpret_cast<const long long*>(indptr),
+                                     reinterpret_cast<const long long*>(indices), sr, si, dr, di, br, bi, ldb, xr,
+                                     xi, ldx, tol, maxiter, iters, work, ld, istate, c->stream),
+                 "bicgstab");
 }
 
 }  // extern "C"

@@ -1,0 +1,393 @@
+"""CSR drivers feast_scsr / feast_hcsr on the GPU (mirrors sparse.py:1-517).
+
+Storage and validation follow the reference's ``CsrMatrix`` (1-based ia/ja,
+uplo 'F'/'L'/'U', sparse.py:21-134).  The device side differs in HOW the
+shifted systems z*B - A are solved:
+
+* ``solver="direct"`` (the reference's minimum-degree sparse LU,
+  sparse.py:172-313): the union pattern of A and B is reordered once by
+  reverse Cuthill-McKee, which turns the FEM/graph matrices this interface
+  is meant for into narrow bands; the reordered pencil is then factored by
+  the GPU band LU (partitioned SPIKE kernels for bandwidth <= 16, the
+  sequential band kernel up to 127) or, when the reordered bandwidth is too
+  wide for a band to pay, by the dense DMMA LU.  Right-hand sides are
+  gathered into the reordered row order and scattered back on the device
+  (fb_permute_rows).  Both are exact factorizations, so results agree with
+  the reference's to rounding.
+* ``solver="iterative"`` (diagonal-preconditioned BiCGStab,
+  sparse.py:354-427): every right-hand-side column runs the reference's
+  recurrence in lockstep on the device, with the per-column scalars and stop
+  tests of sparse.py:354-391 (fb_bicgstab_* kernels).
+* multiply_a / multiply_b are CSR SpMMs on the expanded A and B
+  (fb_csr_matvec, sparse.py:454-462).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._driver import SolverOptions, run_rci
+from ._errors import SingularMatrixError
+from .device import Planar, get_device
+from .kernel import HermitianRci, SymmetricRci
+from .params import FeastParams, feastinit
+
+_UPLOS = ("F", "L", "U")
+_P = ctypes.c_void_p
+
+
+@dataclass
+class CsrMatrix:
+    """Compressed sparse row matrix with 1-based ``ia`` (n+1 offsets, ia[0] = 1)
+    and ``ja`` (column indices, strictly increasing per row); ``uplo`` says
+    whether the full matrix or one triangle of a symmetric/Hermitian matrix is
+    stored (sparse.py:21-62)."""
+
+    n: int
+    ia: np.ndarray
+    ja: np.ndarray
+    values: np.ndarray
+    uplo: str = "F"
+
+    def __post_init__(self):
+        self.ia = np.asarray(self.ia, dtype=np.int64)
+        self.ja = np.asarray(self.ja, dtype=np.int64)
+        self.values = np.asarray(self.values)
+        self.uplo = str(self.uplo).upper()
+        if self.uplo not in _UPLOS:
+            raise ValueError(f"invalid uplo {self.uplo!r}")
+        n = self.n
+        if self.ia.shape != (n + 1,) or self.ia[0] != 1:
+            raise ValueError("ia must have n+1 entries starting at 1")
+        counts = np.diff(self.ia)
+        if (counts < 0).any():
+            raise ValueError("ia must be non-decreasing")
+        nnz = int(self.ia[-1]) - 1
+        if self.ja.shape != (nnz,) or self.values.shape != (nnz,):
+            raise ValueError("ja/values length must equal ia[n]-1")
+        if nnz == 0:
+            return
+        if self.ja.min() < 1 or self.ja.max() > n:
+            raise ValueError("column index out of range")
+        row = self.row_of_entries()
+        same_row = row[1:] == row[:-1]
+        if (same_row & (self.ja[1:] <= self.ja[:-1])).any():
+            raise ValueError("column indices must be strictly increasing per row")
+        col = self.ja - 1
+        if self.uplo == "L" and (col > row).any():
+            raise ValueError("uplo='L' entry above the diagonal")
+        if self.uplo == "U" and (col < row).any():
+            raise ValueError("uplo='U' entry below the diagonal")
+
+    @property
+    def nnz(self) -> int:
+        return int(self.ia[-1]) - 1
+
+    def row_of_entries(self) -> np.ndarray:
+        """0-based row index of every stored entry."""
+        return np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.ia))
+
+    @classmethod
+    def from_coo(cls, n, rows, cols, values, uplo="F") -> "CsrMatrix":
+        """1-based triplets; duplicates are summed (sparse.py:67-89)."""
+        r = np.asarray(rows, dtype=np.int64)
+        c = np.asarray(cols, dtype=np.int64)
+        v = np.asarray(values)
+        uplo = str(uplo).upper()
+        if r.size and (min(r.min(), c.min()) < 1 or max(r.max(), c.max()) > n):
+            raise ValueError("coordinate index out of range 1..n")
+        if uplo == "L" and (c > r).any():
+            raise ValueError("uplo='L' triplet above the diagonal")
+        if uplo == "U" and (c < r).any():
+            raise ValueError("uplo='U' triplet below the diagonal")
+        key = (r - 1) * np.int64(n) + (c - 1)
+        order = np.argsort(key, kind="stable")
+        key, v = key[order], v[order]
+        first = np.ones(key.size, dtype=bool)
+        first[1:] = key[1:] != key[:-1]
+        starts = np.flatnonzero(first)
+        data = np.add.reduceat(v, starts) if key.size else v[:0].copy()
+        ukey = key[starts]
+        urow = ukey // max(n, 1)
+        ia = np.ones(n + 1, dtype=np.int64)
+        ia[1:] += np.cumsum(np.bincount(urow, minlength=n)[:n])
+        return cls(n, ia, ukey % max(n, 1) + 1, data, uplo)
+
+    @classmethod
+    def from_dense(cls, a, uplo="F", tol=0.0) -> "CsrMatrix":
+        a = np.asarray(a)
+        keep = np.abs(a) > tol
+        u = str(uplo).upper()
+        if u == "L":
+            keep = np.tril(keep)
+        elif u == "U":
+            keep = np.triu(keep)
+        r, c = np.nonzero(keep)
+        return cls.from_coo(a.shape[0], r + 1, c + 1, a[r, c], uplo)
+
+    def expand_full(self) -> "CsrMatrix":
+        """The uplo='F' matrix a triangle stores (off-diagonal entries mirrored,
+        conjugated when complex; sparse.py:106-117)."""
+        if self.uplo == "F":
+            return self
+        row = self.row_of_entries()
+        col = self.ja - 1
+        off = row != col
+        mirror = np.conj(self.values[off]) if np.iscomplexobj(self.values) else self.values[off]
+        return CsrMatrix.from_coo(self.n, np.concatenate([row, col[off]]) + 1,
+                                  np.concatenate([col, row[off]]) + 1,
+                                  np.concatenate([self.values, mirror]), "F")
+
+    def to_dense(self) -> np.ndarray:
+        f = self.expand_full()
+        out = np.zeros((self.n, self.n), dtype=f.values.dtype)
+        out[f.row_of_entries(), f.ja - 1] = f.values
+        return out
+
+    def to_banded(self):
+        """(2kl+1, n) full band array (row kl+i-j holds entry (i, j)) and kl."""
+        f = self.expand_full()
+        row, col = f.row_of_entries(), f.ja - 1
+        kl = int(np.abs(row - col).max()) if f.nnz else 0
+        ab = np.zeros((2 * kl + 1, self.n), dtype=f.values.dtype)
+        ab[kl + row - col, col] = f.values
+        return ab, kl
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        return csr_matvec(self, x)
+
+
+def csr_matvec(m: CsrMatrix, x: np.ndarray) -> np.ndarray:
+    """Host product with implicit triangle expansion (sparse.py:137-153); a
+    convenience of the storage class, not part of the device solve path."""
+    f = m.expand_full()
+    x = np.asarray(x)
+    xb = x.reshape(x.shape[0], -1)
+    y = np.zeros((m.n, xb.shape[1]), dtype=np.result_type(f.values.dtype, x.dtype))
+    np.add.at(y, f.row_of_entries(), f.values[:, None] * xb[f.ja - 1])
+    return y[:, 0] if x.ndim == 1 else y
+
+
+# --- device side --------------------------------------------------------------------------
+
+
+class _DeviceCsr:
+    """A full-pattern CSR matrix resident on the device (0-based int64
+    indptr/indices, values as real and optional imaginary planes)."""
+
+    def __init__(self, dev, indptr, indices, values, cplx):
+        t = dev.torch
+        self.n = len(indptr) - 1
+        self.indptr = t.from_numpy(np.ascontiguousarray(indptr, dtype=np.int64)).to(dev.tdev)
+        self.indices = t.from_numpy(np.ascontiguousarray(indices, dtype=np.int64)).to(dev.tdev)
+        v = np.asarray(values)
+        self.re = t.from_numpy(np.ascontiguousarray(v.real, dtype=np.float64)).to(dev.tdev)
+        self.im = (t.from_numpy(np.ascontiguousarray(v.imag, dtype=np.float64)).to(dev.tdev)
+                   if cplx else None)
+
+    @classmethod
+    def of(cls, dev, m: CsrMatrix, cplx):
+        return cls(dev, m.ia - 1, m.ja - 1, m.values, cplx)
+
+    def ptrs(self):
+        return (self.indptr.data_ptr(), self.indices.data_ptr(), self.re.data_ptr(),
+                None if self.im is None else self.im.data_ptr())
+
+    def apply(self, dev, X: Planar, Y: Planar):
+        ip, ix, vr, vi = self.ptrs()
+        dev.check(dev.lib.fb_csr_matvec(dev.h, self.n, X.cols, ip, ix, vr, vi, X.re, X.im, X.ld,
+                                        Y.re, Y.im, Y.ld), "csr_matvec")
+
+
+def _union_pattern(a_full: CsrMatrix, b_full: CsrMatrix | None):
+    """(rows, cols) of the union pattern of A and B (B = I when absent), the
+    pattern the shifted systems live on (sparse.py:316-351)."""
+    n = a_full.n
+    ka = a_full.row_of_entries() * np.int64(n) + (a_full.ja - 1)
+    if b_full is None:
+        kb = np.arange(n, dtype=np.int64) * np.int64(n + 1)
+    else:
+        kb = b_full.row_of_entries() * np.int64(n) + (b_full.ja - 1)
+    keys = np.union1d(ka, kb)
+    return keys // max(n, 1), keys % max(n, 1)
+
+
+def bandwidth_reducing_order(n, rows, cols):
+    """Reverse Cuthill-McKee order of a symmetric pattern: perm[i] = original
+    index of reordered row i.  Plays the role of the reference's fill-reducing
+    minimum-degree order (sparse.py:172-198, 209-212) for a band factor."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    g = sp.csr_matrix((np.ones(rows.size, dtype=np.int8), (rows, cols)), shape=(n, n))
+    return np.asarray(reverse_cuthill_mckee(g, symmetric_mode=True), dtype=np.int64)
+
+
+# band kernels handle kl <= 127; past this share of n a dense LU is cheaper
+_BAND_MAX_KL = 127
+
+
+class DeviceCsrOps:
+    """Device backend for feast_scsr / feast_hcsr (_SparseOps, sparse.py:430-462)."""
+
+    on_device = True
+
+    def __init__(self, dev, a_full: CsrMatrix, b_full: CsrMatrix | None, hermitian: bool,
+                 solver="direct", iter_tol=1e-3, dense_max_n=32768):
+        self.dev, self.hermitian, self.n = dev, hermitian, a_full.n
+        self.solver = solver
+        self.A = _DeviceCsr.of(dev, a_full, hermitian)
+        self.B = None if b_full is None else _DeviceCsr.of(dev, b_full, hermitian)
+        self.factorizations = 0
+        rows, cols = _union_pattern(a_full, b_full)
+        if solver == "iterative":
+            from ._bicgstab import DeviceBicgstab
+            self._it = DeviceBicgstab(dev, self.n, rows, cols, a_full, b_full, hermitian, iter_tol)
+            self.mode = "iterative"
+            return
+        if solver != "direct":
+            raise ValueError(f"unknown solver {solver!r}")
+        perm = bandwidth_reducing_order(self.n, rows, cols)
+        iperm = np.empty_like(perm)
+        iperm[perm] = np.arange(self.n, dtype=np.int64)
+        kl = int(np.abs(iperm[rows] - iperm[cols]).max()) if rows.size else 0
+        self.kl = kl
+        if kl <= 16 or (kl <= _BAND_MAX_KL and 8 * kl <= self.n) or self.n > dense_max_n:
+            if kl > _BAND_MAX_KL:
+                raise MemoryError(f"reordered bandwidth {kl} > {_BAND_MAX_KL} at n = {self.n}")
+            from .banded import DeviceBandOps
+            self.mode = "band"
+            FA = dev.upload(self._band(a_full, iperm, kl), cplx=hermitian)
+            FB = None if b_full is None else dev.upload(self._band(b_full, iperm, kl), cplx=hermitian)
+            self.inner = DeviceBandOps(dev, FA, FB, kl, hermitian)
+            t = dev.torch
+            self.perm = t.from_numpy(perm).to(dev.tdev)
+            self.iperm = t.from_numpy(iperm).to(dev.tdev)
+            self._tmp = None
+        else:
+            from .dense import DeviceDenseOps
+            self.mode = "dense"
+            A = dev.upload(a_full.to_dense(), cplx=hermitian)
+            B = None if b_full is None else dev.upload(b_full.to_dense(), cplx=hermitian)
+            self.inner = DeviceDenseOps(dev, A, B, hermitian)
+            # the dense backend's batched pass solves apply unchanged (no reordering)
+            self.solve_pass = self.inner.solve_pass
+            self.pass_result = self.inner.pass_result
+
+    @staticmethod
+    def _band(m: CsrMatrix, iperm, kl):
+        r, c = iperm[m.row_of_entries()], iperm[m.ja - 1]
+        ab = np.zeros((2 * kl + 1, m.n), dtype=m.values.dtype)
+        ab[kl + r - c, c] = m.values
+        return ab
+
+    # -- factorization -------------------------------------------------------------
+    def prefactorize(self, zs):
+        if self.mode == "iterative":
+            return {complex(z): self.factorize(z) for z in zs}
+        out = self.inner.prefactorize(zs)
+        self.factorizations = self.inner.factorizations
+        return out
+
+    def factorize(self, z):
+        if self.mode == "iterative":
+            self.factorizations += 1
+            return self._it.factorize(complex(z))
+        f = self.inner.factorize(z)
+        self.factorizations = self.inner.factorizations
+        return f
+
+    # -- solves --------------------------------------------------------------------
+    def _permute(self, idx, S: Planar, D: Planar):
+        dev = self.dev
+        dev.check(dev.lib.fb_permute_rows(dev.h, self.n, S.cols, idx.data_ptr(), S.re, S.im, S.ld,
+                                          D.re, D.im, D.ld), "permute_rows")
+
+    def _solve(self, f, W: Planar, adjoint):
+        if self.mode == "iterative":
+            self._it.solve(f, W, adjoint)
+            return
+        if self.mode == "dense":
+            (self.inner.solve_adjoint if adjoint else self.inner.solve)(f, W)
+            return
+        m = W.cols
+        if self._tmp is None or self._tmp.ld < m + (m & 1):
+            self._tmp = self.dev.empty(self.n, m, True, ld=m + (m & 1))
+        T = Planar(self._tmp.t, True, self.n, m, self._tmp.ld)
+        self._permute(self.perm, W, T)              # T(i) = W(perm(i))
+        (self.inner.solve_adjoint if adjoint else self.inner.solve)(f, T)
+        self._permute(self.iperm, T, W)             # W(j) = T(iperm(j))
+
+    def solve(self, f, W: Planar):
+        self._solve(f, W, False)
+
+    def solve_adjoint(self, f, W: Planar):
+        self._solve(f, W, True)
+
+    # -- products ------------------------------------------------------------------
+    def multiply_a(self, X: Planar, Y: Planar):
+        self.A.apply(self.dev, X, Y)
+
+    def multiply_b(self, X: Planar, Y: Planar):
+        if self.B is None:
+            Y.copy_from(X)
+        else:
+            self.B.apply(self.dev, X, Y)
+
+
+def _sparse_driver(a, b, emin, emax, m0, fpm, options, x0, hermitian, device=None):
+    """sparse.py:465-500 with the device ops."""
+    options = options or SolverOptions()
+    fpm = FeastParams.coerce(fpm) if fpm is not None else feastinit()
+    if not isinstance(a, CsrMatrix):
+        raise TypeError("a must be a CsrMatrix")
+    if b is not None and not isinstance(b, CsrMatrix):
+        raise TypeError("b must be a CsrMatrix")
+    n = a.n
+    single = a.values.dtype in (np.float32, np.complex64)
+    scalar = (np.complex64 if single else np.complex128) if hermitian else (np.float32 if single else np.float64)
+    t = ("C" if single else "Z") if hermitian else ("S" if single else "D")
+    routine = f"{t}FEAST_{'HCSR' if hermitian else 'SCSR'}{'GV' if b is not None else 'EV'}"
+    cls = HermitianRci if hermitian else SymmetricRci
+    kernel = cls(n, m0, emin, emax, fpm, seed=options.seed, block_size=options.block_size,
+                 dtype=scalar, routine_name=routine, device=device, host_mirror=False)
+    if b is not None and b.n != n:
+        kernel.abort(-106)
+        return kernel.result
+    if kernel.done:
+        return kernel.result
+    a_full = a.expand_full()
+    b_full = None if b is None else b.expand_full()
+    if a_full.values.dtype != scalar:
+        a_full = CsrMatrix(n, a_full.ia, a_full.ja, a_full.values.astype(scalar), "F")
+    if b_full is not None and b_full.values.dtype != scalar:
+        b_full = CsrMatrix(n, b_full.ia, b_full.ja, b_full.values.astype(scalar), "F")
+    dev = kernel.dev
+    if fpm.slot(5) == 1:
+        if x0 is None:
+            raise ValueError("fpm(5)=1 requires an initial subspace x0")
+        dev.upload(np.asarray(x0)[:, :m0], cplx=hermitian, out=kernel.X)
+    try:
+        ops = DeviceCsrOps(dev, a_full, b_full, hermitian, options.solver, options.iter_tol)
+    except MemoryError:
+        kernel.abort(-1)
+        return kernel.result
+    result = run_rci(kernel, ops, options)
+    result.factorizations = ops.factorizations
+    return result
+
+
+def feast_scsr(a, emin, emax, m0, *, b=None, fpm=None, options=None, x0=None, device=None):
+    """Real symmetric CSR driver (sparse.py:503-511); A and B may have
+    different patterns (the shifted systems use their union)."""
+    return _sparse_driver(a, b, emin, emax, m0, fpm, options, x0, False, device)
+
+
+def feast_hcsr(a, emin, emax, m0, *, b=None, fpm=None, options=None, x0=None, device=None):
+    """Complex Hermitian CSR driver (sparse.py:514-517); adjoint solves use
+    the factor of the conjugate shift."""
+    return _sparse_driver(a, b, emin, emax, m0, fpm, options, x0, True, device)

@@ -370,6 +370,99 @@ def make_config(tag, w):
           f"wall={wall:.1f}s {t}")
 
 
+def _sparse_cases():
+    """Seeded CSR pencils for the sparse golden: (name, kind, a, b, uplo, m0,
+    solver, iter_tol, fpm slots).  Node numbering is shuffled so the matrices
+    are NOT banded in the given order (the GPU reorders them)."""
+    from paper_1203_4031_b200.sparse import CsrMatrix as C
+    rng = np.random.default_rng(1203)
+    cases = []
+    # 2-D 5-point Laplacian on a 12 x 15 grid + random diagonal, shuffled
+    gx, gy = 12, 15
+    n = gx * gy
+    lap = np.zeros((n, n))
+    for i in range(gx):
+        for j in range(gy):
+            k = i * gy + j
+            lap[k, k] = 4.0 + 0.3 * rng.random()
+            for di, dj in ((1, 0), (0, 1)):
+                if i + di < gx and j + dj < gy:
+                    l = (i + di) * gy + j + dj
+                    lap[k, l] = lap[l, k] = -1.0
+    p = rng.permutation(n)
+    lap = lap[np.ix_(p, p)]
+    cases.append(("lap2d", lap, None, "F", False))
+    # 1-D FEM stiffness with random coefficients (pentadiagonal) / mass, lower storage, shuffled
+    n = 250
+    a = np.zeros((n, n))
+    for d, s in ((0, 2.0), (1, -0.7), (2, 0.2)):
+        v = s * (1 + 0.2 * rng.standard_normal(n - d))
+        a += np.diag(v, -d) + (np.diag(v, d) if d else 0)
+    b = (4 * np.eye(n) + np.eye(n, k=1) + np.eye(n, k=-1)) / 6
+    p = rng.permutation(n)
+    cases.append(("fem1d_gv", a[np.ix_(p, p)], b[np.ix_(p, p)], "L", False))
+    # complex Hermitian random sparse pattern (~6 per row), upper storage
+    n = 200
+    h = np.zeros((n, n), dtype=complex)
+    for _ in range(3 * n):
+        i, j = rng.integers(0, n, 2)
+        if i != j:
+            v = rng.standard_normal() + 1j * rng.standard_normal()
+            h[i, j] += v
+            h[j, i] += np.conj(v)
+    h += np.diag(rng.uniform(-3, 3, n))
+    cases.append(("herm_rand", h, None, "U", True))
+    # Hermitian generalized on the Laplacian's pattern, B = mass-like SPD with a different pattern
+    n = 180
+    hb = lap.astype(complex)
+    iu = np.triu_indices(n, 1)
+    nz = np.abs(hb[iu]) > 0
+    ph = np.exp(1j * rng.uniform(0, 2 * np.pi, nz.sum()))
+    vals = hb[iu].copy()
+    vals[nz] = vals[nz] * ph
+    hb[iu] = vals
+    hb[(iu[1], iu[0])] = np.conj(vals)
+    bb = np.eye(n) * 1.2 + 0.05 * (np.eye(n, k=1) + np.eye(n, k=-1))
+    cases.append(("herm_gv", hb, bb.astype(complex), "F", True))
+    return cases
+
+
+def make_sparse():
+    """feast_scsr / feast_hcsr golden runs of the reference (direct and
+    iterative inner solver) on the seeded pencils of _sparse_cases()."""
+    import scipy.linalg as sla
+    out = {}
+
+    def gap(ev, lo, hi):
+        return 0.5 * (ev[lo - 1] + ev[lo]) if lo > 0 else ev[0] - 0.1, 0.5 * (ev[hi] + ev[hi + 1])
+
+    for name, a, b, uplo, herm in _sparse_cases():
+        ev = sla.eigh(a, b, eigvals_only=True)
+        mid = int(np.argmin(np.abs(ev - np.median(ev))))
+        emin, emax = gap(ev, mid - 4, mid + 5)        # interior: 10 eigenvalues
+        lmin, lmax = gap(ev, 0, 7)                    # lowest 8 eigenvalues
+        ca = fl.CsrMatrix.from_dense(a, uplo)
+        cb = None if b is None else fl.CsrMatrix.from_dense(b, uplo)
+        out[name + "_ia"], out[name + "_ja"], out[name + "_v"] = ca.ia, ca.ja, ca.values
+        if cb is not None:
+            out[name + "_bia"], out[name + "_bja"], out[name + "_bv"] = cb.ia, cb.ja, cb.values
+        out[name + "_meta"] = np.array([a.shape[0], emin, emax, 16, int(herm), "FLU".index(uplo), lmin, lmax])
+        fn = fl.feast_hcsr if herm else fl.feast_scsr
+        runs = [("direct", 1e-3, emin, emax, "")]
+        if name in ("lap2d", "fem1d_gv"):
+            runs += [("iterative", 1e-10, lmin, lmax, "_low"), ("iterative", 1e-3, lmin, lmax, "_low")]
+        if name == "lap2d":
+            runs += [("iterative", 1e-10, emin, emax, "")]   # reference ends with info -2 (no convergence)
+        for solver, tol, e0, e1, where in runs:
+            tag = f"{name}_{solver}{'' if solver == 'direct' else '_%g' % tol}{where}"
+            t0 = time.time()
+            r = fn(ca, e0, e1, 16, b=cb, options=fl.SolverOptions(solver=solver, iter_tol=tol))
+            _pack(tag + "_", r, out)
+            print(f"{tag}: info={r.info} m={r.m} loop={r.loop} "
+                  f"maxres={np.max(r.res[:r.m]) if r.m else 0:.2e} {time.time() - t0:.1f}s")
+    _save("sparse.npz", **out)
+
+
 if __name__ == "__main__":
     from paper_1203_4031_b200 import workloads as W
     what = sys.argv[1:] or ["unit", "small"]
@@ -377,6 +470,8 @@ if __name__ == "__main__":
         make_unit()
     if "small" in what:
         make_small()
+    if "sparse" in what:
+        make_sparse()
     if "scaled" in what:
         for tag in ("c1s", "c2s", "c3s", "c5s", "c4s"):
             make_config(f"scaled_{tag}", W.scaled(tag))
