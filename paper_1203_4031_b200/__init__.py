@@ -32,6 +32,8 @@ _LAZY = {
     "feast_hb": "banded", "B200BandOps": "banded", "DeviceBandOps": "banded",
     "feast_sy_distributed": "distributed", "feast_he_distributed": "distributed",
     "feast_sy_intervals": "distributed", "feast_he_intervals": "distributed",
+    "CsrMatrix": "sparse", "csr_matvec": "sparse", "feast_scsr": "sparse", "feast_hcsr": "sparse",
+    "DeviceCsrOps": "sparse",
 }
 
 
