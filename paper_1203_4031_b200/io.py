@@ -93,6 +93,14 @@ class CooMatrix:
             out += lower.conj().T if np.iscomplexobj(out) else lower.T
         return out
 
+    def to_csr(self, uplo="F", dtype=None):
+        """CsrMatrix in the stored triangle, duplicates summed (io.py's
+        CooMatrix.to_csr, via CsrMatrix.from_coo, sparse.py:67-89)."""
+        from .sparse import CsrMatrix
+        uplo = self._checked(uplo)
+        vals = self.values if dtype is None else self.values.astype(dtype)
+        return CsrMatrix.from_coo(self.n, self.rows, self.cols, vals, uplo)
+
     def to_band(self, uplo="F", dtype=None):
         """(ab, kl): full band layout ab[kl + i - j, j] = A[i, j] and its
         half-bandwidth (the widest stored offset)."""

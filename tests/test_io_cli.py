@@ -120,14 +120,20 @@ def test_cli_missing_files_and_parse_errors_exit_two(tmp_path, capsys):
     assert "line 2" in capsys.readouterr().err
 
 
-def test_cli_sparse_format_not_in_this_build(hello, capsys):
-    from paper_1203_4031_b200.cli import main
-    assert main([hello, "--format", "sparse"]) == 2
-    assert "not available" in capsys.readouterr().err
+def test_cli_unknown_format(hello, capsys):
+    from paper_1203_4031_b200.cli import run_driver
+    assert run_driver(hello, fmt="coo") == 2
+    assert "unknown format" in capsys.readouterr().err
+
+
+def test_coo_to_csr_matches_dense_assembly():
+    coo = parse_coordinate("3 3 5\n1 1 1.0\n2 1 -1.0\n2 1 -0.5\n2 2 2.0\n3 3 4.0\n")
+    for uplo in ("F", "L"):
+        assert np.array_equal(coo.to_csr(uplo).to_dense(), coo.to_dense(uplo))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fmt", ["dense", "banded"])
+@pytest.mark.parametrize("fmt", ["sparse", "dense", "banded"])
 def test_cli_helloworld_gpu(hello, capsys, fmt):
     from paper_1203_4031_b200.cli import run_driver
     assert run_driver(hello, fmt=fmt) == 0
@@ -145,3 +151,12 @@ def test_cli_interval_error_exit_one(tmp_path, capsys):
     (tmp_path / "bad.A").write_text(HELLO_A)
     assert run_driver(str(tmp_path / "bad")) == 1
     assert "Emin>=Emax" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_cli_helloworld_gpu_iterative(hello, capsys):
+    from paper_1203_4031_b200.cli import main
+    assert main([hello, "--solver", "iterative", "--iter-tol", "1e-12"]) == 0
+    out = capsys.readouterr().out
+    assert "mode found/subspace 2 2" in out
+    assert "1 1.000000000000000e+00" in out
