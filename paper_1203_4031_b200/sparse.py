@@ -204,15 +204,19 @@ class _DeviceCsr:
 
 def _union_pattern(a_full: CsrMatrix, b_full: CsrMatrix | None):
     """(rows, cols) of the union pattern of A and B (B = I when absent), the
-    pattern the shifted systems live on (sparse.py:316-351)."""
+    pattern the shifted systems live on (sparse.py:316-351); row-major order.
+    Both inputs are row-sorted CSR, so the union is a linear-time sparse
+    pattern sum rather than a sort of the concatenated keys."""
+    import scipy.sparse as sp
     n = a_full.n
-    ka = a_full.row_of_entries() * np.int64(n) + (a_full.ja - 1)
-    if b_full is None:
-        kb = np.arange(n, dtype=np.int64) * np.int64(n + 1)
-    else:
-        kb = b_full.row_of_entries() * np.int64(n) + (b_full.ja - 1)
-    keys = np.union1d(ka, kb)
-    return keys // max(n, 1), keys % max(n, 1)
+
+    def pattern(m):
+        return sp.csr_matrix((np.ones(m.nnz, dtype=np.int8), m.ja - 1, m.ia - 1), shape=(n, n))
+
+    u = pattern(a_full) + (sp.identity(n, dtype=np.int8, format="csr") if b_full is None else pattern(b_full))
+    u.sort_indices()
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(u.indptr))
+    return rows, u.indices.astype(np.int64)
 
 
 def bandwidth_reducing_order(n, rows, cols):
