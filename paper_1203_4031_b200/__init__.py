@@ -33,7 +33,7 @@ _LAZY = {
     "feast_sy_distributed": "distributed", "feast_he_distributed": "distributed",
     "feast_sy_intervals": "distributed", "feast_he_intervals": "distributed",
     "CsrMatrix": "sparse", "csr_matvec": "sparse", "feast_scsr": "sparse", "feast_hcsr": "sparse",
-    "DeviceCsrOps": "sparse",
+    "DeviceCsrOps": "sparse", "B200CsrOps": "sparse",
 }
 
 
@@ -53,4 +53,5 @@ __all__ = [
     "feast_sy", "feast_sy_distributed", "feast_he_distributed", "feast_sy_intervals",
     "feast_he_intervals", "feastinit", "gauss_legendre", "info_classification", "info_description",
     "run_rci", "validate_params", "CsrMatrix", "csr_matvec", "feast_scsr", "feast_hcsr", "DeviceCsrOps",
+    "B200CsrOps",
 ]

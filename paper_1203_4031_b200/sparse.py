@@ -343,6 +343,50 @@ class DeviceCsrOps:
             self.B.apply(self.dev, X, Y)
 
 
+class B200CsrOps:
+    """Numpy-protocol adapter over DeviceCsrOps with _SparseOps' constructor
+    (sparse.py:430-441: full-storage A and B, solver, iter_tol), so the
+    reference's own run_rci can drive the GPU solves.  Accepts any object
+    with n / ia / ja / values (/ uplo), e.g. feastlib's CsrMatrix."""
+
+    def __init__(self, a_full, b_full, solver="direct", iter_tol=1e-3, hermitian=None, device=None):
+        def conv(m):
+            if m is None or isinstance(m, CsrMatrix):
+                return m
+            return CsrMatrix(m.n, m.ia, m.ja, m.values, getattr(m, "uplo", "F"))
+        a_full, b_full = conv(a_full).expand_full(), None if b_full is None else conv(b_full).expand_full()
+        self.hermitian = np.iscomplexobj(a_full.values) if hermitian is None else hermitian
+        self.dev = get_device(device)
+        self._ops = DeviceCsrOps(self.dev, a_full, b_full, self.hermitian, solver, iter_tol)
+        self.n = a_full.n
+
+    def factorize(self, z):
+        return self._ops.factorize(complex(z))
+
+    def _solve(self, f, rhs, adjoint):
+        W = self.dev.upload(np.asarray(rhs, dtype=np.complex128), cplx=True)
+        self._ops._solve(f, W, adjoint)
+        return self.dev.download(W)
+
+    def solve(self, f, rhs):
+        return self._solve(f, rhs, False)
+
+    def solve_adjoint(self, f, rhs):
+        return self._solve(f, rhs, True)
+
+    def _mult(self, fn, x):
+        X = self.dev.upload(np.asarray(x), cplx=self.hermitian)
+        Y = self.dev.empty(self.n, X.cols, self.hermitian)
+        fn(X, Y)
+        return self.dev.download(Y)
+
+    def multiply_a(self, x):
+        return self._mult(self._ops.multiply_a, x)
+
+    def multiply_b(self, x):
+        return self._mult(self._ops.multiply_b, x)
+
+
 def _sparse_driver(a, b, emin, emax, m0, fpm, options, x0, hermitian, device=None):
     """sparse.py:465-500 with the device ops."""
     options = options or SolverOptions()

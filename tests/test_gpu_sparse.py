@@ -209,3 +209,22 @@ def test_argument_errors():
         fb.feast_scsr(np.eye(4), -1, 1, 2)
     r = fb.feast_scsr(a, -1, 1, 2, b=fb.CsrMatrix.from_dense(np.eye(3)))
     assert r.info == -106
+
+
+@pytest.mark.parametrize("solver", ["direct", "iterative"])
+def test_numpy_ops_adapter_under_run_rci(rng, solver):
+    """B200CsrOps answers the numpy ops protocol of _SparseOps (sparse.py:430-462)
+    that the reference's own run_rci consumes (host-mirrored kernel here)."""
+    fb = _fb()
+    from paper_1203_4031_b200.sparse import B200CsrOps
+    n = 40
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    a = (a + a.conj().T) / 2
+    a = np.where(np.abs(np.subtract.outer(np.arange(n), np.arange(n))) <= 2, a, 0) + 6 * np.eye(n)
+    ev = np.linalg.eigvalsh(a)
+    emin, emax = gap_interval(ev, 0, 5)
+    k = fb.HermitianRci(n, 10, emin, emax)
+    csr = fb.CsrMatrix.from_dense(a)
+    r = fb.run_rci(k, B200CsrOps(csr, None, solver, 1e-12), fb.SolverOptions())
+    assert r.info == 0 and r.m == 6
+    assert np.abs(r.e[:6] - ev[:6]).max() <= 1e-10 * max(abs(emin), abs(emax))
