@@ -226,11 +226,14 @@ int fb_band_solve_batched_rhs(fb_ctx* ctx, int count, int n, int kl, int nrhs,
  * indices[nnz], values planar: val_im NULL for real M) and a row-major
  * n x m block X (x_im NULL: real).  Replaces _csr_block_matvec
  * (sparse.py:156-169) behind _SparseOps.multiply_a / multiply_b
- * (sparse.py:454-462).  y_im is required when M or X is complex. */
+ * (sparse.py:454-462).  y_im is required when M or X is complex.
+ * row_order (NULL: 0..n-1) is the order rows are visited in -- a
+ * bandwidth-reducing permutation keeps the gathered X rows L2-resident;
+ * results do not depend on it. */
 int fb_csr_matvec(fb_ctx* ctx, int n, int m, const int64_t* indptr, const int64_t* indices,
                   const double* val_re, const double* val_im,
                   const double* x_re, const double* x_im, int64_t ldx,
-                  double* y_re, double* y_im, int64_t ldy);
+                  double* y_re, double* y_im, int64_t ldy, const int64_t* row_order);
 /* dst(i, :) = src(perm[i], :) for i < n (row gather; src_im and dst_im both
  * NULL for real blocks).  Carries right-hand sides into and out of the
  * bandwidth-reducing order of the CSR direct solver (the role of

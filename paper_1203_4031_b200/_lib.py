@@ -59,7 +59,7 @@ SIGNATURES = {
                                           P, P, c_int64, c_int64, P, P, c_int64, c_int64]),
     "fb_band_solve_batched": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
                                       P, P, c_int64, c_int64]),
-    "fb_csr_matvec": (c_int, [P, c_int, c_int, P, P, P, P, P, P, c_int64, P, P, c_int64]),
+    "fb_csr_matvec": (c_int, [P, c_int, c_int, P, P, P, P, P, P, c_int64, P, P, c_int64, P]),
     "fb_permute_rows": (c_int, [P, c_int, c_int, P, P, P, c_int64, P, P, c_int64]),
     "fb_bicgstab_workspace_doubles": (c_int64, [c_int, c_int, c_int64]),
     "fb_bicgstab": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P, P, P, P, c_int64, P, P, c_int64, c_double,

@@ -498,14 +498,14 @@ int fb_debug_reduced_profile(unsigned long long* out8) {
 
 int fb_csr_matvec(fb_ctx* c, int n, int m, const int64_t* indptr, const int64_t* indices, const double* vr,
                   const double* vi, const double* xr, const double* xi, int64_t ldx, double* yr, double* yi,
-                  int64_t ldy) {
+                  int64_t ldy, const int64_t* row_order) {
   CTX_GUARD(c);
   if (n < 0 || m < 0 || !indptr || !xr || !yr) return FB_ERR_ARG;
   if ((vi || xi) && !yi) return FB_ERR_ARG;
   return set_err(c,
                  fb::csr_spmm_launch(n, m, reinterpret_cast<const long long*>(indptr),
                                      reinterpret_cast<const long long*>(indices), vr, vi, xr, xi, ldx, yr, yi, ldy,
-                                     c->stream),
+                                     reinterpret_cast<const long long*>(row_order), c->stream),
                  "csr_matvec");
 }
 

@@ -31,10 +31,13 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(int n, int m, const long 
                                                        const double* __restrict__ xr,
                                                        const double* __restrict__ xi, long long ldx,
                                                        double* __restrict__ yr, double* __restrict__ yi,
-                                                       long long ldy) {
-  const int row = blockIdx.x * kRowsPerCta + threadIdx.y;
+                                                       long long ldy, const long long* __restrict__ order) {
+  const int slot = blockIdx.x * kRowsPerCta + threadIdx.y;
   const int col = blockIdx.y * 32 + threadIdx.x;
-  if (row >= n) return;
+  if (slot >= n) return;
+  // rows visited in a bandwidth-reducing order: rows processed together share
+  // neighbours, so the X rows they gather are re-read from L2, not HBM
+  const long long row = order ? order[slot] : slot;
   const long long k0 = indptr[row], k1 = indptr[row + 1];
   if (col >= m) return;
   double ar = 0.0, ai = 0.0;
@@ -57,8 +60,8 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(int n, int m, const long 
       if (ACPLX) ai += b * p;
     }
   }
-  yr[(long long)row * ldy + col] = ar;
-  if (ACPLX || XCPLX) yi[(long long)row * ldy + col] = ai;
+  yr[row * ldy + col] = ar;
+  if (ACPLX || XCPLX) yi[row * ldy + col] = ai;
 }
 
 // 16-byte moves when both strides and the column count allow it
@@ -82,21 +85,21 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(int n, int mv, const l
 
 cudaError_t csr_spmm_launch(int n, int m, const long long* indptr, const long long* indices, const double* vr,
                             const double* vi, const double* xr, const double* xi, long long ldx, double* yr,
-                            double* yi, long long ldy, cudaStream_t st) {
+                            double* yi, long long ldy, const long long* order, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
   const bool acplx = vi != nullptr, xcplx = xi != nullptr;
   if ((acplx || xcplx) && yi == nullptr) return cudaErrorInvalidValue;
   count_launch();
   dim3 grid(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), block(32, kRowsPerCta);
   if (acplx && xcplx)
-    csr_spmm_kernel<true, true><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi, ldy);
+    csr_spmm_kernel<true, true><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi, ldy, order);
   else if (acplx)
-    csr_spmm_kernel<true, false><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi, ldy);
+    csr_spmm_kernel<true, false><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi, ldy, order);
   else if (xcplx)
-    csr_spmm_kernel<false, true><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi, ldy);
+    csr_spmm_kernel<false, true><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi, ldy, order);
   else
     csr_spmm_kernel<false, false><<<grid, block, 0, st>>>(n, m, indptr, indices, vr, vi, xr, xi, ldx, yr, yi,
-                                                          ldy);
+                                                          ldy, order);
   return cudaGetLastError();
 }
 
@@ -383,7 +386,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
     bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(1, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
     bicg_update_kernel<<<ugrid, ublk, 0, st>>>(1, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
     csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, st>>>(
-        n, m, indptr, indices, s_re, s_im, V.qr, V.qi, ld, V.vr, V.vi, ld);
+        n, m, indptr, indices, s_re, s_im, V.qr, V.qi, ld, V.vr, V.vi, ld, nullptr);
     bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.hr, V.hi, V.vr, V.vi, ld, status, part);
     bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(2, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
     bicg_update_kernel<<<ugrid, ublk, 0, st>>>(2, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
@@ -392,7 +395,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
     bicg_update_kernel<<<ugrid, ublk, 0, st>>>(3, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
     // columns that met the |s| test are final (status 2 -> 1)
     csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, st>>>(
-        n, m, indptr, indices, s_re, s_im, V.wr, V.wi, ld, V.tr, V.ti, ld);
+        n, m, indptr, indices, s_re, s_im, V.wr, V.wi, ld, V.tr, V.ti, ld, nullptr);
     bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.tr, V.ti, V.tr, V.ti, ld, status, part);
     bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.tr, V.ti, V.sr, V.si, ld, status, part2);
     bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(4, m, parts, part, part2, tol, maxiter, stt, status, itc);

@@ -6,7 +6,7 @@ namespace fb {
 
 cudaError_t csr_spmm_launch(int n, int m, const long long* indptr, const long long* indices, const double* vr,
                             const double* vi, const double* xr, const double* xi, long long ldx, double* yr,
-                            double* yi, long long ldy, cudaStream_t st);
+                            double* yi, long long ldy, const long long* order, cudaStream_t st);
 cudaError_t gather_rows_launch(int n, int m, const long long* perm, const double* sr, const double* si,
                                 long long lds, double* dr, double* di, long long ldd, cudaStream_t st);
 

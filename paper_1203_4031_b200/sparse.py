@@ -196,10 +196,11 @@ class _DeviceCsr:
         return (self.indptr.data_ptr(), self.indices.data_ptr(), self.re.data_ptr(),
                 None if self.im is None else self.im.data_ptr())
 
-    def apply(self, dev, X: Planar, Y: Planar):
+    def apply(self, dev, X: Planar, Y: Planar, order=None):
         ip, ix, vr, vi = self.ptrs()
         dev.check(dev.lib.fb_csr_matvec(dev.h, self.n, X.cols, ip, ix, vr, vi, X.re, X.im, X.ld,
-                                        Y.re, Y.im, Y.ld), "csr_matvec")
+                                        Y.re, Y.im, Y.ld, None if order is None else order.data_ptr()),
+                  "csr_matvec")
 
 
 def _union_pattern(a_full: CsrMatrix, b_full: CsrMatrix | None):
@@ -247,6 +248,7 @@ class DeviceCsrOps:
         self.A = _DeviceCsr.of(dev, a_full, hermitian)
         self.B = None if b_full is None else _DeviceCsr.of(dev, b_full, hermitian)
         self.factorizations = 0
+        self.row_order = None
         rows, cols = _union_pattern(a_full, b_full)
         if solver == "iterative":
             from ._bicgstab import DeviceBicgstab
@@ -256,6 +258,7 @@ class DeviceCsrOps:
         if solver != "direct":
             raise ValueError(f"unknown solver {solver!r}")
         perm = bandwidth_reducing_order(self.n, rows, cols)
+        self.row_order = dev.torch.from_numpy(perm).to(dev.tdev)    # SpMM row visiting order
         iperm = np.empty_like(perm)
         iperm[perm] = np.arange(self.n, dtype=np.int64)
         kl = int(np.abs(iperm[rows] - iperm[cols]).max()) if rows.size else 0
@@ -334,13 +337,13 @@ class DeviceCsrOps:
 
     # -- products ------------------------------------------------------------------
     def multiply_a(self, X: Planar, Y: Planar):
-        self.A.apply(self.dev, X, Y)
+        self.A.apply(self.dev, X, Y, self.row_order)
 
     def multiply_b(self, X: Planar, Y: Planar):
         if self.B is None:
             Y.copy_from(X)
         else:
-            self.B.apply(self.dev, X, Y)
+            self.B.apply(self.dev, X, Y, self.row_order)
 
 
 class B200CsrOps:

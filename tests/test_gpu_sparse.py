@@ -42,6 +42,11 @@ def test_csr_matvec_kernel(rng, acplx, xcplx):
     M.apply(dev, X, Y)
     y = dev.download(Y)
     assert np.abs(y - a @ x).max() <= 1e-12 * max(1.0, np.abs(a @ x).max())
+    # a row visiting order changes only the schedule, never the bits
+    order = dev.torch.from_numpy(rng.permutation(n).astype(np.int64)).to(dev.tdev)
+    Y2 = dev.empty(n, m, acplx or xcplx)
+    M.apply(dev, X, Y2, order)
+    assert np.array_equal(dev.download(Y2), y)
 
 
 def test_permute_rows_kernel(rng):
