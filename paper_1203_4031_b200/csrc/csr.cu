@@ -41,13 +41,8 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(int n, int m, const long 
   const long long k0 = indptr[row], k1 = indptr[row + 1];
   if (col >= m) return;
   double ar = 0.0, ai = 0.0;
-  for (long long k = k0; k < k1; ++k) {
-    const long long j = indices[k];
-    const double a = vr[k];
-    const double b = ACPLX ? vi[k] : 0.0;
-    const double p = xr[j * ldx + col];
+  auto fma_term = [&](double a, double b, double p, double q) {
     if (XCPLX) {
-      const double q = xi[j * ldx + col];
       if (ACPLX) {
         ar += a * p - b * q;
         ai += a * q + b * p;
@@ -59,6 +54,31 @@ __global__ void __launch_bounds__(256) csr_spmm_kernel(int n, int m, const long 
       ar += a * p;
       if (ACPLX) ai += b * p;
     }
+  };
+  long long k = k0;
+  // four entries' index/value loads, then their four X gathers, in flight
+  // together (the chain index -> X row is otherwise one latency per entry);
+  // the sum is still taken in pattern order
+  for (; k + 4 <= k1; k += 4) {
+    long long j[4];
+    double a[4], b[4], p[4], q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      j[u] = indices[k + u];
+      a[u] = vr[k + u];
+      b[u] = ACPLX ? vi[k + u] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      p[u] = xr[j[u] * ldx + col];
+      q[u] = XCPLX ? xi[j[u] * ldx + col] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) fma_term(a[u], b[u], p[u], q[u]);
+  }
+  for (; k < k1; ++k) {
+    const long long j = indices[k];
+    fma_term(vr[k], ACPLX ? vi[k] : 0.0, xr[j * ldx + col], XCPLX ? xi[j * ldx + col] : 0.0);
   }
   yr[row * ldy + col] = ar;
   if (ACPLX || XCPLX) yi[row * ldy + col] = ai;
