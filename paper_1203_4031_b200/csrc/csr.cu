@@ -12,7 +12,11 @@
 // stream is a warp-uniform broadcast load.  Products are accumulated in the
 // pattern's column order, the order of np.add.reduceat in the reference.
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "csr.cuh"
@@ -400,28 +404,87 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
     bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(0, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
     return cudaGetLastError();
   }
+  auto run_iters = [&](cudaStream_t q) {
   for (int it = 0; it < iters; ++it) {
-    count_launch(16);
-    bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.hr, V.hi, V.rr, V.ri, ld, status, part);
-    bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(1, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
-    bicg_update_kernel<<<ugrid, ublk, 0, st>>>(1, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
-    csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, st>>>(
+    bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.hr, V.hi, V.rr, V.ri, ld, status, part);
+    bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(1, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
+    bicg_update_kernel<<<ugrid, ublk, 0, q>>>(1, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
+    csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, q>>>(
         n, m, indptr, indices, s_re, s_im, V.qr, V.qi, ld, V.vr, V.vi, ld, nullptr);
-    bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.hr, V.hi, V.vr, V.vi, ld, status, part);
-    bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(2, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
-    bicg_update_kernel<<<ugrid, ublk, 0, st>>>(2, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
-    bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.sr, V.si, V.sr, V.si, ld, status, part);
-    bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(3, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
-    bicg_update_kernel<<<ugrid, ublk, 0, st>>>(3, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
+    bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.hr, V.hi, V.vr, V.vi, ld, status, part);
+    bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(2, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
+    bicg_update_kernel<<<ugrid, ublk, 0, q>>>(2, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
+    bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.sr, V.si, V.sr, V.si, ld, status, part);
+    bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(3, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
+    bicg_update_kernel<<<ugrid, ublk, 0, q>>>(3, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
     // columns that met the |s| test are final (status 2 -> 1)
-    csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, st>>>(
+    csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, q>>>(
         n, m, indptr, indices, s_re, s_im, V.wr, V.wi, ld, V.tr, V.ti, ld, nullptr);
-    bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.tr, V.ti, V.tr, V.ti, ld, status, part);
-    bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.tr, V.ti, V.sr, V.si, ld, status, part2);
-    bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(4, m, parts, part, part2, tol, maxiter, stt, status, itc);
-    bicg_update_kernel<<<ugrid, ublk, 0, st>>>(4, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
-    bicg_colred_kernel<<<rgrid, rblk, 0, st>>>(n, m, V.rr, V.ri, V.rr, V.ri, ld, status, part);
-    bicg_scalar_kernel<<<sgrid, sblk, 0, st>>>(5, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
+    bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.tr, V.ti, V.tr, V.ti, ld, status, part);
+    bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.tr, V.ti, V.sr, V.si, ld, status, part2);
+    bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(4, m, parts, part, part2, tol, maxiter, stt, status, itc);
+    bicg_update_kernel<<<ugrid, ublk, 0, q>>>(4, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
+    bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.rr, V.ri, V.rr, V.ri, ld, status, part);
+    bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(5, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
+  }
+  };
+  count_launch(16 * iters);
+  // The `iters`-iteration chunk is replayed from a CUDA graph captured on a
+  // private stream (16 launches per iteration; capture needs a non-legacy
+  // stream, torch's current stream is usually the legacy one).  Cached by the
+  // full argument tuple, so a hit replays exactly the same launches.
+  static const bool use_graph = [] {
+    const char* e = getenv("FB_BICG_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  if (!use_graph || iters == 0) {
+    run_iters(st);
+  } else {
+    struct Key {
+      const void* p[14];
+      long long l[3];
+      double tol;
+      int i[5];
+    } key;
+    memset(&key, 0, sizeof(key));
+    const void* ps[14] = {indptr, indices, s_re, s_im, d_re, d_im, b_re, b_im, x_re, x_im, work, istate, st, nullptr};
+    memcpy(key.p, ps, sizeof(ps));
+    key.l[0] = ldb; key.l[1] = ldx; key.l[2] = ld;
+    key.tol = tol;
+    key.i[0] = n; key.i[1] = m; key.i[2] = maxiter; key.i[3] = iters;
+    struct Entry {
+      Key k;
+      cudaGraphExec_t exec;
+    };
+    static std::vector<Entry> cache;
+    static std::mutex mu;
+    static cudaStream_t cap = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    cudaGraphExec_t exec = nullptr;
+    for (auto& e : cache)
+      if (!memcmp(&e.k, &key, sizeof(Key))) exec = e.exec;
+    if (!exec) {
+      if (!cap) {
+        cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+      }
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return e;
+      run_iters(cap);
+      e = cudaStreamEndCapture(cap, &g);
+      if (e != cudaSuccess) return e;
+      e = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return e;
+      if (cache.size() >= 64) {
+        cudaGraphExecDestroy(cache.front().exec);
+        cache.erase(cache.begin());
+      }
+      cache.push_back({key, exec});
+    }
+    cudaError_t e = cudaGraphLaunch(exec, st);
+    if (e != cudaSuccess) return e;
   }
   count_launch();
   count_active_kernel<<<1, 32, 0, st>>>(m, status, flags);
