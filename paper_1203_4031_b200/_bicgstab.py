@@ -94,11 +94,14 @@ class DeviceBicgstab:
                 op.dre.data_ptr(), op.dim.data_ptr(), W.re, W.im, W.ld, X.re, X.im, X.ld, self.tol,
                 self.maxiter)
         dev.check(dev.lib.fb_bicgstab(dev.h, 0, *args, 0, work.data_ptr(), ld, ist.data_ptr()), "bicgstab init")
-        done = 0
+        done, chunk = 0, self.chunk
         while True:
-            dev.check(dev.lib.fb_bicgstab(dev.h, 1, *args, self.chunk, work.data_ptr(), ld, ist.data_ptr()),
+            # poll after 8, 16, 32, then every 64 iterations (iterations past a
+            # column's convergence are no-ops, so only the poll cadence changes)
+            dev.check(dev.lib.fb_bicgstab(dev.h, 1, *args, chunk, work.data_ptr(), ld, ist.data_ptr()),
                       "bicgstab")
-            done += self.chunk
+            done += chunk
+            chunk = min(2 * chunk, 64)
             active, fail = (int(v) for v in ist[2 * m:2 * m + 2].cpu())
             if fail:
                 if fail == -4:
@@ -107,6 +110,6 @@ class DeviceBicgstab:
                 raise SingularMatrixError(_FAIL[fail])
             if active == 0:
                 break
-            if done > self.maxiter + self.chunk:      # cannot happen: maxiter fails first
+            if done > self.maxiter + 64:              # cannot happen: maxiter fails first
                 raise SingularMatrixError("BiCGStab iteration budget exceeded")
         W.copy_from(X)

@@ -477,7 +477,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
       e = cudaGraphInstantiate(&exec, g, 0);
       cudaGraphDestroy(g);
       if (e != cudaSuccess) return e;
-      if (cache.size() >= 64) {
+      if (cache.size() >= 256) {
         cudaGraphExecDestroy(cache.front().exec);
         cache.erase(cache.begin());
       }
