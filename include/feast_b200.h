@@ -251,12 +251,15 @@ int fb_permute_rows(fb_ctx* ctx, int n, int m, const int64_t* perm,
  * iterating, istate[2m+1] = first failure code (0 none; -1 rho = 0,
  * -2 rhat.v = 0, -3 t.t = 0, -4 maxiter reached: the reference's
  * SingularMatrixError cases).  istate holds 2m+2 ints; work holds
- * fb_bicgstab_workspace_doubles(n, m, ld) doubles. */
+ * fb_bicgstab_workspace_doubles(n, m, ld) doubles.  row_order (NULL: natural)
+ * is the SpMM row visiting order, as in fb_csr_matvec; it never changes
+ * results. */
 int64_t fb_bicgstab_workspace_doubles(int n, int m, int64_t ld);
 int fb_bicgstab(fb_ctx* ctx, int phase, int n, int m, const int64_t* indptr, const int64_t* indices,
                 const double* s_re, const double* s_im, const double* d_re, const double* d_im,
                 const double* b_re, const double* b_im, int64_t ldb, double* x_re, double* x_im, int64_t ldx,
-                double tol, int maxiter, int iters, double* work, int64_t ld, int* istate);
+                double tol, int maxiter, int iters, double* work, int64_t ld, int* istate,
+                const int64_t* row_order);
 
 #ifdef __cplusplus
 }

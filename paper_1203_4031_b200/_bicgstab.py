@@ -28,8 +28,9 @@ class _IterFactor:
 
 
 class DeviceBicgstab:
-    def __init__(self, dev, n, rows, cols, a_full, b_full, hermitian, tol, chunk=8):
+    def __init__(self, dev, n, rows, cols, a_full, b_full, hermitian, tol, chunk=8, row_order=None):
         t = dev.torch
+        self.row_order = row_order          # device int64 SpMM visiting order (RCM) or None
         self.dev, self.n, self.tol, self.chunk = dev, n, float(tol), chunk
         self.maxiter = max(8 * n, 200)
         keys = rows * np.int64(n) + cols
@@ -64,6 +65,9 @@ class DeviceBicgstab:
         op.dim = t.from_numpy(np.ascontiguousarray(diag.imag)).to(dev.tdev)
         return op
 
+    def _order(self):
+        return None if self.row_order is None else self.row_order.data_ptr()
+
     def factorize(self, z):
         f = _IterFactor()
         f.z = z
@@ -93,13 +97,14 @@ class DeviceBicgstab:
         args = (n, m, self.indptr.data_ptr(), self.indices.data_ptr(), op.re.data_ptr(), op.im.data_ptr(),
                 op.dre.data_ptr(), op.dim.data_ptr(), W.re, W.im, W.ld, X.re, X.im, X.ld, self.tol,
                 self.maxiter)
-        dev.check(dev.lib.fb_bicgstab(dev.h, 0, *args, 0, work.data_ptr(), ld, ist.data_ptr()), "bicgstab init")
+        dev.check(dev.lib.fb_bicgstab(dev.h, 0, *args, 0, work.data_ptr(), ld, ist.data_ptr(),
+                                      self._order()), "bicgstab init")
         done, chunk = 0, self.chunk
         while True:
             # poll after 8, 16, 32, then every 64 iterations (iterations past a
             # column's convergence are no-ops, so only the poll cadence changes)
-            dev.check(dev.lib.fb_bicgstab(dev.h, 1, *args, chunk, work.data_ptr(), ld, ist.data_ptr()),
-                      "bicgstab")
+            dev.check(dev.lib.fb_bicgstab(dev.h, 1, *args, chunk, work.data_ptr(), ld, ist.data_ptr(),
+                                          self._order()), "bicgstab")
             done += chunk
             chunk = min(2 * chunk, 64)
             active, fail = (int(v) for v in ist[2 * m:2 * m + 2].cpu())

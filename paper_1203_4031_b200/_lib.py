@@ -63,7 +63,7 @@ SIGNATURES = {
     "fb_permute_rows": (c_int, [P, c_int, c_int, P, P, P, c_int64, P, P, c_int64]),
     "fb_bicgstab_workspace_doubles": (c_int64, [c_int, c_int, c_int64]),
     "fb_bicgstab": (c_int, [P, c_int, c_int, c_int, P, P, P, P, P, P, P, P, c_int64, P, P, c_int64, c_double,
-                            c_int, c_int, P, c_int64, P]),
+                            c_int, c_int, P, c_int64, P, P]),
 }
 
 FB_OK, FB_ERR_ALLOC, FB_ERR_SINGULAR, FB_ERR_REDUCED, FB_ERR_ARG, FB_ERR_CUDA = 0, -1, -2, -3, -10, -11

@@ -527,7 +527,7 @@ int64_t fb_bicgstab_workspace_doubles(int n, int m, int64_t ld) {
 int fb_bicgstab(fb_ctx* c, int phase, int n, int m, const int64_t* indptr, const int64_t* indices, const double* sr,
                 const double* si, const double* dr, const double* di, const double* br, const double* bi,
                 int64_t ldb, double* xr, double* xi, int64_t ldx, double tol, int maxiter, int iters, double* work,
-                int64_t ld, int* istate) {
+                int64_t ld, int* istate, const int64_t* row_order) {
   CTX_GUARD(c);
   if (n <= 0 || m <= 0 || !indptr || !indices || !sr || !si || !dr || !di || !br || !xr || !xi || !work ||
       !istate || ldx != ld || ld < m || (phase != 0 && phase != 1) || iters < 0)
@@ -535,7 +535,8 @@ int fb_bicgstab(fb_ctx* c, int phase, int n, int m, const int64_t* indptr, const
   return set_err(c,
                  fb::bicgstab_launch(phase, n, m, reinterpret_cast<const long long*>(indptr),
                                      reinterpret_cast<const long long*>(indices), sr, si, dr, di, br, bi, ldb, xr,
-                                     xi, ldx, tol, maxiter, iters, work, ld, istate, c->stream),
+                                     xi, ldx, tol, maxiter, iters, work, ld, istate,
+                                     reinterpret_cast<const long long*>(row_order), c->stream),
                  "bicgstab");
 }
 

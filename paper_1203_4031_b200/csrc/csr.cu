@@ -376,7 +376,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
                             const double* s_re, const double* s_im, const double* d_re, const double* d_im,
                             const double* b_re, const double* b_im, long long ldb, double* x_re, double* x_im,
                             long long ldx, double tol, int maxiter, int iters, double* work, long long ld,
-                            int* istate, cudaStream_t st) {
+                            int* istate, const long long* order, cudaStream_t st) {
   // work layout: 8 planar vectors (r rhat p v s t phat shat), then state, then partials
   const long long plane = (long long)n * ld;
   BicgVecs V;
@@ -410,7 +410,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
     bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(1, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
     bicg_update_kernel<<<ugrid, ublk, 0, q>>>(1, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
     csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, q>>>(
-        n, m, indptr, indices, s_re, s_im, V.qr, V.qi, ld, V.vr, V.vi, ld, nullptr);
+        n, m, indptr, indices, s_re, s_im, V.qr, V.qi, ld, V.vr, V.vi, ld, order);
     bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.hr, V.hi, V.vr, V.vi, ld, status, part);
     bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(2, m, parts, part, nullptr, tol, maxiter, stt, status, itc);
     bicg_update_kernel<<<ugrid, ublk, 0, q>>>(2, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
@@ -419,7 +419,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
     bicg_update_kernel<<<ugrid, ublk, 0, q>>>(3, n, m, ld, V, b_re, b_im, ldb, d_re, d_im, stt, status);
     // columns that met the |s| test are final (status 2 -> 1)
     csr_spmm_kernel<true, true><<<dim3(ceil_div(n, kRowsPerCta), ceil_div(m, 32)), dim3(32, kRowsPerCta), 0, q>>>(
-        n, m, indptr, indices, s_re, s_im, V.wr, V.wi, ld, V.tr, V.ti, ld, nullptr);
+        n, m, indptr, indices, s_re, s_im, V.wr, V.wi, ld, V.tr, V.ti, ld, order);
     bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.tr, V.ti, V.tr, V.ti, ld, status, part);
     bicg_colred_kernel<<<rgrid, rblk, 0, q>>>(n, m, V.tr, V.ti, V.sr, V.si, ld, status, part2);
     bicg_scalar_kernel<<<sgrid, sblk, 0, q>>>(4, m, parts, part, part2, tol, maxiter, stt, status, itc);
@@ -447,7 +447,7 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
       int i[5];
     } key;
     memset(&key, 0, sizeof(key));
-    const void* ps[14] = {indptr, indices, s_re, s_im, d_re, d_im, b_re, b_im, x_re, x_im, work, istate, st, nullptr};
+    const void* ps[14] = {indptr, indices, s_re, s_im, d_re, d_im, b_re, b_im, x_re, x_im, work, istate, st, order};
     memcpy(key.p, ps, sizeof(ps));
     key.l[0] = ldb; key.l[1] = ldx; key.l[2] = ld;
     key.tol = tol;

@@ -16,6 +16,6 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
                             const double* s_re, const double* s_im, const double* d_re, const double* d_im,
                             const double* b_re, const double* b_im, long long ldb, double* x_re, double* x_im,
                             long long ldx, double tol, int maxiter, int iters, double* work, long long ld,
-                            int* istate, cudaStream_t st);
+                            int* istate, const long long* order, cudaStream_t st);
 
 }  // namespace fb

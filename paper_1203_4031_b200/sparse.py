@@ -252,7 +252,10 @@ class DeviceCsrOps:
         rows, cols = _union_pattern(a_full, b_full)
         if solver == "iterative":
             from ._bicgstab import DeviceBicgstab
-            self._it = DeviceBicgstab(dev, self.n, rows, cols, a_full, b_full, hermitian, iter_tol)
+            # RCM order only schedules the SpMM rows (L2 reuse of gathered rows)
+            self.row_order = dev.torch.from_numpy(bandwidth_reducing_order(self.n, rows, cols)).to(dev.tdev)
+            self._it = DeviceBicgstab(dev, self.n, rows, cols, a_full, b_full, hermitian, iter_tol,
+                                      row_order=self.row_order)
             self.mode = "iterative"
             return
         if solver != "direct":
