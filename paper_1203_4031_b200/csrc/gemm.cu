@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
 
   double accr[4][4][2], acci[4][4][2];
   // C += -A*B (alpha = -1, beta = 1, no split-K: the LU / solve updates): the
-  // accumulators start from C, so the epilogue is a plain store and the C
-  // loads overlap the pipeline prologue; the products are negated through
-  // the A fragments.
+  // products are negated through the A fragments and accumulated from zero;
+  // the epilogue adds them to C with ONE rounding per element (accumulating
+  // onto C directly would round every one of the k FMAs at |C|'s magnitude:
+  // sqrt(k) times the error, tools/dmma_rounding.py).
   const bool cinit = p.splits == 1 && p.alpha_re == -1.0 && p.alpha_im == 0.0 && p.beta_re == 1.0 &&
                      p.beta_im == 0.0;
 #pragma unroll
@@ -105,15 +106,6 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         accr[a][b][e] = acci[a][b][e] = 0.0;
-        if (cinit) {
-          const int i = m0 + wm + a * 8 + (lane >> 2);
-          const int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
-          if (i < p.m && j < p.n) {
-            const long long c = (long long)i * p.cs0 + (long long)j * p.cs1;
-            accr[a][b][e] = cre[c];
-            if (CPLX && cim) acci[a][b][e] = cim[c];
-          }
-        }
       }
   const double sgn = cinit ? -1.0 : 1.0;
   const double sa = p.a.conj ? -sgn : sgn;  // sign of the A imaginary fragments
@@ -182,8 +174,8 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
         double vr = accr[a][b][e], vi = CPLX ? acci[a][b][e] : 0.0;
         if (cinit) {
           const long long c = (long long)i * p.cs0 + (long long)j * p.cs1;
-          cre[c] = vr;
-          if (CPLX && cim) cim[c] = vi;
+          cre[c] += vr;
+          if (CPLX && cim) cim[c] += vi;
           continue;
         }
         if (p.splits > 1) {
@@ -212,8 +204,9 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmParams p) {
 // Same tiling and fragment order as gemm_kernel, but each thread streams
 // fixed 16-byte chunks (pointer increments instead of per-element 64-bit
 // index math, half the cp.async count), sign handling is compile-time (sign
-// flips are integer ops, off the FP64 pipe the DMMAs run on), and for
-// MODE 1 (C -= A*B) the accumulators start from C so the epilogue is a store.
+// flips are integer ops, off the FP64 pipe the DMMAs run on); MODE 1
+// (C -= A*B) negates the A fragments and adds the product to C once in the
+// epilogue (one rounding per element, as gemm_kernel).
 __device__ __forceinline__ double dneg(double v) {
   return __longlong_as_double(__double_as_longlong(v) ^ 0x8000000000000000ull);
 }
@@ -289,15 +282,6 @@ __global__ void __launch_bounds__(NT, 2) zgemm_fast_kernel(GemmParams p) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         accr[a][b][e] = acci[a][b][e] = 0.0;
-        if (MODE == 1) {
-          const int i = m0 + wm + a * 8 + (lane >> 2);
-          const int j = n0 + wn + b * 8 + 2 * (lane & 3) + e;
-          if (i < p.m && j < p.n) {
-            const long long c = (long long)i * p.cs0 + j;
-            accr[a][b][e] = cre[c];
-            acci[a][b][e] = cim[c];
-          }
-        }
       }
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -364,8 +348,8 @@ __global__ void __launch_bounds__(NT, 2) zgemm_fast_kernel(GemmParams p) {
         const long long c = (long long)i * p.cs0 + j;
         const double vr = accr[a][b][e], vi = acci[a][b][e];
         if (MODE == 1) {
-          cre[c] = vr;
-          cim[c] = vi;
+          cre[c] += vr;
+          cim[c] += vi;
           continue;
         }
         double outr = p.alpha_re * vr - p.alpha_im * vi;

@@ -7,8 +7,8 @@
 //   * right-looking blocked LU, outer block NB = 256 (trailing update is one
 //     DMMA ZGEMM with K = 256), inner sub-panels of PW = 32 columns factored by
 //     panel.cu (cluster/DSMEM exchange, one pivot per column);
-//   * the panel kernel also emits the 32x32 unit-lower / upper diagonal-block
-//     inverses (every triangular solve downstream is then a DMMA GEMM) and the
+//   * the panel kernel also emits the 32x32 unit-lower diagonal-block inverse
+//     (the in-factorization U12 = L11^-1 A12 is then a DMMA GEMM) and the
 //     panel's interchanges as a (dst, src) row list, applied to the other
 //     columns by one gather/scatter kernel;
 //   * piv[k] = row swapped with k at step k (0-based) as lu_factor; an exactly
@@ -208,9 +208,10 @@ size_t zgetrf_scratch_bytes(int n, int count) {
   return panel_scratch_bytes() * (size_t)count;
 }
 
-// Factor side storage, in doubles: [nblk][4][PW][PW] diagonal inverses (L re/im,
-// U re/im), then perm[n] ints, then nblk swap lists, then the per-block sweep
-// operators G / D (trsm.cu) of the fused solves.
+// Factor side storage, in doubles: [nblk][4][PW][PW] (the unit-lower diagonal
+// inverses L re/im used by the factorization; the second half is unused), then
+// perm[n] ints, then nblk swap lists, then the per-block substitution operators
+// (trsm.cu tdiag_kernel) of the fused solves.
 static size_t lists_doubles(int n) { return ((size_t)ceil_div(n, PW) * LIST + 1) / 2 + 2; }
 size_t dinv_doubles(int n) {
   size_t nblk = ceil_div(n, PW);
@@ -393,7 +394,7 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
       if ((e = block_factor(k + nb, st))) return e;
     }
   }
-  // composed permutation and sweep operators for the solves
+  // composed permutation and the sweeps' diagonal-block operators for the solves
   size_t psmem = sizeof(int) * (size_t)n;
   static bool pcfg = false;
   if (!pcfg) {
@@ -404,7 +405,6 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
   perm_kernel<<<B, 256, psmem, st>>>(n, lists, const_cast<int*>(factor_perm(f.dinv, n)), 2 * sd);
   count_launch();
   if ((e = cudaGetLastError())) return e;
-  if ((e = uinv_batched_launch(n, B, re, im, ld, slu, f.dinv, sd, st))) return e;
   return gmat_launch(n, B, re, im, ld, slu, f.dinv, sd, const_cast<double*>(factor_gmat(f.dinv, n)), st);
 }
 

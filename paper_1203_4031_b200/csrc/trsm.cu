@@ -7,9 +7,14 @@
 // whole sweep (a group of S CTAs per chunk), so at step t it stages the final
 // block X_{b(t)}[:, chunk] in shared memory once and then:
 //   * sub-CTA 0 of the group finalises the NEXT block ("look-ahead"):
-//       X_{b(t+1)} <- D_{b(t+1)} X_{b(t+1)} - G_{b(t+1)} X_{b(t)}
-//     with D the diagonal-block inverse and G = D * M(b(t+1), b(t)) precomputed
-//     per factor, so the critical path per step is ONE K=64 product;
+//       P = X_{b(t+1)} - M(b(t+1), b(t)) X_{b(t)}     (DMMA, K = 32)
+//       X_{b(t+1)} = T_{b(t+1)}^{-1} P                 (substitution)
+//     The 32x32 diagonal block T is applied by forward/backward SUBSTITUTION
+//     in shared memory (lanes = rows, 8 columns per warp, the pivot row
+//     broadcast by shuffles), not by an explicit inverse: a precomputed
+//     diagonal-block inverse costs a factor cond(T) in backward error (4x
+//     LAPACK's at N = 8192, profiles/r02_backward_error.txt), substitution
+//     is backward stable like zgetrs;
 //   * the group streams the rank-32 update of its share of the pending rows,
 //       X_i -= M(i, b(t)) X_{b(t)},   i in b(t+2) ...
 //     with the 32x32 M tiles double-buffered by 16-byte cp.async and the X_i
@@ -17,7 +22,7 @@
 //   * no grid barriers: per (row block, chunk) counters in global memory
 //     (release/acquire) let each CTA start a step as soon as the blocks it
 //     reads are final, so steps overlap (see sweep_body).
-// All products run on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA),
+// All block products run on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA),
 // complex as 4 real DMMAs on planar operands; each warp owns a 16x16 sub-tile
 // (8 independent accumulator chains).
 //
@@ -53,14 +58,14 @@ constexpr int PA = 36;                 // operator tile pitch (= 4 mod 16: confl
 constexpr int XP = CW + 4;             // X tile pitch (= 4 mod 16)
 constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 operator tile in shared memory
 constexpr int XTILE = 2 * BS * XP;     // doubles per planar 32 x CW X tile
-constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): G re/im, D re/im
+constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): T re/im [32][32], inv re/im [32] (padded)
 
 struct SweepArgs {
   int n, nrhs, nblk, variant;
   const double *lre, *lim;
   long long ld;
-  const double* dinv;  // [nblk][L re, L im, U re, U im][32][32]
-  const double* gmat;  // [4][nblk][G re, G im, D re, D im][32][32]
+  const double* dinv;  // factor side store (only its gmat part is read here)
+  const double* gmat;  // [4][nblk][T re, T im][32][32] + [inv re, inv im][32] (see tdiag_kernel)
   double *xre, *xim;
   long long ldx;
   long long slu, sdinv, sx;  // batch strides (item b: + b * stride)
@@ -129,6 +134,18 @@ __device__ __forceinline__ void acc_zero(Acc& c) {
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) c.r[mt][nt][e] = c.i[mt][nt][e] = 0.0;
+}
+
+__device__ __forceinline__ void acc_add(Acc& c, const Acc& d) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        c.r[mt][nt][e] += d.r[mt][nt][e];
+        c.i[mt][nt][e] += d.i[mt][nt][e];
+      }
 }
 
 // acc += (SR*Re A + i*SI*Im A) (32x32) * B (32 x CW tile of X); A is read as
@@ -239,8 +256,90 @@ __device__ __forceinline__ void acc_store(const SweepArgs& a, int b, int c0, con
   }
 }
 
-__device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b, int which) {
-  return a.gmat + ((size_t)a.variant * a.nblk + b) * GM_BLK + which * 2 * BS * BS;  // 0: G, 1: D
+__device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b) {
+  return a.gmat + ((size_t)a.variant * a.nblk + b) * GM_BLK;
+}
+
+// The diagonal-block operator of block b in processing coordinates (tdiag_kernel):
+// T[i][k] (step i, lane k) is the multiplier of the pivot row of step i applied
+// to processing row k (zero unless k > i), inv[k] the final scale of row k.
+// Copy it into a pitch-PA tile followed by inv (64 doubles).
+template <bool VEC>
+__device__ __forceinline__ void cp_tdiag(const double* src, double* s) {
+  cp_op<VEC>(src, s);
+  for (int e = threadIdx.x; e < 2 * BS; e += TT) cp_async8(s + 2 * BS * PA + e, src + 2 * BS * BS + e, true);
+}
+
+// X <- T^{-1} X on the planar shared tile X (pitch XP): forward substitution in
+// processing order (tile row = lane for the ascending sweeps, 31 - lane for the
+// descending ones).  Warp w owns columns [8w, 8w + 8); lane k holds row k of
+// its 8 columns; step i broadcasts row i (final) by shuffles and every lane
+// subtracts T[i][k] * x_i (T[i][k] = 0 for k <= i).  Backward stable as the
+// column-oriented substitution of zgetrs; the pivot scale of the non-unit
+// sweeps (U, U^H) is folded into T and applied to each row once at the end.
+template <bool FWD>
+__device__ __forceinline__ void tile_subst(double* X, const double* T, int c0, int nrhs) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int WCOL = CW / (TT / 32);
+  if (c0 + w * WCOL >= nrhs) return;  // warp-uniform: no live column
+  const int row = FWD ? lane : BS - 1 - lane;
+  double* Xr = X + row * XP + w * WCOL;
+  double* Xi = Xr + BS * XP;
+  double yr[WCOL], yi[WCOL];
+#pragma unroll
+  for (int c = 0; c < WCOL; ++c) {
+    yr[c] = Xr[c];
+    yi[c] = Xi[c];
+  }
+  const double* Ti = T + BS * PA;
+#pragma unroll
+  for (int i = 0; i < BS - 1; ++i) {
+    const double tr = T[i * PA + lane], ti = Ti[i * PA + lane];
+#pragma unroll
+    for (int c = 0; c < WCOL; ++c) {
+      const double br = __shfl_sync(0xffffffffu, yr[c], i), bi = __shfl_sync(0xffffffffu, yi[c], i);
+      yr[c] = fma(-tr, br, fma(ti, bi, yr[c]));
+      yi[c] = fma(-tr, bi, fma(-ti, br, yi[c]));
+    }
+  }
+  const double sr = T[2 * BS * PA + lane], si = T[2 * BS * PA + BS + lane];
+#pragma unroll
+  for (int c = 0; c < WCOL; ++c) {
+    Xr[c] = yr[c] * sr - yi[c] * si;
+    Xi[c] = yr[c] * si + yi[c] * sr;
+  }
+}
+
+// P = X_shared + acc (acc = -M X_b as fragments) written back into the shared tile
+__device__ __forceinline__ void acc_add_to_tile(const Acc& c, double* X) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wr = w / WC, wc = w % WC;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int r = wr * 16 + mt * 8 + (lane >> 2);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int col = wc * 16 + nt * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        X[r * XP + col + e] += c.r[mt][nt][e];
+        X[BS * XP + r * XP + col + e] += c.i[mt][nt][e];
+      }
+    }
+  }
+}
+
+// shared X tile -> global rows of block b, chunk columns [c0, c0 + CW) (L2 stores)
+__device__ __forceinline__ void tile_store(const SweepArgs& a, int b, int c0, const double* X) {
+  for (int e = threadIdx.x; e < BS * CW; e += TT) {
+    const int r = e / CW, c = e % CW;
+    const int gr = b * BS + r, gc = c0 + c;
+    if (gr < a.n && gc < a.nrhs) {
+      const long long o = (long long)gr * a.ldx + gc;
+      __stcg(a.xre + o, X[r * XP + c]);
+      __stcg(a.xim + o, X[BS * XP + r * XP + c]);
+    }
+  }
 }
 
 // X tile rows of block b, chunk columns [c0, c0 + 32).  X is written by other
@@ -318,19 +417,22 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
   auto fin = [&](int blk, int c) { return a.fin + (size_t)blk * C + c; };
   const int c_first = G >= C ? g % C : g, c_step = G >= C ? C : G;
 
-  // prologue: the first block of the sweep is final after D
+  const bool fwd = a.variant == 0 || a.variant == 2;
+  // prologue: the first block of the sweep is final after its substitution
   if (sub == 0) {
     const int b0 = blk_at(a, 0);
     for (int c = c_first; c < C; c += c_step) {
-      cp_op<VEC>(op_ptr(a, b0, 1), T0);
+      cp_tdiag<VEC>(op_ptr(a, b0), T1);
       cp_x<VEC>(a, b0, c * CW, Xt);
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
-      Acc acc;
-      acc_zero(acc);
-      tile_mma<false, 1, 1>(acc, T0, Xt, c * CW + wcol < a.nrhs);
-      acc_store<VEC>(a, b0, c * CW, acc);
+      if (fwd)
+        tile_subst<true>(Xt, T1, c * CW, a.nrhs);
+      else
+        tile_subst<false>(Xt, T1, c * CW, a.nrhs);
+      __syncthreads();
+      tile_store(a, b0, c * CW, Xt);
       __syncthreads();
       publish(fin(b0, c), 1);
     }
@@ -360,16 +462,22 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
       if (do_ahead) {
         const int bn = blk_at(a, t + 1);
         cp_x<VEC>(a, bn, c0, Xn);
-        cp_op<VEC>(op_ptr(a, bn, 1), T0);
-        cp_op<VEC>(op_ptr(a, bn, 0), T1);
+        cp_m<VEC>(a, bn, bt, T0);
+        cp_tdiag<VEC>(op_ptr(a, bn), T1);
         cp_async_commit();
         cp_async_wait<0>();
         __syncthreads();
         Acc acc;
         acc_zero(acc);
-        tile_mma<false, 1, 1>(acc, T0, Xn, live);
-        tile_mma<false, -1, -1>(acc, T1, Xt, live);
-        acc_store<VEC>(a, bn, c0, acc);
+        tile_mma<TR, -1, (TR ? 1 : -1)>(acc, T0, Xt, live);
+        acc_add_to_tile(acc, Xn);
+        __syncthreads();
+        if (fwd)
+          tile_subst<true>(Xn, T1, c0, a.nrhs);
+        else
+          tile_subst<false>(Xn, T1, c0, a.nrhs);
+        __syncthreads();
+        tile_store(a, bn, c0, Xn);
         __syncthreads();
         publish(fin(bn, c), 1);
       }
@@ -377,7 +485,11 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
         // the rows' previous-step updates
         for (int q = qb + threadIdx.x; q < qe; q += TT) wait_ge(upd(blk_at(a, t + 2 + q), c), t);
         __syncthreads();
-        Acc cur, nxt;
+        // the product -M X_b accumulates from zero and is added to the
+        // prefetched X_i once (one rounding per element and step, as zgetrs'
+        // GEMM updates; accumulating onto X_i would round all 32 FMAs at
+        // |X_i|'s magnitude, tools/dmma_rounding.py)
+        Acc cur, nxt, prod;
         cp_m<VEC>(a, blk_at(a, t + 2 + qb), bt, T0);
         cp_async_commit();
         acc_load<VEC>(a, blk_at(a, t + 2 + qb), c0, nxt);
@@ -395,7 +507,9 @@ __device__ void sweep_body(SweepArgs& a, double* s) {
             cp_async_wait<0>();
           }
           __syncthreads();
-          tile_mma<TR, -1, (TR ? 1 : -1)>(cur, Tq, Xt, live);
+          acc_zero(prod);
+          tile_mma<TR, -1, (TR ? 1 : -1)>(prod, Tq, Xt, live);
+          acc_add(cur, prod);
           acc_store<VEC>(a, rb, c0, cur);
           __syncthreads();
         }
@@ -419,66 +533,83 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
   sweep_body<TR, VEC>(a, s);
 }
 
-// Per (block, variant): D_v (the variant's diagonal inverse, conj-transposed for
-// the adjoint sweeps) and G_v = D_v * M(b, prev(b)).
-__global__ void __launch_bounds__(GT) gmat_kernel(SweepArgs a0) {
-  __shared__ double Dr[BS * 33], Di[BS * 33], Mr[BS * 33], Mi[BS * 33];
+// Per (block, variant): the diagonal block of the factor as the substitution
+// operator of tile_subst, in processing coordinates p (tile row r = p for the
+// ascending sweeps 0 (L) and 2 (U^H), r = 31 - p for the descending sweeps
+// 1 (U) and 3 (L^H)):
+//   T[i][k] = op(i -> k) / d_i  for k > i (0 otherwise),   inv[k] = 1 / d_k,
+// where op(i -> k) is the entry of the triangular block that multiplies row i
+// when eliminating row k and d the diagonal (1 for the unit sweeps 0 and 3).
+//   variant 0: op = L[rk][ri]          variant 1: op = U[rk][ri], d = U[r][r]
+//   variant 2: op = conj(U[ri][rk]),   variant 3: op = conj(L[ri][rk])
+//              d = conj(U[r][r])
+// Rows past n get inv = 0 and no coupling.
+__global__ void __launch_bounds__(GT) tdiag_kernel(SweepArgs a0) {
+  __shared__ double Dr[BS * 33], Di[BS * 33], Sr[BS], Si[BS];
   SweepArgs a = a0;
   offset_item(a, blockIdx.z);
   const int b = blockIdx.x, variant = blockIdx.y;
-  const bool upper = variant == 1 || variant == 2;
+  const bool unit = variant == 0 || variant == 3;
+  const bool fwd = variant == 0 || variant == 2;
   const bool trans = variant >= 2;
-  const double* dr = a.dinv + (size_t)b * 4 * BS * BS + (upper ? 2 : 0) * BS * BS;
-  const double* di = dr + BS * BS;
+  const int i0 = b * BS;
   double* out = const_cast<double*>(a.gmat) + ((size_t)variant * a.nblk + b) * GM_BLK;
   for (int e = threadIdx.x; e < BS * BS; e += GT) {
-    const int r = e / BS, k = e % BS;
-    const double vr = trans ? dr[k * BS + r] : dr[e];
-    const double vi = trans ? -di[k * BS + r] : di[e];
-    Dr[r * 33 + k] = vr;
-    Di[r * 33 + k] = vi;
-    out[2 * BS * BS + e] = vr;  // D
-    out[3 * BS * BS + e] = vi;
+    const int r = e / BS, c = e % BS;
+    const bool ok = i0 + r < a.n && i0 + c < a.n;
+    Dr[r * 33 + c] = ok ? a.lre[(long long)(i0 + r) * a.ld + i0 + c] : 0.0;
+    Di[r * 33 + c] = ok ? a.lim[(long long)(i0 + r) * a.ld + i0 + c] : 0.0;
   }
-  const bool fwd = variant == 0 || variant == 2;
-  const int prev = fwd ? b - 1 : b + 1;
-  if (prev < 0 || prev >= a.nblk) {
-    for (int e = threadIdx.x; e < BS * BS; e += GT) out[e] = out[BS * BS + e] = 0.0;
-    return;
-  }
-  const int i0 = b * BS, p0 = prev * BS;
-  for (int e = threadIdx.x; e < BS * BS; e += GT) {
-    const int r = e / BS, k = e % BS;
-    const int gr = i0 + r, gk = p0 + k;
-    double vr = 0.0, vi = 0.0;
-    if (gr < a.n && gk < a.n) {
-      if (!trans) {
-        vr = a.lre[(long long)gr * a.ld + gk];
-        vi = a.lim[(long long)gr * a.ld + gk];
+  __syncthreads();
+  if (threadIdx.x < BS) {
+    const int r = threadIdx.x;  // tile row
+    double sr = 0.0, si = 0.0;
+    if (i0 + r < a.n) {
+      if (unit) {
+        sr = 1.0;
       } else {
-        vr = a.lre[(long long)gk * a.ld + gr];
-        vi = -a.lim[(long long)gk * a.ld + gr];
+        const double dr = Dr[r * 33 + r], di = trans ? -Di[r * 33 + r] : Di[r * 33 + r];
+        const double den = dr * dr + di * di;
+        sr = dr / den;
+        si = -di / den;
       }
     }
-    Mr[r * 33 + k] = vr;
-    Mi[r * 33 + k] = vi;
+    Sr[r] = sr;
+    Si[r] = si;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < BS * BS; e += GT) {
-    const int r = e / BS, c = e % BS;
-    double sr = 0.0, si = 0.0;
-    for (int k = 0; k < BS; ++k) {
-      const double xr = Dr[r * 33 + k], xi = Di[r * 33 + k];
-      const double yr = Mr[k * 33 + c], yi = Mi[k * 33 + c];
-      sr += xr * yr - xi * yi;
-      si += xr * yi + xi * yr;
+    const int i = e / BS, k = e % BS;
+    const int ri = fwd ? i : BS - 1 - i, rk = fwd ? k : BS - 1 - k;
+    double vr = 0.0, vi = 0.0;
+    if (k > i && i0 + ri < a.n && i0 + rk < a.n) {
+      double orr, oi;
+      if (!trans) {
+        orr = Dr[rk * 33 + ri];
+        oi = Di[rk * 33 + ri];
+      } else {
+        orr = Dr[ri * 33 + rk];
+        oi = -Di[ri * 33 + rk];
+      }
+      if (unit) {
+        vr = orr;
+        vi = oi;
+      } else {
+        vr = orr * Sr[ri] - oi * Si[ri];
+        vi = orr * Si[ri] + oi * Sr[ri];
+      }
     }
-    out[e] = sr;
-    out[BS * BS + e] = si;
+    out[e] = vr;
+    out[BS * BS + e] = vi;
+  }
+  if (threadIdx.x < BS) {
+    const int k = threadIdx.x, rk = fwd ? k : BS - 1 - k;
+    out[2 * BS * BS + k] = Sr[rk];
+    out[2 * BS * BS + BS + k] = Si[rk];
   }
 }
 
-size_t sweep_smem() { return sizeof(double) * (2 * XTILE + 2 * TILE); }
+size_t sweep_smem() { return sizeof(double) * (2 * XTILE + 2 * TILE + 2 * BS); }
 
 }  // namespace
 
@@ -489,7 +620,7 @@ cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, 
   SweepArgs a{};
   a.n = n; a.nblk = ceil_div(n, BS); a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.slu = slu; a.sdinv = sdinv; a.sx = 0;
-  gmat_kernel<<<dim3(a.nblk, 4, count), GT, 0, st>>>(a);
+  tdiag_kernel<<<dim3(a.nblk, 4, count), GT, 0, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }

@@ -463,6 +463,33 @@ def make_sparse():
     _save("sparse.npz", **out)
 
 
+def make_c3_trajectories(ks):
+    """Config 3 under 1-ulp perturbations A*(1 + k*2^-52): the reference
+    kernel's trajectory (final M0 after the loop-0 shrink, loop count, info,
+    per-loop history) for each k, so the GPU run can be compared with the
+    reference trajectory that has the same post-shrink M0 (the shrink index is
+    decided at rounding level, kernel.py:385-400;
+    profiles/r01_c3_ref_sensitivity.txt)."""
+    from paper_1203_4031_b200 import workloads as W
+    w = W.c3_heev()
+    a0 = w.a.copy()
+    out = {}
+    path = os.path.join(HERE, "c3_trajectories.npz")
+    if os.path.exists(path):
+        out = dict(np.load(path))
+    for k in ks:
+        w.a = a0 * (1.0 + k * 2.0 ** -52)
+        r, hist, wall, _ = run_kernel_lapack(w)
+        m = int(r.m)
+        out[f"k{k}_scal"] = np.array([k, r.m0, r.loop, r.info, m], dtype=np.int64)
+        out[f"k{k}_e"] = r.e[:m]
+        out[f"k{k}_res"] = r.res[:m]
+        out[f"k{k}_history"] = hist
+        print(f"c3 k={k}: m0={r.m0} loop={r.loop} info={r.info} m={m} "
+              f"maxres={np.max(r.res[:m]):.2e} wall={wall:.0f}s", flush=True)
+        _save("c3_trajectories.npz", **out)
+
+
 if __name__ == "__main__":
     from paper_1203_4031_b200 import workloads as W
     what = sys.argv[1:] or ["unit", "small"]
@@ -472,6 +499,8 @@ if __name__ == "__main__":
         make_small()
     if "sparse" in what:
         make_sparse()
+    if "c3traj" in what:
+        make_c3_trajectories([int(v) for v in os.environ.get("C3_KS", "0 1 2 3 4 5").split()])
     if "scaled" in what:
         for tag in ("c1s", "c2s", "c3s", "c5s", "c4s"):
             make_config(f"scaled_{tag}", W.scaled(tag))
