@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes
 
+import threading
+
 import numpy as np
 
 from . import _lib
@@ -335,6 +337,7 @@ class B200BandOps:
 
     def __init__(self, fa, fb, kl, hermitian=None, device=None):
         fa = np.asarray(fa)
+        self._lock = threading.RLock()
         self.hermitian = np.iscomplexobj(fa) if hermitian is None else hermitian
         self.dev = get_device(device)
         FA = self.dev.upload(fa, cplx=self.hermitian)
@@ -343,12 +346,17 @@ class B200BandOps:
         self.n = fa.shape[1]
 
     def factorize(self, z):
-        return self._ops.factorize(z)
+        # feastlib's run_rci calls this from a ThreadPoolExecutor when
+        # parallel_contour > 1 (_driver.py:51-54): one GPU context, one stream,
+        # shared factor cache -> calls are serialised
+        with self._lock:
+            return self._ops.factorize(z)
 
     def _solve(self, f, rhs, adjoint):
         W = self.dev.upload(np.asarray(rhs, dtype=np.complex128), cplx=True)
-        self._ops._solve(f, W, adjoint)
-        return self.dev.download(W)
+        with self._lock:
+            self._ops._solve(f, W, adjoint)
+            return self.dev.download(W)
 
     def solve(self, f, rhs):
         return self._solve(f, rhs, False)
@@ -359,8 +367,9 @@ class B200BandOps:
     def _mult(self, fn, x):
         X = self.dev.upload(np.asarray(x), cplx=self.hermitian)
         Y = self.dev.empty(self.n, X.cols, self.hermitian)
-        fn(X, Y)
-        return self.dev.download(Y)
+        with self._lock:
+            fn(X, Y)
+            return self.dev.download(Y)
 
     def multiply_a(self, x):
         return self._mult(self._ops.multiply_a, x)

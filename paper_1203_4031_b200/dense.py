@@ -10,6 +10,8 @@ protocol, for plugging into feastlib's own ``run_rci``.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 
 from ._driver import SolverOptions, run_rci
@@ -302,6 +304,7 @@ class B200DenseOps:
 
     def __init__(self, a, b=None, hermitian=None, device=None):
         a = np.asarray(a)
+        self._lock = threading.RLock()
         self.hermitian = np.iscomplexobj(a) if hermitian is None else hermitian
         self.dev = get_device(device)
         A = self.dev.upload(a, cplx=self.hermitian)
@@ -310,13 +313,18 @@ class B200DenseOps:
         self.n = a.shape[0]
 
     def factorize(self, z):
-        return self._ops.factorize(z)
+        # feastlib's run_rci calls this from a ThreadPoolExecutor when
+        # parallel_contour > 1 (_driver.py:51-54): one GPU context, one stream,
+        # shared factor cache -> calls are serialised
+        with self._lock:
+            return self._ops.factorize(z)
 
     def _solve(self, f, rhs, adjoint):
         rhs = np.asarray(rhs, dtype=np.complex128)
         W = self.dev.upload(rhs, cplx=True)
-        self._ops._solve(f, W, adjoint)
-        return self.dev.download(W)
+        with self._lock:
+            self._ops._solve(f, W, adjoint)
+            return self.dev.download(W)
 
     def solve(self, f, rhs):
         return self._solve(f, rhs, False)
@@ -328,8 +336,9 @@ class B200DenseOps:
         x = np.asarray(x)
         X = self.dev.upload(x, cplx=self.hermitian)
         Y = self.dev.empty(self.n, X.cols, self.hermitian)
-        fn(X, Y)
-        return self.dev.download(Y)
+        with self._lock:
+            fn(X, Y)
+            return self.dev.download(Y)
 
     def multiply_a(self, x):
         return self._mult(self._ops.multiply_a, x)

@@ -296,9 +296,11 @@ class _RciKernel:
         x = self.x_host()
         if self.host_mirror and self.x is not None:
             self.x[...] = x
-        return EigenResult(e=self.e.astype(self._out_real), x=x, m=self.m,
-                           res=self.res.astype(self._out_real), epsout=float(self.epsout),
-                           loop=self.loop, info=self.info, m0=self.m0)
+        r = EigenResult(e=self.e.astype(self._out_real), x=x, m=self.m,
+                        res=self.res.astype(self._out_real), epsout=float(self.epsout),
+                        loop=self.loop, info=self.info, m0=self.m0)
+        r.history = np.array(getattr(self, "history", []), dtype=np.float64).reshape(-1, 5)
+        return r
 
     # -- engine internals ----------------------------------------------------
     def _tolerance(self):
@@ -371,6 +373,7 @@ class _RciKernel:
 
         trace_prev = None
         self.loop = 0
+        self.history = []     # the fpm(1) report lines: (loop, #eig, trace, error-trace, max-residual)
         while True:
             m0 = self.m0
             Q = self.Q.cols_view(0, m0)
@@ -474,6 +477,7 @@ class _RciKernel:
             trace_cur = float(lam[inside].sum())
             self.epsout = 1.0 if trace_prev is None else trace_error(trace_cur, trace_prev, emin, emax)
             max_res = float(res[inside].max()) if m else 0.0
+            self.history.append((self.loop, m, trace_cur, float(self.epsout), max_res))
             if verbose:
                 print(f"{self.loop:<8d}{m:<7d}{trace_cur:.15e}  "
                       f"{self.epsout:.15e}  {max_res:.15e}")

@@ -105,8 +105,10 @@ def c4_sbgv(n=1_000_000, kd=16, m0=96, seed=4, interval=None, expect_m=None):
                     interval[1], ab, bb, kla=kd, klb=1, uplo="L", expect_m=expect_m)
 
 
-def c5_hegv(n=32768, m0=512, seed=5, interval=(-0.0174, 0.0174), expect_m=None, ne=16):
+def c5_hegv(n=32768, m0=512, seed=5, interval=None, expect_m=None, ne=16):
     """zfeast_hegv: A as config 3; B = I + 0.05 H H^H / N, H complex Gaussian."""
+    if interval is None:
+        interval, expect_m = C5_INTERVAL, C5_COUNT
     rng = np.random.default_rng(seed)
     g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
     a = (g + g.conj().T) / (2.0 * np.sqrt(n))
@@ -115,6 +117,15 @@ def c5_hegv(n=32768, m0=512, seed=5, interval=(-0.0174, 0.0174), expect_m=None, 
     b = 0.5 * (b + b.conj().T)
     return Workload("c5_zfeast_hegv", "dense", True, n, m0, ne, interval[0],
                     interval[1], a, b, expect_m=expect_m)
+
+
+def c5m_hegv(n=12288, m0=240, seed=5, interval=None, expect_m=None):
+    """Mid-size config-5 construction (same seeded draws, N = 12288): the
+    largest zfeast_hegv pencil the reference kernel + LAPACK can factor in this
+    container's RAM (16 factors x 2.4 GB); golden tests/golden/mid_c5m.npz."""
+    if interval is None:
+        interval, expect_m = C5M_INTERVAL, C5M_COUNT
+    return c5_hegv(n=n, m0=m0, seed=seed, interval=interval, expect_m=expect_m)
 
 
 # Frozen C4 intervals: mid-gap endpoints placed by Sylvester inertia of the
@@ -195,7 +206,15 @@ def c5_device_planar(dev, n=32768, seed=5, chunk_rows=2048):
     return A, B
 
 
-# C5 interval: mid-gap endpoints around the ~400 eigenvalues nearest 0, placed
-# once from an independent dense eigensolve of the pencil (tools/c5_full.py).
-C5_INTERVAL = None
-C5_COUNT = None
+# C5 interval: mid-gap endpoints around the ~400 eigenvalues nearest 0.  The
+# neighbouring eigenvalues come from a first FEAST run on the semicircle
+# estimate (-0.0174, 0.0174) (profiles/r01_c5_full_report_run4.json: Ritz
+# values -0.017556972 | -0.017439996 and 0.017348207 | 0.017460059 with
+# residuals <= 1.5e-9, gaps 1.2e-4 and 1.1e-4); the count inside is confirmed
+# by the Sylvester inertia of A - sigma B at both ends (tools/c5_full.py).
+C5_INTERVAL = (-0.0174985, 0.0174041)
+C5_COUNT = 401
+# mid-gap endpoints around the 150 eigenvalues nearest 0 of the N = 12288
+# pencil (scipy eigh subset, tests/golden/make_golden.py c5m)
+C5M_INTERVAL = None
+C5M_COUNT = None

@@ -504,6 +504,23 @@ if __name__ == "__main__":
     if "scaled" in what:
         for tag in ("c1s", "c2s", "c3s", "c5s", "c4s"):
             make_config(f"scaled_{tag}", W.scaled(tag))
+    if "c5m" in what:
+        # mid-size config-5 pencil: place the interval mid-gap around the 150
+        # eigenvalues nearest 0 (independent LAPACK zhegvx), then the reference
+        # kernel + LAPACK caller
+        w = W.c5m_hegv(interval=(-1.0, 1.0))
+        if W.C5M_INTERVAL is None:
+            t0 = time.time()
+            ev = sla.eigh(w.a, w.b, eigvals_only=True, subset_by_value=(-0.03, 0.03), driver="gvx")
+            i0 = int(np.searchsorted(ev, 0.0))
+            lo, hi = i0 - 75, i0 + 75
+            w.emin, w.emax = 0.5 * (ev[lo - 1] + ev[lo]), 0.5 * (ev[hi - 1] + ev[hi])
+            w.expect_m = 150
+            print(f"C5M_INTERVAL = ({w.emin!r}, {w.emax!r})  count 150  gaps "
+                  f"{ev[lo] - ev[lo - 1]:.2e} {ev[hi] - ev[hi - 1]:.2e}  ({time.time() - t0:.0f}s)", flush=True)
+        else:
+            (w.emin, w.emax), w.expect_m = W.C5M_INTERVAL, W.C5M_COUNT
+        make_config("mid_c5m", w)
     for tag, fn in (("c1", W.c1_syev), ("c2", W.c2_sygv), ("c3", W.c3_heev), ("c4", W.c4_sbgv)):
         if tag in what:
             make_config(f"full_{tag}", fn())

@@ -1,0 +1,139 @@
+"""Drop-in proof through the REFERENCE's own pump: feastlib's unmodified
+``run_rci`` (_driver.py:42-92) and RCI kernels (kernel.py:183-531), loaded from
+oracle/_ref (oracle/ref.py; test infrastructure), with this repository's
+``B200DenseOps`` / ``B200BandOps`` plugged in at the swap point
+(dense.py:156, banded.py:235) -- the one-line change INTEGRATION.md shows.
+Results are held to the goldens the reference produced with its own ops
+(tests/golden/small.npz, scaled_*.npz)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fl():
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref/feastlib not present (python __graft_entry__.py build where /root/reference exists)")
+    return ref.load_feastlib()
+
+
+def _reference_driver(fl, kind, case, ops_factory, options=None):
+    """The body of feastlib's _dense_driver / _banded_driver with the ops swapped."""
+    from feastlib import banded as fband
+    from feastlib import dense as fdense
+    from feastlib._driver import run_rci
+    herm = kind in ("he", "hb")
+    cls = fl.HermitianRci if herm else fl.SymmetricRci
+    extra = {"adjoint_capable": True} if herm else {}
+    fpm = fl.feastinit()
+    for i, v in enumerate(case["fpm"], start=1):
+        if fpm.slot(i) != int(v):
+            fpm.set_slot(i, int(v))
+    a = case["a"]
+    n = a.shape[0] if kind in ("sy", "he") else a.shape[1]
+    k = cls(n, int(case["m0"]), case["emin"], case["emax"], fpm, **extra)
+    uplo = case["uplo"]
+    if kind in ("sy", "he"):
+        a_full = fdense.expand_uplo(a, uplo, herm)
+        b_full = None if case.get("b") is None else fdense.expand_uplo(case["b"], uplo, herm)
+        ops = ops_factory(a_full, b_full, herm)
+    else:
+        kla, klb = int(case["kla"]), int(case["klb"])
+        kl = max(kla, klb if case.get("b") is not None else 0)
+        fa = fband._pad_band(fband.expand_band(a, kla, uplo, herm), kla, kl)
+        fbm = None
+        if case.get("b") is not None:
+            fbm = fband._pad_band(fband.expand_band(case["b"], klb, uplo, herm), klb, kl)
+        ops = ops_factory(fa, fbm, kl, herm)
+    return run_rci(k, ops, options)
+
+
+def _small_case(g, name):
+    cfg = g[f"{name}__cfg"]
+    c = {"a": g[f"{name}__a"], "b": g[f"{name}__b"] if f"{name}__b" in g.files else None,
+         "emin": float(cfg[0]), "emax": float(cfg[1]), "m0": int(cfg[2]), "kla": int(cfg[3]),
+         "klb": int(cfg[4]), "uplo": str(g[f"{name}__uplo"]), "fpm": g[f"{name}__fpm"]}
+    return str(g[f"{name}__kind"]), c
+
+
+def _check(r, g, name):
+    m, loop, info, _ = (int(v) for v in g[f"{name}__scal"])
+    cfg = g[f"{name}__cfg"]
+    s = max(abs(cfg[0]), abs(cfg[1]))
+    assert r.info == info, (name, r.info, info)
+    assert r.m == m, (name, r.m, m)
+    assert abs(r.loop - loop) <= 1, (name, r.loop, loop)
+    if info in (0, 2, 3) and m:
+        assert np.abs(r.e[:m] - g[f"{name}__e"][:m]).max() <= 1e-10 * s, name
+        if info == 0:
+            assert np.max(r.res[:m]) <= 1e-10
+
+
+def test_feastlib_run_rci_with_b200_ops_small_goldens(fl, small_golden):
+    from paper_1203_4031_b200.banded import B200BandOps
+    from paper_1203_4031_b200.dense import B200DenseOps
+    g = small_golden
+    ran = 0
+    for name in [str(v) for v in g["names"]]:
+        kind, case = _small_case(g, name)
+        if int(g[f"{name}__scal"][2]) < 0 or case["a"].dtype in (np.float32, np.complex64):
+            continue
+        if kind in ("sy", "he"):
+            r = _reference_driver(fl, kind, case, lambda a, b, h: B200DenseOps(a, b, hermitian=h))
+        else:
+            r = _reference_driver(fl, kind, case, lambda fa, fb_, kl, h: B200BandOps(fa, fb_, kl, hermitian=h))
+        assert isinstance(r, fl.EigenResult)
+        _check(r, g, name)
+        ran += 1
+    assert ran >= 15
+
+
+def test_feastlib_parallel_contour_threads(fl, small_golden):
+    """feastlib's ThreadPoolExecutor calls ops.factorize concurrently
+    (_driver.py:51-54); the adapter serialises them and results are unchanged."""
+    from paper_1203_4031_b200.dense import B200DenseOps
+    g = small_golden
+    name = next(n for n in (str(v) for v in g["names"]) if str(g[f"{n}__kind"]) == "sy"
+                and int(g[f"{n}__scal"][2]) == 0 and g[f"{n}__a"].dtype == np.float64)
+    kind, case = _small_case(g, name)
+    from feastlib._driver import SolverOptions
+    serial = _reference_driver(fl, kind, case, lambda a, b, h: B200DenseOps(a, b, hermitian=h))
+    par = _reference_driver(fl, kind, case, lambda a, b, h: B200DenseOps(a, b, hermitian=h),
+                            SolverOptions(parallel_contour=8))
+    assert par.info == serial.info and par.m == serial.m and par.loop == serial.loop
+    assert par.e.tobytes() == serial.e.tobytes()
+    _check(par, g, name)
+
+
+@pytest.mark.parametrize("tag", ["c2s", "c3s", "c5s", "c4s"])
+def test_feastlib_run_rci_with_b200_ops_scaled_configs(fl, tag):
+    """Scaled BASELINE constructions: reference kernel + reference pump + B200 ops
+    vs the reference kernel + LAPACK golden."""
+    from paper_1203_4031_b200 import workloads as W
+    from paper_1203_4031_b200.banded import B200BandOps
+    from paper_1203_4031_b200.dense import B200DenseOps
+    from oracle import ref
+    g = np.load(os.path.join(GOLDEN, f"scaled_{tag}.npz"))
+    w = W.scaled(tag)
+    if w.kind == "dense":
+        ops = B200DenseOps(w.a, w.b, hermitian=w.hermitian)
+    else:
+        from feastlib import banded as fband
+        kl = max(w.kla, w.klb)
+        fa = fband._pad_band(fband.expand_band(w.a, w.kla, w.uplo, False), w.kla, kl)
+        fbm = fband._pad_band(fband.expand_band(w.b, w.klb, w.uplo, False), w.klb, kl)
+        ops = B200BandOps(fa, fbm, kl, hermitian=False)
+    r = ref.reference_solve(w, ops=ops)
+    m, loop, info, _ = (int(v) for v in g["scal"])
+    s = max(abs(w.emin), abs(w.emax))
+    assert (r.info, r.m) == (info, m)
+    assert abs(r.loop - loop) <= 1
+    assert np.abs(r.e[:m] - g["e"][:m]).max() <= 1e-10 * s
+    assert np.max(r.res[:m]) <= 1e-10

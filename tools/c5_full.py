@@ -80,8 +80,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--m0", type=int, default=512)
-    ap.add_argument("--emin", type=float, default=-0.0174)
-    ap.add_argument("--emax", type=float, default=0.0174)
+    ap.add_argument("--emin", type=float, default=W.C5_INTERVAL[0])
+    ap.add_argument("--emax", type=float, default=W.C5_INTERVAL[1])
     ap.add_argument("--no-inertia", action="store_true")
     ap.add_argument("--loops", type=int, default=None, help="cap fpm(4) (refinement passes)")
     args = ap.parse_args()
@@ -114,6 +114,7 @@ def main():
     rep = {"info": int(r.info), "m": int(r.m), "m0_final": int(r.m0), "loop": int(r.loop), "seconds": dt,
            "it_per_s": (r.loop + 1) / dt, "factorizations": int(getattr(r, "factorizations", -1)),
            "max_res": float(np.max(r.res[:r.m])) if r.m else None, "epsout": float(r.epsout)}
+    rep["history"] = [[float(v) for v in row] for row in getattr(r, "history", [])]
     rep["e_all"] = [float(v) for v in r.e[:r.m0]]
     rep["res_all"] = [float(v) for v in r.res[:r.m0]]
     if "inertia_count" in report:
