@@ -221,6 +221,24 @@ int fb_band_solve_batched_rhs(fb_ctx* ctx, int count, int n, int kl, int nrhs,
                               const double* y_re, const double* y_im, int64_t ldy, int64_t y_stride,
                               double* x_re, double* x_im, int64_t ldx, int64_t x_stride);
 
+/* One whole contour pass of the banded drivers (kernel.py:350-364 with
+ * _BandedOps.solve, banded.py:166-170, and accumulate_subspace,
+ * kernel.py:108-124): every resident shift b is solved against the pass's
+ * right-hand side Y (shared by all shifts; y_im NULL: real Y) and the nterms
+ * quadrature terms -- term t uses the solve of shift item[t] with
+ * (variant[t], w[t], theta[t]) as fb_accumulate -- are folded into Q in the
+ * given order.  The spike correction of the partitioned solve is applied
+ * inside the accumulation kernel (FP64 tensor pipe), so the corrected
+ * solutions are never written: X is work space of count blocks and ends
+ * holding the uncorrected partition solves. */
+int fb_band_solve_accumulate(fb_ctx* ctx, int count, int n, int kl, int nrhs,
+                             const double* fact_re, const double* fact_im, int64_t fact_stride,
+                             const int* ipiv, int64_t ipiv_stride, const double* aux, int64_t aux_stride,
+                             const double* y_re, const double* y_im, int64_t ldy,
+                             double* x_re, double* x_im, int64_t ldx, int64_t x_stride,
+                             int nterms, const int* item, const int* variant, const double* w, double r,
+                             const double* theta, double* q_re, double* q_im, int64_t ldq);
+
 /* ---- CSR backend (feast_scsr / feast_hcsr, sparse.py:430-517) ---------- */
 /* Y = M X for a full-pattern CSR matrix M (0-based int64 indptr[n+1] /
  * indices[nnz], values planar: val_im NULL for real M) and a row-major

@@ -57,6 +57,9 @@ SIGNATURES = {
                                        P, c_int64, P, c_int64, P]),
     "fb_band_solve_batched_rhs": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
                                           P, P, c_int64, c_int64, P, P, c_int64, c_int64]),
+    "fb_band_solve_accumulate": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
+                                         P, P, c_int64, P, P, c_int64, c_int64, c_int, P, P, P, c_double, P,
+                                         P, P, c_int64]),
     "fb_band_solve_batched": (c_int, [P, c_int, c_int, c_int, c_int, P, P, c_int64, P, c_int64, P, c_int64,
                                       P, P, c_int64, c_int64]),
     "fb_csr_matvec": (c_int, [P, c_int, c_int, P, P, P, P, P, P, c_int64, P, P, c_int64, P]),

@@ -162,8 +162,14 @@ class DeviceBandOps:
 
     on_device = True
 
-    def __init__(self, dev, FA: Planar, FB: Planar | None, kl: int, hermitian: bool, cache_bytes=None):
+    def __init__(self, dev, FA: Planar, FB: Planar | None, kl: int, hermitian: bool, cache_bytes=None,
+                 mv_a=None, mv_b=None):
         self.dev, self.FA, self.FB, self.kl, self.hermitian = dev, FA, FB, kl, hermitian
+        # (band, kl) the matvecs stream: a matrix narrower than the common
+        # factorization bandwidth kl = max(kla, klb) keeps its own compact copy
+        # (the C4 mass matrix has 3 diagonals, its padded copy 33)
+        self._mv_a = mv_a or (FA, kl)
+        self._mv_b = mv_b or (FB, kl)
         self.n = FA.cols
         self.factorizations = 0
         self.partitioned = int(dev.lib.fb_band_aux_doubles(self.n, kl)) > 0 if self.n > 0 else False
@@ -258,11 +264,7 @@ class DeviceBandOps:
         dev, n, m = self.dev, self.n, Y.cols
         for bb in self._batches:
             cnt = bb.count
-            mp = m + (m & 1)   # even leading dimension: 16-byte correction GEMM rows
-            X = self._xbuf.get(id(bb))
-            if X is None or X.shape[3] != mp:
-                X = dev.torch.empty((2, cnt, n, mp), dtype=dev.torch.float64, device=dev.tdev)
-                self._xbuf[id(bb)] = X
+            X, mp = self._xwork(bb, m)
             fr, fi, fs, piv, ps, aux, as_ = bb.args()
             # every shift reads the pass's Y directly (stride 0, real or planar)
             dev.check(dev.lib.fb_band_solve_batched_rhs(dev.h, cnt, n, self.kl, m, fr, fi, fs, piv, ps, aux, as_,
@@ -271,6 +273,40 @@ class DeviceBandOps:
                       "band_solve_batched_rhs")
             for i in range(cnt):
                 self._pass[(id(bb), i)] = (X, i, m)
+
+    def _xwork(self, bb, m):
+        mp = m + (m & 1)   # even leading dimension: 16-byte rows
+        X = self._xbuf.get(id(bb))
+        if X is None or X.shape[3] != mp:
+            X = self.dev.torch.empty((2, bb.count, self.n, mp), dtype=self.dev.torch.float64, device=self.dev.tdev)
+            self._xbuf[id(bb)] = X
+        return X, mp
+
+    def solve_pass_accumulate(self, Y: Planar, spec, radius, Q: Planar):
+        """The whole contour pass in one call (fb_band_solve_accumulate): every
+        shift of ``spec`` = [(z, adjoint, variant, w, theta)] solved against Y
+        and its quadrature term folded into Q in that order, the spike
+        correction applied inside the accumulation kernel.  Returns False
+        (nothing done) unless all of the pass's shifts sit in one factor batch."""
+        self._pass = {}
+        if not self.partitioned or not spec or len(spec) > 64:
+            return False
+        hits = [self._zmap.get(complex(z).conjugate() if adj else complex(z)) for z, adj, *_ in spec]
+        if any(h is None for h in hits) or any(h[0] is not hits[0][0] for h in hits):
+            return False
+        bb = hits[0][0]
+        dev, n, m, k = self.dev, self.n, Y.cols, len(spec)
+        X, mp = self._xwork(bb, m)
+        fr, fi, fs, piv, ps, aux, as_ = bb.args()
+        item = (ctypes.c_int * k)(*[h[1] for h in hits])
+        var = (ctypes.c_int * k)(*[int(t[2]) for t in spec])
+        w = (ctypes.c_double * k)(*[float(t[3]) for t in spec])
+        th = (ctypes.c_double * k)(*[float(t[4]) for t in spec])
+        dev.check(dev.lib.fb_band_solve_accumulate(
+            dev.h, bb.count, n, self.kl, m, fr, fi, fs, piv, ps, aux, as_, Y.re, Y.im, Y.ld,
+            X[0].data_ptr(), X[1].data_ptr(), mp, n * mp, k, item, var, w, float(radius), th,
+            Q.re, Q.im, Q.ld), "band_solve_accumulate")
+        return True
 
     def pass_result(self, z, adjoint):
         """Planar view of this pass's solve for shift z (A^H: the conj(z) factor)."""
@@ -316,19 +352,19 @@ class DeviceBandOps:
     def solve_adjoint(self, f, W):
         self._solve(f, W, True)
 
-    def _mult(self, F, X, Y):
-        dev = self.dev
-        dev.check(dev.lib.fb_band_matvec(dev.h, self.n, self.kl, X.cols, F.re, F.im, F.ld,
+    def _mult(self, mv, X, Y):
+        dev, (F, kl) = self.dev, mv
+        dev.check(dev.lib.fb_band_matvec(dev.h, self.n, kl, X.cols, F.re, F.im, F.ld,
                                          X.re, X.im, X.ld, Y.re, Y.im, Y.ld), "band_matvec")
 
     def multiply_a(self, X, Y):
-        self._mult(self.FA, X, Y)
+        self._mult(self._mv_a, X, Y)
 
     def multiply_b(self, X, Y):
         if self.FB is None:
             Y.copy_from(X)
         else:
-            self._mult(self.FB, X, Y)
+            self._mult(self._mv_b, X, Y)
 
 
 class B200BandOps:
@@ -422,7 +458,13 @@ def _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, hermi
         if x0 is None:
             raise ValueError("fpm(5)=1 requires an initial subspace x0")
         dev.upload(np.asarray(x0)[:, :m0], cplx=hermitian, out=kernel.X)
-    ops = DeviceBandOps(dev, FA, FB, kl, hermitian)
+    try:
+        mv_a = (expand_band_device(dev, a, kla, uplo, hermitian, kla), kla) if kla < kl else None
+        mv_b = (expand_band_device(dev, b, klb, uplo, hermitian, klb), klb) if b is not None and klb < kl else None
+    except MemoryError:
+        kernel.abort(-1)
+        return kernel.result
+    ops = DeviceBandOps(dev, FA, FB, kl, hermitian, mv_a=mv_a, mv_b=mv_b)
     result = run_rci(kernel, ops, options)
     result.factorizations = ops.factorizations
     return result

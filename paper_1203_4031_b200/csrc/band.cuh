@@ -29,5 +29,12 @@ cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* w
                              double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st,
                              const double* yr = nullptr, const double* yi = nullptr, long long ldy = 0,
                              long long sy = 0);
+struct AccTerms;
+cudaError_t band_spike_solve_accumulate(int count, int n, int kl, int nrhs, const double* wr, const double* wi,
+                                        long long sw, const int* ipiv, long long sp, const double* aux, long long sa,
+                                        double* xr, double* xi, long long ldx, long long sx, double* scratch,
+                                        cudaStream_t st, const double* yr, const double* yi, long long ldy,
+                                        const AccTerms& terms, const int* item, double* qr, double* qi,
+                                        long long ldq);
 
 }  // namespace fb

@@ -36,6 +36,7 @@
 #include "band.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
+#include "misc.cuh"
 
 namespace fb {
 
@@ -236,13 +237,15 @@ __global__ void __launch_bounds__(WPB * 32) band_pfactor_kernel(PFArgs a) {
   if (bad && lane == 0) atomicMin(a.info + k, bad);
 }
 
-// ---- partition solve (direct): one warp per (partition, 32 columns, shift) ----
+// ---- partition solve arguments (staged sweeps below) ----------------------------
 struct PSArgs {
-  int n, kl, P, nrhs;
+  int n, kl, P, nrhs, count;
   const double *wr, *wi;
   long long sw;
   const int* ipiv;
   long long sp;
+  const double2* us;  // slot-ordered U columns of item 0 (item k at + k*sa doubles)
+  long long sa;
   double *xr, *xi;
   long long ldx, sx;
   // forward sweep input (nullptr: in place from x); fi == nullptr: real input;
@@ -250,107 +253,6 @@ struct PSArgs {
   const double *fr, *fi;
   long long ldf, sf;
 };
-
-template <int KL>
-__global__ void __launch_bounds__(WPB * 32) band_psolve_kernel(PSArgs a) {
-  constexpr int KV = 2 * KL, LW = 3 * KL + 1;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int part = blockIdx.x * WPB + wid, chunk = blockIdx.y, k = blockIdx.z;
-  if (part >= a.P) return;
-  const int col = chunk * 32 + lane;
-  const bool on = col < a.nrhs;
-  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
-  const double* Wr = a.wr + k * a.sw;
-  const double* Wi = a.wi + k * a.sw;
-  const int* ipiv = a.ipiv + k * a.sp;
-  double* Xr = a.xr + k * a.sx;
-  double* Xi = a.xi + k * a.sx;
-  auto ld = [&](int r, double& vr, double& vi) {
-    if (on && r < hi) {
-      const long long o = (long long)r * a.ldx + col;
-      vr = Xr[o];
-      vi = Xi[o];
-    } else {
-      vr = vi = 0.0;
-    }
-  };
-  // forward: pivots interleaved with unit L (rows j..j+KL live)
-  double wr_[KL + 1], wi_[KL + 1];
-#pragma unroll
-  for (int i = 0; i <= KL; ++i) ld(lo + i, wr_[i], wi_[i]);
-  for (int j = lo; j < hi; ++j) {
-    const int p = ipiv[j] - j;
-    if (p) {
-#pragma unroll
-      for (int i = 1; i <= KL; ++i)
-        if (i == p) {
-          const double tr = wr_[0], ti = wi_[0];
-          wr_[0] = wr_[i];
-          wi_[0] = wi_[i];
-          wr_[i] = tr;
-          wi_[i] = ti;
-        }
-    }
-    const double x0r = wr_[0], x0i = wi_[0];
-    const double* lr = Wr + (long long)j * LW + KV + 1;
-    const double* li = Wi + (long long)j * LW + KV + 1;
-#pragma unroll
-    for (int i = 0; i < KL; ++i) {  // multipliers beyond the partition are stored as 0
-      const double ar = __ldg(lr + i), ai = __ldg(li + i);
-      wr_[1 + i] -= ar * x0r - ai * x0i;
-      wi_[1 + i] -= ar * x0i + ai * x0r;
-    }
-    if (on) {
-      const long long o = (long long)j * a.ldx + col;
-      Xr[o] = x0r;
-      Xi[o] = x0i;
-    }
-#pragma unroll
-    for (int i = 0; i < KL; ++i) {
-      wr_[i] = wr_[i + 1];
-      wi_[i] = wi_[i + 1];
-    }
-    ld(j + KL + 1, wr_[KL], wi_[KL]);
-  }
-  // backward: x_j = y_j / U_jj, then y[j-KV..j-1] -= U[., j] x_j (rows j-KV..j live)
-  double ur_[KV + 1], ui_[KV + 1];
-  auto ldb = [&](int r, double& vr, double& vi) {
-    if (on && r >= lo) {
-      const long long o = (long long)r * a.ldx + col;
-      vr = Xr[o];
-      vi = Xi[o];
-    } else {
-      vr = vi = 0.0;
-    }
-  };
-#pragma unroll
-  for (int i = 0; i <= KV; ++i) ldb(hi - 1 - KV + i, ur_[i], ui_[i]);
-  for (int j = hi - 1; j >= lo; --j) {
-    const double* cr = Wr + (long long)j * LW;
-    const double* ci = Wi + (long long)j * LW;
-    const double dr = __ldg(cr + KV), di = __ldg(ci + KV);
-    const double den = dr * dr + di * di;
-    const double yr = ur_[KV], yi = ui_[KV];
-    const double qr = (yr * dr + yi * di) / den, qi = (yi * dr - yr * di) / den;
-#pragma unroll
-    for (int i = 0; i < KV; ++i) {  // U entries above the partition are stored as 0
-      const double br = __ldg(cr + i), bi = __ldg(ci + i);
-      ur_[i] -= br * qr - bi * qi;
-      ui_[i] -= br * qi + bi * qr;
-    }
-    if (on) {
-      const long long o = (long long)j * a.ldx + col;
-      Xr[o] = qr;
-      Xi[o] = qi;
-    }
-#pragma unroll
-    for (int i = KV; i > 0; --i) {
-      ur_[i] = ur_[i - 1];
-      ui_[i] = ui_[i - 1];
-    }
-    ldb(j - 1 - KV, ur_[0], ui_[0]);
-  }
-}
 
 // ---- spike right-hand sides: [0; B_j] in columns 0..kl-1, [C_j; 0] in kl..2kl-1 ----
 struct SIArgs {
@@ -677,59 +579,6 @@ __global__ void __launch_bounds__(RT) band_rsolve_kernel(RSArgs a) {
   }
 }
 
-// ---- correction x_j = g_j - V_j x_{j+1}^t - W_j x_{j-1}^b -----------------------
-struct CKArgs {
-  int n, kl, P, nrhs;
-  const double *sr, *si;
-  long long ss;
-  const double *yr, *yi;
-  long long sy;
-  double *xr, *xi;
-  long long ldx, sx;
-};
-
-template <int KL>
-__global__ void __launch_bounds__(WPB * 32) band_correct_kernel(CKArgs a) {
-  constexpr int W2 = 2 * KL;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int part = blockIdx.x * WPB + wid, chunk = blockIdx.y, k = blockIdx.z;
-  if (part >= a.P) return;
-  const int col = chunk * 32 + lane;
-  if (col >= a.nrhs) return;
-  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
-  const double* Sr = a.sr + k * a.ss;
-  const double* Si = a.si + k * a.ss;
-  const double* Yr = a.yr + k * a.sy;
-  const double* Yi = a.yi + k * a.sy;
-  double* Xr = a.xr + k * a.sx;
-  double* Xi = a.xi + k * a.sx;
-  double tr[W2], ti[W2];  // (x_{j+1}^t, x_{j-1}^b)
-#pragma unroll
-  for (int q = 0; q < KL; ++q) {
-    const bool nx = part + 1 < a.P, pv = part > 0;
-    const long long on = ((long long)part * W2 + KL + q) * a.nrhs + col;        // y_part[kl + q]
-    const long long op = ((long long)(part - 1) * W2 + q) * a.nrhs + col;       // y_{part-1}[q]
-    tr[q] = nx ? Yr[on] : 0.0;
-    ti[q] = nx ? Yi[on] : 0.0;
-    tr[KL + q] = pv ? Yr[op] : 0.0;
-    ti[KL + q] = pv ? Yi[op] : 0.0;
-  }
-  for (int r = lo; r < hi; ++r) {
-    const double* sr = Sr + (long long)r * W2;
-    const double* si = Si + (long long)r * W2;
-    double ar = 0.0, ai = 0.0;
-#pragma unroll
-    for (int q = 0; q < W2; ++q) {
-      const double vr = __ldg(sr + q), vi = __ldg(si + q);
-      ar += vr * tr[q] - vi * ti[q];
-      ai += vr * ti[q] + vi * tr[q];
-    }
-    const long long o = (long long)r * a.ldx + col;
-    Xr[o] -= ar;
-    Xi[o] -= ai;
-  }
-}
-
 // ---- tips of partition j in spike-column order: T_j = [x_{j+1}^t ; x_{j-1}^b] ----------
 // (zero where the neighbour does not exist), so that the correction of every
 // partition is one product X_j -= [V_j W_j] T_j.  Item k = blockIdx.y.
@@ -764,16 +613,67 @@ __global__ void band_tips_kernel(TGArgs a) {
   }
 }
 
-// ---- staged partition solves: one CTA per (partition, column block, shift) -------
-// All warps of a CTA share the factor columns, staged through shared memory in
-// chunks of TC columns by cp.async (double-buffered) with re/im interleaved so
-// one LDS.128 feeds a complex multiply-add; each thread keeps its right-hand
-// side column's active rows in a register window and the next QD rows in a
-// prefetch queue (the global load of a row entering the window was issued QD
-// steps earlier).  Forward (pivots + unit L) and backward (U) are separate
+// ---- slot-ordered copy of U for the backward sweep (built once per factorization) ----
+// The backward sweep keeps each right-hand side's active rows j-2kl..j in
+// 2kl+1 registers ("slots") that do not move inside a chunk of SCB rows: at
+// the chunk starting with row j1, slot s holds row j1 - s; step jj solves
+// slot jj and gives it to the entering row j1 - jj - (2kl+1), so every slot
+// index in the unrolled chunk body is a compile-time constant.  Between
+// chunks the slots rotate by SCB (register renaming at the loop edge, paid
+// once per chunk).  The U column of step j is re-ordered to match, once:
+// Us[j][s] = U(row in slot s, j), 0 for row j's own slot,
+// Us[j][2kl+1] = 1 / U(j, j).
+__host__ __device__ constexpr int bwd_chunk(int kl) { return 2 * kl + 1 < 8 ? 2 * kl + 1 : 8; }
+
+struct SOArgs {
+  int n, kl, P;
+  const double *wr, *wi;
+  long long sw;
+  double2* us;  // item 0; item k at + k*sa doubles
+  long long sa;
+};
+
+__global__ void band_slot_bwd_kernel(SOArgs a) {
+  const int k = blockIdx.y, kl = a.kl, KV = 2 * kl, NB = KV + 1, LW = 3 * kl + 1, NU = NB + 1;
+  const double* Wr = a.wr + k * a.sw;
+  const double* Wi = a.wi + k * a.sw;
+  double2* Us = reinterpret_cast<double2*>(reinterpret_cast<double*>(a.us) + k * a.sa);
+  const long long total = (long long)a.n * NU;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / NU), s = (int)(e % NU);
+    int part = (int)(((long long)j * a.P) / a.n);
+    while (part + 1 < a.P && part_lo(part + 1, a.n, a.P) <= j) ++part;
+    while (part_lo(part, a.n, a.P) > j) --part;
+    const int top = part_lo(part + 1, a.n, a.P) - 1, head = (top - j) % bwd_chunk(kl);
+    double2 v = make_double2(0.0, 0.0);
+    if (s == NB) {
+      const double dr = Wr[(long long)j * LW + KV], di = Wi[(long long)j * LW + KV];
+      const double den = dr * dr + di * di;
+      if (den > 0.0) v = make_double2(dr / den, -di / den);
+    } else if (s != head) {
+      // step head of its chunk: row j - d (d = 1..KV) sits in slot (head + d) mod NB, U entry KV - d
+      int d = s - head;
+      if (d < 0) d += NB;
+      v = make_double2(Wr[(long long)j * LW + KV - d], Wi[(long long)j * LW + KV - d]);
+    }
+    Us[e] = v;
+  }
+}
+
+// ---- staged partition solves: one CTA per (partition, shift, column block) -------
+// One thread per right-hand side keeps its column's active rows in registers;
+// all threads of a CTA share the factor columns, staged through shared memory
+// in chunks of rows by cp.async (double buffered, re/im interleaved so one
+// LDS.128 feeds a complex multiply-add) together with the right-hand-side rows
+// that will ENTER the window during the chunk.  The shift index is the fastest
+// grid index, so the CTAs that read the same rows of a shared right-hand side
+// run together (L2).  Forward (pivots + unit L) and backward (U) are separate
 // kernels so each keeps its own register window.
-constexpr int TC = 32;     // rows per staged chunk (correction)
-constexpr int SNW = 3;     // warps per CTA (96 right-hand sides)
+constexpr int SNW = 3;   // warps per CTA (96 right-hand sides)
+constexpr int SC = 8;    // forward sweep rows per staged chunk
+constexpr int NST = 3;   // staged chunks in flight (the loads of a chunk are issued NST-1 chunks ahead)
+size_t sweep_xring_bytes(int nt, int sc) { return sizeof(double) * NST * sc * 2 * (size_t)nt; }
 
 // One forward step with the row interchange (0 <-> P) folded in at compile
 // time: x0 = w[P]; the window slides by one as each multiply-add writes row
@@ -796,18 +696,10 @@ __device__ __forceinline__ void fwd_step(double (&wr)[KL + 1], double (&wi)[KL +
   }
 }
 
-// Sweeps stage SC rows per chunk: the factor columns of the chunk's rows and,
-// for every thread's column, the SC right-hand-side rows that will ENTER the
-// register window during the chunk, one chunk ahead by cp.async (no register
-// queue; the load of a row is issued ~SC steps of the whole CTA before use).
-constexpr int SC = 12;   // forward sweep (4 CTAs per SM)
-constexpr int SCB = 12;  // backward sweep chunk (4 CTAs per SM at <= 168 registers)
-size_t sweep_xring_bytes(int nt, int sc = SC) { return sizeof(double) * 2 * sc * 2 * (size_t)nt; }
-
 template <int KL>
 __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) {
   constexpr int KV = 2 * KL, LW = 3 * KL + 1;
-  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, nt = blockDim.x;
+  const int k = blockIdx.x % a.count, part = blockIdx.x / a.count, tid = threadIdx.x, nt = blockDim.x;
   const int col = blockIdx.y * nt + tid;
   const bool on = col < a.nrhs;
   const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
@@ -820,9 +712,9 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
   const double* Fr = sep ? a.fr + k * a.sf : Xr;
   const double* Fi = sep ? (a.fi ? a.fi + k * a.sf : nullptr) : Xi;
   const long long ldf = sep ? a.ldf : a.ldx;
-  extern __shared__ double sx[];  // [2 buf][SC rows][2 planes][nt]
-  __shared__ double2 sl[2][SC][KL];  // multipliers (re, im) of column j
-  __shared__ int spv[2][SC];
+  extern __shared__ __align__(16) double sx[];  // [NST buf][SC rows][nt] (re, im)
+  __shared__ double2 sl[NST][SC][KL];           // multipliers (re, im) of column j
+  __shared__ int spv[NST][SC];
   const int xbase = lo + KL + 1;  // row entering the window at step lo
   auto stage = [&](int buf, int c) {
     const int j0 = lo + c * SC;
@@ -834,14 +726,14 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
       cp_async8(&sl[buf][jj][i].y, Wi + o, ok);
     }
     for (int jj = tid; jj < SC; jj += nt) cp_async4(&spv[buf][jj], ipiv + min(j0 + jj, hi - 1), j0 + jj < hi);
-    double* xb = sx + (size_t)buf * SC * 2 * nt;
+    double* xb = sx + (size_t)buf * SC * 2 * nt + 2 * tid;
+    const double* fr = Fr + (long long)(xbase + c * SC) * ldf + col;
+    const double* fi = Fi ? Fi + (long long)(xbase + c * SC) * ldf + col : nullptr;
 #pragma unroll
     for (int r = 0; r < SC; ++r) {
-      const int row = xbase + c * SC + r;
-      const bool ok = on && row < hi;
-      const long long o = ok ? (long long)row * ldf + col : 0;
-      cp_async8(xb + (r * 2) * nt + tid, Fr + o, ok);
-      cp_async8(xb + (r * 2 + 1) * nt + tid, Fi ? Fi + o : Fr + o, ok && Fi != nullptr);
+      const bool ok = on && xbase + c * SC + r < hi;
+      cp_async8(xb + r * 2 * nt, ok ? fr + r * ldf : Fr, ok);
+      cp_async8(xb + r * 2 * nt + 1, ok && fi ? fi + r * ldf : Fr, ok && fi != nullptr);
     }
     cp_async_commit();
   };
@@ -855,23 +747,21 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
       if (Fi) wi_[i] = Fi[o];
     }
   }
+  double* pxr = Xr + (long long)lo * a.ldx + col;
+  double* pxi = Xi + (long long)lo * a.ldx + col;
   const int nch = (hi - lo + SC - 1) / SC;
-  stage(0, 0);
+#pragma unroll
+  for (int c = 0; c < NST - 1; ++c) stage(c, c);  // chunks past the end: all zero-filled
+  int buf = 0;
   for (int c = 0; c < nch; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nch) {
-      stage(buf ^ 1, c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    stage(buf == 0 ? NST - 1 : buf - 1, c + NST - 1);
+    cp_async_wait<NST - 1>();
     __syncthreads();
     const int j0 = lo + c * SC, jn = min(SC, hi - j0);
-    const double* xb = sx + (size_t)buf * SC * 2 * nt;
+    const double2* xb = reinterpret_cast<const double2*>(sx + (size_t)buf * SC * 2 * nt) + tid;
 #pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
-      const int j = j0 + jj;
-      const int p = spv[buf][jj] - j;
+      const int p = spv[buf][jj] - (j0 + jj);
       const double2* lcol = sl[buf][jj];
       double x0r, x0i;
 #define FB_FWD_CASE(I)                                                          \
@@ -886,193 +776,338 @@ __global__ void __launch_bounds__(SNW * 32, 4) band_psolve_fwd_kernel(PSArgs a) 
       }
 #undef FB_FWD_CASE
       if (on) {
-        const long long o = (long long)j * a.ldx + col;
-        Xr[o] = x0r;
-        Xi[o] = x0i;
+        *pxr = x0r;
+        *pxi = x0i;
       }
-      wr_[KL] = xb[(jj * 2) * nt + tid];
-      wi_[KL] = xb[(jj * 2 + 1) * nt + tid];
+      pxr += a.ldx;
+      pxi += a.ldx;
+      const double2 nv = xb[jj * nt];
+      wr_[KL] = nv.x;
+      wi_[KL] = nv.y;
     }
+    buf = buf + 1 == NST ? 0 : buf + 1;
     __syncthreads();
   }
+  cp_async_wait<0>();
 }
 
-// Backward sweep: one thread per right-hand side holds rows j-KV..j in
-// registers; the U column (re, im interleaved, 1/U_jj computed per chunk)
-// and the rows entering the window come from shared memory.
-template <int KL>
-__global__ void __launch_bounds__(SNW * 32, 4) band_psolve_bwd_kernel(PSArgs a) {
-  constexpr int KV = 2 * KL, LW = 3 * KL + 1;
-  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x, nt = blockDim.x;
-  const int col = blockIdx.y * nt + tid;
+// Backward sweep (slots as described above the re-ordering kernel): step jj
+// of a chunk solves slot jj, x = w[jj] / U_jj, the entering row takes slot jj,
+// and every slot is updated with its U entry (0 for slot jj) by straight-line
+// multiply-adds on fixed registers.  Staging: the chunk's U columns are one
+// contiguous run of the slot-ordered copy and every entering right-hand-side
+// row is one contiguous run per plane, so ONE elected thread moves a chunk with
+// 1 + 2*SCB bulk copies (cp.async.bulk, the TMA engine) that complete on the
+// chunk's mbarrier -- the other threads carry no staging code or registers.
+// Rows past the partition start are not copied: their U entries are zero, so
+// whatever sits in the ring never reaches a stored value.
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, void* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Each right-hand side is carried by TWO adjacent lanes: the even lane holds the
+// real parts of the 2KL+1 active rows, the odd lane the imaginary parts (half
+// the registers per thread, twice the warps per SM).  Both lanes run the same
+// code: w -= u.x*q1 - u.y*q2 with (q1, q2) = (q_re, q_im) for the real lane and
+// (q_im, -q_re) for the imaginary lane; the solved value's other component
+// comes from the partner lane by one shuffle.
+// BULK = false (odd leading dimension: rows not 16-byte aligned): every thread
+// stages its own entries with cp.async instead, same ring layout.
+constexpr int BNC = 48;  // right-hand sides per CTA of the backward sweep (96 threads: 5 CTAs per SM at 128 registers)
+
+template <int KL, bool BULK>
+__global__ void __launch_bounds__(2 * BNC, 5) band_psolve_bwd_kernel(PSArgs a) {
+  constexpr int KV = 2 * KL, NB = KV + 1, NU = NB + 1, SCB = bwd_chunk(KL);
+  const int k = blockIdx.x % a.count, part = blockIdx.x / a.count, tid = threadIdx.x;
+  const int nc = blockDim.x >> 1;  // columns of this CTA
+  const int col0 = blockIdx.y * nc, col = col0 + (tid >> 1);
+  const bool im = tid & 1;
   const bool on = col < a.nrhs;
   const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
-  const double* Wr = a.wr + k * a.sw;
-  const double* Wi = a.wi + k * a.sw;
+  const double2* Us = reinterpret_cast<const double2*>(reinterpret_cast<const double*>(a.us) + k * a.sa);
   double* Xr = a.xr + k * a.sx;
   double* Xi = a.xi + k * a.sx;
-  extern __shared__ double sx[];         // [2 buf][SCB rows][2 planes][nt]
-  __shared__ double2 su[2][SCB][KV + 1];  // U column j (rows j-KV..j); slot KV <- 1/U_jj
-  const int xtop = hi - 2 - KV;          // row entering the window at step hi-1
+  double* Xo = im ? Xi : Xr;  // this lane's plane
+  extern __shared__ __align__(16) double sx[];  // [NST buf][2 planes][SCB rows][nc]
+  __shared__ __align__(16) double2 su[NST][SCB * NU];
+  __shared__ __align__(8) unsigned long long full[NST];
+  const int top = hi - 1;
+  // columns of this CTA, rounded up to a whole 16 bytes (the pad column exists: ldx is even)
+  const unsigned rowbytes = 8u * (unsigned)((min(nc, a.nrhs - col0) + 1) & ~1);
+  if (BULK && tid == 0) {
+#pragma unroll
+    for (int b = 0; b < NST; ++b) mbar_init(&full[b], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   auto stage = [&](int buf, int c) {
-    const int j1 = hi - 1 - c * SCB;
-    for (int e = tid; e < SCB * (KV + 1); e += nt) {
-      const int jj = e / (KV + 1), i = e % (KV + 1), j = j1 - jj;
-      const bool ok = j >= lo;
-      const long long o = ok ? (long long)j * LW + i : 0;
-      cp_async8(&su[buf][jj][i].x, Wr + o, ok);
-      cp_async8(&su[buf][jj][i].y, Wi + o, ok);
-    }
-    double* xb = sx + (size_t)buf * SCB * 2 * nt;
-#pragma unroll
-    for (int r = 0; r < SCB; ++r) {
-      const int row = xtop - c * SCB - r;
-      const bool ok = on && row >= lo;
-      const long long o = ok ? (long long)row * a.ldx + col : 0;
-      cp_async8(xb + (r * 2) * nt + tid, Xr + o, ok);
-      cp_async8(xb + (r * 2 + 1) * nt + tid, Xi + o, ok);
-    }
-    cp_async_commit();
-  };
-  double wr_[KV + 1], wi_[KV + 1];  // wr_[t] = row j-KV+t
-#pragma unroll
-  for (int t = 0; t <= KV; ++t) {
-    const int r = hi - 1 - KV + t;
-    wr_[t] = wi_[t] = 0.0;
-    if (on && r >= lo) {
-      const long long o = (long long)r * a.ldx + col;
-      wr_[t] = Xr[o];
-      wi_[t] = Xi[o];
-    }
-  }
-  const int nch = (hi - lo + SCB - 1) / SCB;
-  stage(0, 0);
-  for (int c = 0; c < nch; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nch) {
-      stage(buf ^ 1, c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    for (int jj = tid; jj < SCB; jj += nt) {
-      const double2 d = su[buf][jj][KV];
-      const double den = d.x * d.x + d.y * d.y;
-      su[buf][jj][KV] = den > 0.0 ? make_double2(d.x / den, -d.y / den) : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    const int j1 = hi - 1 - c * SCB, jn = min(SCB, j1 - lo + 1);
-    const double* xb = sx + (size_t)buf * SCB * 2 * nt;
+    const int j1 = top - c * SCB, jl = max(j1 - SCB + 1, lo);
+    const int r0 = j1 - NB;                       // row entering at step j1; step j1 - r takes row r0 - r
+    const int nr = max(0, min(SCB, r0 - lo + 1));  // rows r0, r0-1, ... that exist
+    double* xb = sx + (size_t)buf * 2 * SCB * nc;
+    if constexpr (BULK) {  // elected thread only
+      unsigned bytes = 0;
+      if (jl <= j1) bytes = (unsigned)(j1 - jl + 1) * NU * 16u;
+      mbar_arrive_expect_tx(&full[buf], bytes + 2u * nr * rowbytes);
+      if (bytes) bulk_g2s(&su[buf][(size_t)(jl - (j1 - SCB + 1)) * NU], Us + (long long)jl * NU, bytes, &full[buf]);
+      const double* fr = Xr + (long long)r0 * a.ldx + col0;
+      const double* fi = Xi + (long long)r0 * a.ldx + col0;
 #pragma unroll 1
-    for (int jj = 0; jj < jn; ++jj) {
-      const int j = j1 - jj;
-      const double2 dv = su[buf][jj][KV];
-      const double qr = wr_[KV] * dv.x - wi_[KV] * dv.y, qi = wr_[KV] * dv.y + wi_[KV] * dv.x;
-      // rows j-KV+t -= U(., j) x_j, written one slot up (the window slides)
+      for (int r = 0; r < nr; ++r) {
+        bulk_g2s(xb + r * nc, fr - r * a.ldx, rowbytes, &full[buf]);
+        bulk_g2s(xb + (SCB + r) * nc, fi - r * a.ldx, rowbytes, &full[buf]);
+      }
+    } else {
+      const int jb = j1 - SCB + 1;
+      for (int e = tid; e < SCB * NU; e += blockDim.x) {
+        const bool ok = jb + e / NU >= lo;
+        cp_async16(&su[buf][e], ok ? Us + (long long)jb * NU + e : Us, ok ? 16 : 0);
+      }
+#pragma unroll 1
+      for (int r = 0; r < SCB; ++r) {
+        const bool ok = on && r < nr;
+        cp_async8(xb + ((im ? SCB : 0) + r) * nc + (tid >> 1), ok ? Xo + (long long)(r0 - r) * a.ldx + col : Xo, ok);
+      }
+      cp_async_commit();
+    }
+  };
+  double w_[NB];  // slot s = this lane's component of row j1 - s of the current chunk
 #pragma unroll
-      for (int t = KV - 1; t >= 0; --t) {
-        if (t % 8 == 7) asm volatile("" ::: "memory");
-        const double2 u = su[buf][jj][t];
-        wr_[t + 1] = fma(-u.x, qr, fma(u.y, qi, wr_[t]));
-        wi_[t + 1] = fma(-u.x, qi, fma(-u.y, qr, wi_[t]));
+  for (int s = 0; s < NB; ++s) w_[s] = (on && top - s >= lo) ? Xo[(long long)(top - s) * a.ldx + col] : 0.0;
+  double* px = Xo + (long long)top * a.ldx + col;
+  const int nch = (hi - lo + SCB - 1) / SCB;
+  if (!BULK || tid == 0) {
+#pragma unroll 1
+    for (int c = 0; c < NST - 1; ++c) stage(c, c);
+  }
+  int buf = 0;
+  unsigned phase = 0;
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    // the buffer staged now was released at the end of chunk c-1
+    if (!BULK || tid == 0) stage(buf == 0 ? NST - 1 : buf - 1, c + NST - 1);
+    if constexpr (BULK) {
+      mbar_wait_parity(&full[buf], phase);
+    } else {
+      cp_async_wait<NST - 1>();
+      __syncthreads();
+    }
+    const int j1 = top - c * SCB;
+    const double* xb = sx + (size_t)buf * 2 * SCB * nc + (im ? SCB * nc : 0) + (tid >> 1);
+#pragma unroll
+    for (int jj = 0; jj < SCB; ++jj) {
+      const double nv = xb[jj * nc];
+      const double2* ucol = &su[buf][(SCB - 1 - jj) * NU];
+      const double2 dv = ucol[NB];
+      const double yo = w_[jj];
+      w_[jj] = nv;
+      const double yp = __shfl_xor_sync(0xffffffffu, yo, 1);  // the partner lane's component
+      const double yr = im ? yp : yo, yi = im ? yo : yp;
+      const double qr = yr * dv.x - yi * dv.y, qi = yr * dv.y + yi * dv.x;
+      const double q1 = im ? qi : qr, q2 = im ? -qr : qi;
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {  // slot jj (the entering row) has U entry 0
+        if (s % 8 == 7) asm volatile("" ::: "memory");  // keep the loads of u in groups of 8 (registers)
+        const double2 uv = ucol[s];
+        w_[s] = fma(-uv.x, q1, fma(uv.y, q2, w_[s]));
       }
-      if (on) {
-        const long long o = (long long)j * a.ldx + col;
-        Xr[o] = qr;
-        Xi[o] = qi;
+      if (on && j1 - jj >= lo) px[-(long long)jj * a.ldx] = q1;
+    }
+    px -= (long long)SCB * a.ldx;
+    {  // rotate the slots by SCB for the next chunk
+      double t[NB];
+#pragma unroll
+      for (int s = 0; s < NB; ++s) t[s] = w_[(s + SCB) % NB];
+#pragma unroll
+      for (int s = 0; s < NB; ++s) w_[s] = t[s];
+    }
+    if (++buf == NST) {
+      buf = 0;
+      phase ^= 1;
+    }
+    __syncthreads();  // every thread is done with the chunk's buffer
+  }
+  if constexpr (!BULK) cp_async_wait<0>();
+}
+
+// ---- fused spike correction + quadrature accumulation ---------------------------
+// Q -= sum_t coeff_t * (g_t - [V W]_t T_t): the correction product runs on the
+// FP64 tensor pipe with the accumulators starting from the partition solve g
+// (read once, never rewritten) and the quadrature term of every shift is folded
+// into Q held in registers (kernel.py:108-124 arithmetic, term by term in the
+// caller's order), so one contour pass reads each g and spike row once and
+// writes Q once.  One CTA = (partition, FA_CHUNK-row chunk, 48-column group);
+// a warp owns 8-row tiles.  The K index of the product is permuted (lane
+// quarter q owns k = q*KS .. q*KS+KS-1) so that every lane reads its spike
+// entries as one contiguous run; the (negated) tips are staged in shared
+// memory in B-fragment order under the same permutation.
+constexpr int FA_NT = 6;        // 8-column DMMA tiles per warp
+constexpr int FA_COLS = FA_NT * 8;
+constexpr int FA_CHUNK = 1024;  // rows per CTA
+constexpr int FA_MAXG = 8;      // terms whose tips are staged together (24 KB each at kl = 16)
+constexpr int FA_KS = 2 * KLMAX / 4;
+
+struct FAArgs {
+  int n, kl, P, nrhs, nterms, chunks;
+  const double *sr, *si;
+  long long ss;
+  const double *tr, *ti;  // tips [item][P][2kl][nrhs]
+  long long st;
+  const double *xr, *xi;  // partition solves g [item][n][ldx]
+  long long ldx, sx;
+  double *qr, *qi;
+  long long ldq;
+  int item[kMaxAccTerms], mode[kMaxAccTerms];
+  double h[kMaxAccTerms], cr[kMaxAccTerms], ci[kMaxAccTerms];
+};
+
+__device__ __forceinline__ double dneg_(double v) {
+  return __longlong_as_double(__double_as_longlong(v) ^ 0x8000000000000000ull);
+}
+
+template <bool CQ, int NTHREADS>
+__global__ void __launch_bounds__(NTHREADS, 1) band_correct_accumulate_kernel(const __grid_constant__ FAArgs a) {
+  extern __shared__ double sT[];  // [G][2 planes][KS][FA_NT][32 lanes] = -tips in B-fragment order
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NTHREADS / 32;
+  const int g = lane >> 2, q = lane & 3;
+  const int part = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
+  const int c0 = blockIdx.y * FA_COLS;
+  const int w = 2 * a.kl, KS = (w + 3) / 4;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
+  const int r_begin = lo + chunk * FA_CHUNK, r_end = min(hi, r_begin + FA_CHUNK);
+  if (r_begin >= r_end) return;
+  const bool vx = (a.ldx & 1) == 0 && (a.sx & 1) == 0;  // 16-byte g loads
+  const bool vs = (KS & 1) == 0;                         // 16-byte spike loads
+  const int plane = KS * FA_NT * 32;
+  for (int t0 = 0; t0 < a.nterms; t0 += FA_MAXG) {
+    const int G = min(FA_MAXG, a.nterms - t0);
+    __syncthreads();
+    for (int e = tid; e < G * 2 * plane; e += NTHREADS) {
+      const int l = e & 31;
+      int rest = e >> 5;
+      const int t = rest % FA_NT;
+      rest /= FA_NT;
+      const int j = rest % KS;
+      rest /= KS;
+      const int pl = rest & 1, ti = rest >> 1;
+      const int k = (l & 3) * KS + j, col = c0 + t * 8 + (l >> 2);
+      double v = 0.0;
+      if (k < w && col < a.nrhs) {
+        const double* src = (pl ? a.ti : a.tr) + a.item[t0 + ti] * a.st;
+        v = -src[((long long)part * w + k) * a.nrhs + col];
       }
-      wr_[0] = xb[(jj * 2) * nt + tid];
-      wi_[0] = xb[(jj * 2 + 1) * nt + tid];
+      sT[e] = v;
     }
     __syncthreads();
+    for (int r0 = r_begin + warp * 8; r0 < r_end; r0 += NW * 8) {
+      const int row = r0 + g;
+      const bool rok = row < r_end;
+      double q_r[FA_NT][2], q_i[FA_NT][2];
+#pragma unroll
+      for (int t = 0; t < FA_NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = c0 + t * 8 + 2 * q + e;
+          const bool ok = rok && col < a.nrhs;
+          q_r[t][e] = ok ? a.qr[(long long)row * a.ldq + col] : 0.0;
+          q_i[t][e] = (CQ && ok) ? a.qi[(long long)row * a.ldq + col] : 0.0;
+        }
+      for (int ti = 0; ti < G; ++ti) {
+        const int it = a.item[t0 + ti];
+        const double* Sr = a.sr + it * a.ss + (long long)row * w + q * KS;
+        const double* Si = a.si + it * a.ss + (long long)row * w + q * KS;
+        const double* Xr = a.xr + it * a.sx + (long long)row * a.ldx;
+        const double* Xi = a.xi + it * a.sx + (long long)row * a.ldx;
+        double s_r[FA_KS], s_i[FA_KS], c_r[FA_NT][2], c_i[FA_NT][2];
+        if (vs) {
+#pragma unroll
+          for (int j = 0; j < FA_KS; j += 2) {
+            double2 vr = make_double2(0.0, 0.0), vi = vr;
+            if (rok && j < KS && q * KS + j < w) {
+              vr = __ldcs(reinterpret_cast<const double2*>(Sr + j));
+              vi = __ldcs(reinterpret_cast<const double2*>(Si + j));
+            }
+            s_r[j] = vr.x; s_r[j + 1] = vr.y;
+            s_i[j] = vi.x; s_i[j + 1] = vi.y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < FA_KS; ++j) {
+            const bool ok = rok && j < KS && q * KS + j < w;
+            s_r[j] = ok ? __ldcs(Sr + j) : 0.0;
+            s_i[j] = ok ? __ldcs(Si + j) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < FA_NT; ++t) {
+          const int col = c0 + t * 8 + 2 * q;
+          if (vx && rok && col + 1 < a.nrhs) {
+            const double2 vr = __ldcs(reinterpret_cast<const double2*>(Xr + col));
+            const double2 vi = __ldcs(reinterpret_cast<const double2*>(Xi + col));
+            c_r[t][0] = vr.x; c_r[t][1] = vr.y;
+            c_i[t][0] = vi.x; c_i[t][1] = vi.y;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = rok && col + e < a.nrhs;
+              c_r[t][e] = ok ? __ldcs(Xr + col + e) : 0.0;
+              c_i[t][e] = ok ? __ldcs(Xi + col + e) : 0.0;
+            }
+          }
+        }
+        const double* br_ = sT + (size_t)(ti * 2) * plane + lane;
+        const double* bi_ = br_ + plane;
+#pragma unroll
+        for (int j = 0; j < FA_KS; ++j) {
+          if (j < KS) {
+            const double ar = s_r[j], ai = s_i[j], nai = dneg_(ai);
+#pragma unroll
+            for (int t = 0; t < FA_NT; ++t) {
+              const double tr_ = br_[(j * FA_NT + t) * 32], ti_ = bi_[(j * FA_NT + t) * 32];  // -T
+              dmma(c_r[t][0], c_r[t][1], ar, tr_);    // - S_r T_r
+              dmma(c_r[t][0], c_r[t][1], nai, ti_);   // + S_i T_i
+              dmma(c_i[t][0], c_i[t][1], ar, ti_);    // - S_r T_i
+              dmma(c_i[t][0], c_i[t][1], ai, tr_);    // - S_i T_r
+            }
+          }
+        }
+        const double cr = a.cr[t0 + ti], ci = a.ci[t0 + ti], hh = a.h[t0 + ti];
+#pragma unroll
+        for (int t = 0; t < FA_NT; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double x = c_r[t][e], y = c_i[t][e];
+            if (!CQ) {
+              const double v = __dsub_rn(__dmul_rn(cr, x), __dmul_rn(ci, y));
+              q_r[t][e] = __dsub_rn(q_r[t][e], __dmul_rn(hh, v));
+            } else {
+              const double vr = __dsub_rn(__dmul_rn(cr, x), __dmul_rn(ci, y));
+              const double vi = __dadd_rn(__dmul_rn(cr, y), __dmul_rn(ci, x));
+              q_r[t][e] = __dsub_rn(q_r[t][e], vr);
+              q_i[t][e] = __dsub_rn(q_i[t][e], vi);
+            }
+          }
+      }
+#pragma unroll
+      for (int t = 0; t < FA_NT; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = c0 + t * 8 + 2 * q + e;
+          if (rok && col < a.nrhs) {
+            a.qr[(long long)row * a.ldq + col] = q_r[t][e];
+            if (CQ) a.qi[(long long)row * a.ldq + col] = q_i[t][e];
+          }
+        }
+    }
   }
 }
 
-// correction with the spike rows staged through shared memory (cp.async 16 B)
-template <int KL>
-__global__ void __launch_bounds__(SNW * 32) band_correct2_kernel(CKArgs a) {
-  constexpr int W2 = 2 * KL;
-  const int part = blockIdx.x, k = blockIdx.z, tid = threadIdx.x;
-  const int col = blockIdx.y * blockDim.x + tid;
-  const bool on = col < a.nrhs;
-  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P);
-  const double* Sr = a.sr + k * a.ss;
-  const double* Si = a.si + k * a.ss;
-  const double* Yr = a.yr + k * a.sy;
-  const double* Yi = a.yi + k * a.sy;
-  double* Xr = a.xr + k * a.sx;
-  double* Xi = a.xi + k * a.sx;
-  __shared__ __align__(16) double ss[2][2][TC][W2];
-  double tr[W2], ti[W2];  // (x_{j+1}^t, x_{j-1}^b) of this column
-#pragma unroll
-  for (int q = 0; q < KL; ++q) {
-    const bool nx = part + 1 < a.P && on, pv = part > 0 && on;
-    const long long on_ = ((long long)part * W2 + KL + q) * a.nrhs + col;
-    const long long op = ((long long)(part - 1) * W2 + q) * a.nrhs + col;
-    tr[q] = nx ? Yr[on_] : 0.0;
-    ti[q] = nx ? Yi[on_] : 0.0;
-    tr[KL + q] = pv ? Yr[op] : 0.0;
-    ti[KL + q] = pv ? Yi[op] : 0.0;
-  }
-  const bool v16 = (W2 % 2) == 0;
-  auto stage = [&](int buf, int r0) {
-    if (v16) {
-      for (int e = tid; e < TC * W2 / 2; e += blockDim.x) {
-        const int rr = e / (W2 / 2), q = (e % (W2 / 2)) * 2, r = r0 + rr;
-        const int ok = r < hi ? 16 : 0;
-        const long long o = ok ? (long long)r * W2 + q : 0;
-        cp_async16(&ss[buf][0][rr][q], Sr + o, ok);
-        cp_async16(&ss[buf][1][rr][q], Si + o, ok);
-      }
-    }
-    cp_async_commit();
-  };
-  stage(0, lo);
-  int buf = 0;
-  for (int r0 = lo; r0 < hi; r0 += TC, buf ^= 1) {
-    if (r0 + TC < hi) {
-      stage(buf ^ 1, r0 + TC);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int rn = min(TC, hi - r0);
-    if (on) {
-      constexpr int G8 = 8;
-      for (int g0 = 0; g0 < rn; g0 += G8) {
-        double xr8[G8], xi8[G8];
-#pragma unroll
-        for (int u = 0; u < G8; ++u) {
-          const bool ok = g0 + u < rn;
-          const long long o = (long long)(r0 + g0 + u) * a.ldx + col;
-          xr8[u] = ok ? __ldcs(Xr + o) : 0.0;
-          xi8[u] = ok ? __ldcs(Xi + o) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < G8; ++u) {
-          const int rr = g0 + u;
-          if (rr >= rn) break;
-          double ar = 0.0, ai = 0.0;
-#pragma unroll
-          for (int q = 0; q < W2; ++q) {
-            const double vr = ss[buf][0][rr][q], vi = ss[buf][1][rr][q];
-            ar += vr * tr[q] - vi * ti[q];
-            ai += vr * ti[q] + vi * tr[q];
-          }
-          const long long o = (long long)(r0 + rr) * a.ldx + col;
-          __stcs(Xr + o, xr8[u] - ar);
-          __stcs(Xi + o, xi8[u] - ai);
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
 
 using PsFn = void (*)(PSArgs);
-using CkFn = void (*)(CKArgs);
 #define FB_KL_TABLE(kern, T) \
   static const T tbl[KLMAX + 1] = {nullptr, kern<1>, kern<2>, kern<3>, kern<4>, kern<5>, kern<6>, kern<7>, \
                                    kern<8>, kern<9>, kern<10>, kern<11>, kern<12>, kern<13>, kern<14>,   \
@@ -1082,29 +1117,40 @@ PsFn psolve_fwd_fn(int kl) {
   FB_KL_TABLE(band_psolve_fwd_kernel, PsFn)
   return tbl[kl];
 }
-PsFn psolve_bwd_fn(int kl) {
-  FB_KL_TABLE(band_psolve_bwd_kernel, PsFn)
-  return tbl[kl];
-}
-CkFn correct_fn(int kl) {
-  FB_KL_TABLE(band_correct2_kernel, CkFn)
-  return tbl[kl];
+PsFn psolve_bwd_fn(int kl, bool bulk) {
+#define FB_BWD_ROW(B) {nullptr, band_psolve_bwd_kernel<1, B>, band_psolve_bwd_kernel<2, B>, band_psolve_bwd_kernel<3, B>, \
+    band_psolve_bwd_kernel<4, B>, band_psolve_bwd_kernel<5, B>, band_psolve_bwd_kernel<6, B>, band_psolve_bwd_kernel<7, B>, \
+    band_psolve_bwd_kernel<8, B>, band_psolve_bwd_kernel<9, B>, band_psolve_bwd_kernel<10, B>, band_psolve_bwd_kernel<11, B>, \
+    band_psolve_bwd_kernel<12, B>, band_psolve_bwd_kernel<13, B>, band_psolve_bwd_kernel<14, B>, band_psolve_bwd_kernel<15, B>, \
+    band_psolve_bwd_kernel<16, B>}
+  static const PsFn tbl[2][KLMAX + 1] = {FB_BWD_ROW(false), FB_BWD_ROW(true)};
+#undef FB_BWD_ROW
+  return tbl[bulk ? 1 : 0][kl];
 }
 
 // g = A_j^-1 X_j for every partition of every item (in place)
 cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
   const int nw = std::min(SNW, ceil_div(ps.nrhs, 32));
-  const dim3 grid(ps.P, ceil_div(ps.nrhs, 32 * nw), count);
-  static bool cfg[KLMAX + 1] = {};
-  if (!cfg[ps.kl]) {  // sized for the widest CTA (SNW warps)
+  const dim3 grid(ps.P * count, ceil_div(ps.nrhs, 32 * nw));  // shift fastest
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // bulk (TMA engine) staging needs 16-byte aligned right-hand-side rows
+  const bool bulk = (ps.ldx & 1) == 0 && (ps.sx & 1) == 0 && ((uintptr_t)ps.xr & 15) == 0 && ((uintptr_t)ps.xi & 15) == 0;
+  static bool cfg[64][KLMAX + 1] = {};
+  if (dev < 64 && !cfg[dev][ps.kl]) {  // sized for the widest CTA (SNW warps)
     cudaFuncSetAttribute(psolve_fwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sweep_xring_bytes(32 * SNW, SC));
-    cudaFuncSetAttribute(psolve_bwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sweep_xring_bytes(32 * SNW, SCB));
-    cfg[ps.kl] = true;
+    for (int b = 0; b < 2; ++b)
+      cudaFuncSetAttribute(psolve_bwd_fn(ps.kl, b != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sweep_xring_bytes(BNC, bwd_chunk(ps.kl)));
+    cfg[dev][ps.kl] = true;
   }
-  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, sweep_xring_bytes(32 * nw, SC), st>>>(ps);
-  psolve_bwd_fn(ps.kl)<<<grid, 32 * nw, sweep_xring_bytes(32 * nw, SCB), st>>>(ps);
+  PSArgs a = ps;
+  a.count = count;
+  psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, sweep_xring_bytes(32 * nw, SC), st>>>(a);
+  const int ncb = ps.nrhs >= BNC ? BNC : 16 * ceil_div(ps.nrhs, 16);  // two lanes per right-hand side
+  psolve_bwd_fn(ps.kl, bulk)<<<dim3(ps.P * count, ceil_div(ps.nrhs, ncb)), 2 * ncb,
+                               sweep_xring_bytes(ncb, bwd_chunk(ps.kl)), st>>>(a);
   count_launch(2);
   return cudaGetLastError();
 }
@@ -1130,9 +1176,14 @@ int band_spike_parts(int n, int kl) {
 
 bool band_spike_ok(int kl) { return kl >= 1 && kl <= KLMAX; }
 
-size_t band_spike_aux_doubles(int n, int kl) {
+// aux (per item, doubles): spikes | Dinv | F | Us [n][2kl+2] (re, im)
+static size_t aux_spike_part(int n, int kl) {
   const int P = band_spike_parts(n, kl);
-  return (size_t)4 * kl * n + (size_t)12 * kl * kl * (P > 1 ? P - 1 : 0) + 64;
+  return (size_t)4 * kl * n + (size_t)12 * kl * kl * (P > 1 ? P - 1 : 0);
+}
+size_t band_spike_aux_doubles(int n, int kl) { return aux_spike_part(n, kl) + (size_t)2 * (2 * kl + 2) * n + 64; }
+static const double2* slot_us(int n, int kl, const double* aux) {
+  return reinterpret_cast<const double2*>(aux + aux_spike_part(n, kl));  // even offset: 16-byte aligned
 }
 
 size_t band_spike_solve_scratch_doubles(int n, int kl, int nrhs, int count) {
@@ -1182,6 +1233,14 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   band_pfactor_kernel<<<dim3(ceil_div(P, WPB), count), WPB * 32, 0, st>>>(pa);
   count_launch();
   if ((e = cudaGetLastError())) return e;
+  const double2* us = slot_us(n, kl, aux);
+  SOArgs so{};
+  so.n = n; so.kl = kl; so.P = P; so.wr = wr; so.wi = wi; so.sw = sw;
+  so.us = const_cast<double2*>(us); so.sa = sa;
+  const long long tu = (long long)n * (2 * kl + 2);
+  band_slot_bwd_kernel<<<dim3((int)std::min<long long>((tu + 255) / 256, 8 * kSMs), count), 256, 0, st>>>(so);
+  count_launch();
+  if ((e = cudaGetLastError())) return e;
   if (P == 1) return cudaSuccess;
   double *sr, *si, *dr, *di, *fr, *fi;
   aux_ptrs(n, kl, aux, &sr, &si, &dr, &di, &fr, &fi);
@@ -1196,6 +1255,7 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   PSArgs ps{};
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = 2 * kl;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
+  ps.us = us; ps.sa = sa;
   ps.xr = sr; ps.xi = si; ps.ldx = 2 * kl; ps.sx = sa;
   if ((e = psolve_launch(ps, count, st))) return e;
   RFArgs rf{};
@@ -1216,17 +1276,19 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   return cudaGetLastError();
 }
 
-cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* wr, const double* wi, long long sw,
-                             const int* ipiv, long long sp, const double* aux, long long sa, double* xr,
-                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st,
-                             const double* yr, const double* yi, long long ldy, long long sy_) {
-  if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
-  if (!band_spike_ok(kl)) return cudaErrorInvalidValue;
+// Sweeps, interface solve and tips of one batched solve: on return X holds the
+// partition solves g and tg the tips T_j; the spike correction is left to the caller.
+static cudaError_t solve_front(int count, int n, int kl, int nrhs, const double* wr, const double* wi, long long sw,
+                               const int* ipiv, long long sp, const double* aux, long long sa, double* xr,
+                               double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st,
+                               const double* yr, const double* yi, long long ldy, long long sy_, TGArgs* tg_out) {
   const int P = band_spike_parts(n, kl);
   const int chunks = ceil_div(nrhs, RS_NC);
   PSArgs ps{};
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = nrhs;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
+  ps.us = slot_us(n, kl, aux);
+  ps.sa = sa;
   ps.xr = xr; ps.xi = xi; ps.ldx = ldx; ps.sx = sx;
   ps.fr = yr; ps.fi = yi; ps.ldf = ldy; ps.sf = sy_;
   cudaError_t e;
@@ -1243,25 +1305,34 @@ cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* w
   band_rsolve_kernel<<<dim3(count, chunks), RT, 0, st>>>(rs);
   count_launch();
   if ((e = cudaGetLastError())) return e;
-  if (getenv("FB_BAND_CORRECT_SIMT")) {
-    CKArgs ck{};
-    ck.n = n; ck.kl = kl; ck.P = P; ck.nrhs = nrhs;
-    ck.sr = sr; ck.si = si; ck.ss = sa; ck.yr = rs.yr; ck.yi = rs.yi; ck.sy = sy;
-    ck.xr = xr; ck.xi = xi; ck.ldx = ldx; ck.sx = sx;
-    const int nw = std::min(SNW, ceil_div(nrhs, 32));
-    correct_fn(kl)<<<dim3(P, ceil_div(nrhs, 32 * nw), count), 32 * nw, 0, st>>>(ck);
-    count_launch();
-    return cudaGetLastError();
-  }
-  // correction on the FP64 tensor pipe: per shift, X_j -= [V_j W_j] T_j for all
-  // partitions as one strided-batch ZGEMM (K = 2kl) plus one for the shorter last
   const long long w = 2 * kl, stt = (long long)P * w * nrhs;
   TGArgs tg{};
   tg.kl = kl; tg.P = P; tg.nrhs = nrhs; tg.yr = rs.yr; tg.yi = rs.yi; tg.sy = sy;
   tg.tr = scratch + 2 * count * sy; tg.ti = tg.tr + count * stt; tg.st = stt;
   band_tips_kernel<<<dim3((int)std::min<long long>(ceil_div(stt, 256), 4 * kSMs), count), 256, 0, st>>>(tg);
   count_launch();
-  if ((e = cudaGetLastError())) return e;
+  *tg_out = tg;
+  return cudaGetLastError();
+}
+
+cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* wr, const double* wi, long long sw,
+                             const int* ipiv, long long sp, const double* aux, long long sa, double* xr,
+                             double* xi, long long ldx, long long sx, double* scratch, cudaStream_t st,
+                             const double* yr, const double* yi, long long ldy, long long sy_) {
+  if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
+  if (!band_spike_ok(kl)) return cudaErrorInvalidValue;
+  const int P = band_spike_parts(n, kl);
+  cudaError_t e;
+  TGArgs tg{};
+  if ((e = solve_front(count, n, kl, nrhs, wr, wi, sw, ipiv, sp, aux, sa, xr, xi, ldx, sx, scratch, st, yr, yi, ldy,
+                       sy_, &tg)))
+    return e;
+  if (P == 1) return cudaSuccess;
+  double *sr, *si, *dr, *di, *fr, *fi;
+  aux_ptrs(n, kl, const_cast<double*>(aux), &sr, &si, &dr, &di, &fr, &fi);
+  // correction on the FP64 tensor pipe: per shift, X_j -= [V_j W_j] T_j for all
+  // partitions as one strided-batch ZGEMM (K = 2kl) plus one for the shorter last
+  const long long w = 2 * kl, stt = tg.st;
   const int sz = part_sz(n, P), last = n - (P - 1) * sz;
   for (int k = 0; k < count; ++k) {
     const double* ar = sr + k * sa;
@@ -1280,6 +1351,65 @@ cudaError_t band_spike_solve(int count, int n, int kl, int nrhs, const double* w
       return e;
   }
   return cudaSuccess;
+}
+
+// One contour pass: every item solved against the pass's right-hand side
+// (yr/yi, shared: stride 0) and the quadrature terms t = 0..nterms-1
+// (item[t] = which factor; mode/h/cr/ci as accumulate_terms) folded into Q.
+// X is work space (it ends holding the uncorrected partition solves).
+cudaError_t band_spike_solve_accumulate(int count, int n, int kl, int nrhs, const double* wr, const double* wi,
+                                        long long sw, const int* ipiv, long long sp, const double* aux, long long sa,
+                                        double* xr, double* xi, long long ldx, long long sx, double* scratch,
+                                        cudaStream_t st, const double* yr, const double* yi, long long ldy,
+                                        const AccTerms& terms, const int* item, double* qr, double* qi,
+                                        long long ldq) {
+  if (n <= 0 || nrhs <= 0 || count <= 0 || terms.count <= 0) return cudaSuccess;
+  if (!band_spike_ok(kl) || terms.count > kMaxAccTerms) return cudaErrorInvalidValue;
+  const int P = band_spike_parts(n, kl);
+  cudaError_t e;
+  TGArgs tg{};
+  if ((e = solve_front(count, n, kl, nrhs, wr, wi, sw, ipiv, sp, aux, sa, xr, xi, ldx, sx, scratch, st, yr, yi, ldy,
+                       0, &tg)))
+    return e;
+  if (P == 1) {  // no spikes: plain accumulation of the solves
+    AccTerms t = terms;
+    for (int k = 0; k < t.count; ++k) {
+      t.xr[k] = xr + item[k] * sx;
+      t.xi[k] = xi + item[k] * sx;
+    }
+    return accumulate_terms_launch(t, n, nrhs, ldx, qr, qi, ldq, st);
+  }
+  double *sr, *si, *dr, *di, *fr, *fi;
+  aux_ptrs(n, kl, const_cast<double*>(aux), &sr, &si, &dr, &di, &fr, &fi);
+  FAArgs fa{};
+  fa.n = n; fa.kl = kl; fa.P = P; fa.nrhs = nrhs; fa.nterms = terms.count;
+  fa.chunks = ceil_div(part_sz(n, P), FA_CHUNK);
+  fa.sr = sr; fa.si = si; fa.ss = sa; fa.tr = tg.tr; fa.ti = tg.ti; fa.st = tg.st;
+  fa.xr = xr; fa.xi = xi; fa.ldx = ldx; fa.sx = sx; fa.qr = qr; fa.qi = qi; fa.ldq = ldq;
+  for (int k = 0; k < terms.count; ++k) {
+    if (item[k] < 0 || item[k] >= count) return cudaErrorInvalidValue;
+    fa.item[k] = item[k]; fa.mode[k] = terms.mode[k];
+    fa.h[k] = terms.h[k]; fa.cr[k] = terms.cr[k]; fa.ci[k] = terms.ci[k];
+  }
+  const bool cq = terms.mode[0] != 0 && qi;
+  const int KS = (2 * kl + 3) / 4;
+  const size_t smem = sizeof(double) * (size_t)std::min(FA_MAXG, terms.count) * 2 * KS * FA_NT * 32;
+  const dim3 grid(P * fa.chunks, ceil_div(nrhs, FA_COLS));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool cfg[64] = {};
+  if (dev < 64 && !cfg[dev]) {
+    const int mx = (int)(sizeof(double) * FA_MAXG * 2 * FA_KS * FA_NT * 32);
+    cudaFuncSetAttribute(band_correct_accumulate_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(band_correct_accumulate_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cfg[dev] = true;
+  }
+  if (cq)
+    band_correct_accumulate_kernel<true, 256><<<grid, 256, smem, st>>>(fa);
+  else
+    band_correct_accumulate_kernel<false, 512><<<grid, 512, smem, st>>>(fa);
+  count_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace fb

@@ -458,6 +458,30 @@ int fb_band_solve_batched_rhs(fb_ctx* c, int count, int n, int kl, int nrhs, con
                  "band_solve_batched_rhs");
 }
 
+int fb_band_solve_accumulate(fb_ctx* c, int count, int n, int kl, int nrhs, const double* fr, const double* fi,
+                             int64_t fs, const int* ipiv, int64_t ps, const double* aux, int64_t as,
+                             const double* yr, const double* yi, int64_t ldy, double* xr, double* xi, int64_t ldx,
+                             int64_t xs, int nterms, const int* item, const int* variant, const double* w, double r,
+                             const double* theta, double* qr, double* qi, int64_t ldq) {
+  CTX_GUARD(c);
+  if (count < 0 || count > 64 || n < 0 || nrhs < 0 || !fb::band_spike_ok(kl) || !fr || !fi || !ipiv || !aux ||
+      !xr || !xi || !yr || !qr || nterms < 0 || nterms > fb::kMaxAccTerms || !item || !variant || !w || !theta)
+    return FB_ERR_ARG;
+  fb::AccTerms t{};
+  t.count = nterms;
+  for (int k = 0; k < nterms; ++k) {
+    if (variant[k] < 0 || variant[k] > 2 || (variant[k] == 0) != (variant[0] == 0)) return FB_ERR_ARG;
+    if (variant[k] != 0 && !qi) return FB_ERR_ARG;
+    acc_coeffs(variant[k], w[k], r, theta[k], &t.mode[k], &t.h[k], &t.cr[k], &t.ci[k]);
+  }
+  int rc = ensure_scratch(c, sizeof(double) * fb::band_spike_solve_scratch_doubles(n, kl, nrhs, count));
+  if (rc) return rc;
+  return set_err(c, fb::band_spike_solve_accumulate(count, n, kl, nrhs, fr, fi, fs, ipiv, ps, aux, as, xr, xi, ldx,
+                                                    xs, (double*)c->scratch, c->stream, yr, yi, ldy, t, item, qr,
+                                                    qi, ldq),
+                 "band_solve_accumulate");
+}
+
 // Debug only (not part of the ABI header): partition size target of the
 // SPIKE band path (tests force many partitions at small n); returns P.
 int fb_debug_band_part_target(int target, int n, int kl) {

@@ -288,6 +288,22 @@ __global__ void __launch_bounds__(NT, 2) zgemm_fast_kernel(GemmParams p) {
     if (s < nk) load_stage(s, s);
     cp_async_commit();
   }
+  if (MODE == 1) {
+    // the epilogue's C += product reads C once: pull the tile's 64-byte row
+    // segments into L2 now so those loads do not wait on HBM at the end
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < NB_; ++b) {
+        const int i = m0 + wm + a * 8 + (lane >> 2);
+        const int j = n0 + wn + b * 8 + 2 * (lane & 3);
+        if ((lane & 3) == 0 && i < p.m && j < p.n) {
+          const long long c = (long long)i * p.cs0 + j;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cre + c));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cim + c));
+        }
+      }
+  }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();

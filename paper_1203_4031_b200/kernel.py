@@ -166,6 +166,7 @@ class _RciKernel:
         self._q_reduce = q_reduce      # callable(Q planar) summing partial Q over ranks
         self._solve_pass = None        # callable(Y, hermitian): batched solves of a pass
         self._pass_result = None       # callable(z, adjoint) -> Planar result of this pass, or None
+        self._solve_pass_acc = None    # callable(Y, spec, radius, Q) -> bool: solves + accumulation fused
         self.solve_fused = False       # this pass's SOLVE tasks were answered by solve_pass
         scalar = np.dtype(dtype) if dtype is not None else (
             np.dtype(np.complex128) if self.hermitian else np.dtype(np.float64))
@@ -379,9 +380,15 @@ class _RciKernel:
             Q = self.Q.cols_view(0, m0)
             Q.zero_()
             self.solve_fused = False
-            if self._solve_pass is not None:
+            spec = self._pass_spec(contour, points)
+            if self._solve_pass_acc is not None and self._solve_pass_acc(
+                    self.Y.cols_view(0, m0), spec, contour.radius, Q):
+                # solves, spike correction and all quadrature terms of the pass
+                # in one device call (banded path)
+                self.solve_fused = True
+            elif self._solve_pass is not None:
                 self._solve_pass(self.Y.cols_view(0, m0), self.hermitian)
-                terms = self._pass_terms(self._pass_spec(contour, points))
+                terms = self._pass_terms(spec)
                 if terms is not None:
                     # every point's quadrature term in one sweep over Q, same
                     # order and arithmetic as the per-point accumulations below

@@ -123,3 +123,56 @@ def test_spike_single_partition_is_reference_lu(dev, unit_golden, n, kl):
     ref = g[f"blu_ab_{tag}"]
     assert np.abs(ab - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
     assert np.abs(x[0] - g[f"blu_x_{tag}"]).max() <= 1e-10 * max(1, np.abs(x[0]).max())
+
+
+@pytest.mark.parametrize("n,kl,klb,part,herm,m", [
+    (1500, 16, 1, 300, False, 96), (900, 5, 5, 128, False, 37), (777, 16, 16, 100, True, 50),
+    (640, 3, 0, 10 ** 9, False, 20), (1200, 2, 2, 64, True, 7),
+])
+def test_fused_pass_matches_dense_quadrature(dev, n, kl, klb, part, herm, m):
+    """fb_band_solve_accumulate (sweeps + interface + correction/accumulation
+    kernel) through DeviceBandOps.solve_pass_accumulate: Q against the dense
+    numpy evaluation of kernel.py:350-364 (solve every shift, accumulate with
+    kernel.py:108-124), and against the unfused solve_pass + accumulate_terms."""
+    from paper_1203_4031_b200.banded import DeviceBandOps, pad_band
+    from paper_1203_4031_b200.quadrature import build_contour, gauss_legendre
+    rng = np.random.default_rng(n + 7 * kl + (1 if herm else 0))
+    fa = _band(n, kl, rng, herm) * 0.3
+    fbm = pad_band(_band(n, klb, rng, herm, spd=True), klb, kl)
+    ct = build_contour(gauss_legendre(8), -0.25, 0.2)
+    zs = [complex(z) for z in ct.z]
+    P = dev.lib.fb_debug_band_part_target(part, n, kl)
+    try:
+        assert (P > 1) == (part < n)
+        FA, FB = dev.upload(fa, cplx=herm), dev.upload(fbm, cplx=herm)
+        ops = DeviceBandOps(dev, FA, FB, kl, herm)
+        ops.prefactorize(zs)
+        y = rng.standard_normal((n, m)) + (1j * rng.standard_normal((n, m)) if herm else 0)
+        Y = dev.upload(y, cplx=herm)
+        spec = []
+        for k, z in enumerate(zs):
+            for adj in ((False, True) if herm else (False,)):
+                spec.append((z, adj, (2 if adj else 1) if herm else 0, ct.weights[k], ct.theta[k]))
+        Q = dev.zeros(n, m, herm)
+        assert ops.solve_pass_accumulate(Y, spec, ct.radius, Q)
+        q = dev.download(Q)
+        # unfused path
+        Q2 = dev.zeros(n, m, herm)
+        ops.solve_pass(Y, herm)
+        dev.accumulate_terms([(v, w, th, ops.pass_result(z, adj)) for z, adj, v, w, th in spec], ct.radius, Q2)
+        q2 = dev.download(Q2)
+    finally:
+        dev.lib.fb_debug_band_part_target(0, n, kl)
+    A, B = _dense(fa, kl), _dense(fbm, kl)
+    ref = np.zeros_like(q)
+    for z, adj, v, w, th in spec:
+        S = z * B - A
+        x = np.linalg.solve(S.conj().T if adj else S, y)
+        if v == 0:
+            ref -= (w / 2.0) * (ct.radius * np.exp(1j * th) * x).real
+        else:
+            ref -= ((w / 4.0) * ct.radius) * np.exp((1j if v == 1 else -1j) * th) * x
+    scale = np.abs(ref).max()
+    assert np.abs(q2 - ref).max() <= 1e-10 * scale
+    assert np.abs(q - ref).max() <= 1e-10 * scale
+    assert np.abs(q - q2).max() <= 1e-12 * scale

@@ -73,7 +73,9 @@ def _check(r, g, name):
     if info in (0, 2, 3) and m:
         assert np.abs(r.e[:m] - g[f"{name}__e"][:m]).max() <= 1e-10 * s, name
         if info == 0:
-            assert np.max(r.res[:m]) <= 1e-10
+            # the residual bar is 1e-10, or the reference's own residual where
+            # its converged run ends above that (sbev200_L: 1.63e-10 at info 0)
+            assert np.max(r.res[:m]) <= max(1e-10, 1.5 * float(np.max(g[f"{name}__res"][:m])))
 
 
 def test_feastlib_run_rci_with_b200_ops_small_goldens(fl, small_golden):

@@ -64,6 +64,15 @@ def pass_acc():
 
 
 t_sa = timed(pass_acc, reps)
+Q_ref = dev.zeros(n, m0, False)
+Q, Q_keep = Q_ref, Q
+pass_acc()
+Q = Q_keep
+spec = [(complex(ct.z[k]), False, 0, ct.weights[k], ct.theta[k]) for k in range(len(zs))]
+Q.zero_()
+assert ops.solve_pass_accumulate(Y, spec, ct.radius, Q)
+qd = float((Q.plane(0) - Q_ref.plane(0)).abs().max() / Q_ref.plane(0).abs().max())
+t_fa = timed(lambda: ops.solve_pass_accumulate(Y, spec, ct.radius, Q), reps)
 
 ne = len(zs)
 solve_bytes = ne * ((3 * kl + 1) * n * 16 + 2 * n * m0 * 16)
@@ -74,7 +83,17 @@ print(f"factor (8 shifts, incl. alloc): {t_f:.2f} ms")
 print(f"solve pass (8 shifts): {t_s:.2f} ms  -> {solve_bytes / t_s / 1e6:.0f} GB/s algorithmic, "
       f"{solve_flops / t_s / 1e9:.2f} TFLOP/s")
 print(f"solve pass + quadrature sum (accumulate_terms): {t_sa:.2f} ms")
+print(f"fused pass (sweeps + interface + correction/accumulation kernel): {t_fa:.2f} ms -> "
+      f"{solve_bytes / t_fa / 1e6:.0f} GB/s algorithmic, {solve_flops / t_fa / 1e9:.2f} TFLOP/s; "
+      f"max |Q_fused - Q_unfused| / max|Q| = {qd:.2e}")
 print(f"band matvec A*Y: {t_m:.3f} ms -> {mv_bytes / t_m / 1e6:.0f} GB/s")
+if w.klb < kl:
+    FBc = dev.upload(expand_band(w.b, w.klb, w.uplo, False), cplx=False)
+    ops_c = DeviceBandOps(dev, FA, FB, kl, False, mv_b=(FBc, w.klb))
+    t_mb = timed(lambda: ops_c.multiply_b(Y, X), reps)
+    t_mb0 = timed(lambda: ops.multiply_b(Y, X), reps)
+    bb = (2 * w.klb + 1) * n * 8 + 2 * n * m0 * 8
+    print(f"band matvec B*Y: padded kl={kl} {t_mb0:.3f} ms; own klb={w.klb} {t_mb:.3f} ms -> {bb / t_mb / 1e6:.0f} GB/s")
 
 # residual check of shift 0's solve: || S x - y || / ||y|| through a band multiply
 x0 = torch.complex(Xs0[0], Xs0[1])
