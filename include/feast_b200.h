@@ -149,6 +149,13 @@ int fb_symmetrize(fb_ctx* ctx, int m, double* re, double* im, int64_t ld);
 int fb_residuals(fb_ctx* ctx, int n, int m, const double* ax_re, const double* ax_im,
                  const double* bx_re, const double* bx_im, int64_t ld,
                  const double* lam, double scale, double* res);
+/* The same sums without the division, for a ROW BLOCK of AX / BX (the
+ * multi-GPU path shards the rows of _column_residuals, kernel.py:147-153,
+ * over ranks and adds the blocks' sums with one all-reduce):
+ * sums[2j] = sum_i |AX_ij - lam_j BX_ij|, sums[2j+1] = sum_i |scale BX_ij|. */
+int fb_residual_sums(fb_ctx* ctx, int n, int m, const double* ax_re, const double* ax_im,
+                     const double* bx_re, const double* bx_im, int64_t ld,
+                     const double* lam, double scale, double* sums);
 
 /* Cholesky probe of the leading m x m block: *fail = 0 or the 1-based index of
  * the first non-positive pivot (spd_factor, reduced.py:22-40).  Synchronous. */

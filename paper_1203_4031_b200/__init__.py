@@ -31,6 +31,7 @@ _LAZY = {
     "B200DenseOps": "dense", "DeviceDenseOps": "dense", "feast_sb": "banded",
     "feast_hb": "banded", "B200BandOps": "banded", "DeviceBandOps": "banded",
     "feast_sy_distributed": "distributed", "feast_he_distributed": "distributed",
+    "feast_sb_distributed": "distributed", "feast_hb_distributed": "distributed",
     "feast_sy_intervals": "distributed", "feast_he_intervals": "distributed",
     "CsrMatrix": "sparse", "csr_matvec": "sparse", "feast_scsr": "sparse", "feast_hcsr": "sparse",
     "DeviceCsrOps": "sparse", "B200CsrOps": "sparse",
@@ -50,7 +51,8 @@ __all__ = [
     "DeviceBandOps", "DeviceDenseOps", "EigenResult", "FeastParams", "HermitianRci",
     "QuadratureRule", "RciTask", "ReducedSolverError", "SingularMatrixError", "SolverOptions",
     "SymmetricRci", "build_contour", "check_problem", "feast_hb", "feast_he", "feast_sb",
-    "feast_sy", "feast_sy_distributed", "feast_he_distributed", "feast_sy_intervals",
+    "feast_sy", "feast_sy_distributed", "feast_he_distributed", "feast_sb_distributed",
+    "feast_hb_distributed", "feast_sy_intervals",
     "feast_he_intervals", "feastinit", "gauss_legendre", "info_classification", "info_description",
     "run_rci", "validate_params", "CsrMatrix", "csr_matvec", "feast_scsr", "feast_hcsr", "DeviceCsrOps",
     "B200CsrOps",

@@ -46,6 +46,7 @@ SIGNATURES = {
                         c_int64, P, P, c_int64, c_double, c_double, P, P, c_int64]),
     "fb_symmetrize": (c_int, [P, c_int, P, P, c_int64]),
     "fb_residuals": (c_int, [P, c_int, c_int, P, P, P, P, c_int64, P, c_double, P]),
+    "fb_residual_sums": (c_int, [P, c_int, c_int, P, P, P, P, c_int64, P, c_double, P]),
     "fb_chol_check": (c_int, [P, c_int, P, P, c_int64, PI]),
     "fb_reduced_eig": (c_int, [P, c_int, P, P, P, P, c_int64, P, P, P, c_int64, PI]),
     "fb_pack": (c_int, [P, c_int, c_int, P, c_int64, P, P, c_int64, c_int]),

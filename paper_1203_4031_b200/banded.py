@@ -21,6 +21,10 @@ from .device import Planar, get_device
 from .kernel import HermitianRci, SymmetricRci
 from .params import feastinit, FeastParams
 
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
 _UPLOS = ("F", "L", "U")
 
 
@@ -64,7 +68,9 @@ def expand_band_device(dev, ab, kl: int, uplo: str, hermitian: bool, kl_to: int)
     triangle conjugated for Hermitian input) -- the same values as the host
     functions, bit for bit (banded.py:21-47, 181-187)."""
     torch = dev.torch
-    ab = np.asarray(ab)
+    on_dev = isinstance(ab, torch.Tensor)   # a band array already resident on the device
+    if not on_dev:
+        ab = np.asarray(ab)
     n = ab.shape[1]
     uplo = uplo.upper()
     off = kl_to - kl
@@ -73,11 +79,19 @@ def expand_band_device(dev, ab, kl: int, uplo: str, hermitian: bool, kl_to: int)
     # LAPACK band rows: 'F' 2kl+1 rows (diagonal in row kl); 'L' diagonal in
     # row 0, subdiagonals below; 'U' superdiagonals above the diagonal in row kl
     rows = list(range(2 * kl + 1)) if uplo == "F" else list(range(kl + 1))
-    src = np.ascontiguousarray(ab[rows[0]:rows[-1] + 1])
-    if hermitian:
+    if on_dev:
+        st = ab[rows[0]:rows[-1] + 1].to(dev.tdev)
+        if hermitian:
+            st = st.to(torch.complex128)
+            sp = [st.real, st.imag]
+        else:
+            sp = [(st.real if st.is_complex() else st).to(torch.float64)]
+    elif hermitian:
+        src = np.ascontiguousarray(ab[rows[0]:rows[-1] + 1])
         st = torch.from_numpy(src.astype(np.complex128, copy=False)).to(dev.tdev)
         sp = [st.real, st.imag]
     else:
+        src = np.ascontiguousarray(ab[rows[0]:rows[-1] + 1])
         st = torch.from_numpy(np.ascontiguousarray(src.real if np.iscomplexobj(src) else src,
                                                    dtype=np.float64)).to(dev.tdev)
         sp = [st]
@@ -161,6 +175,9 @@ class DeviceBandOps:
     bandwidths use the sequential per-shift kernels."""
 
     on_device = True
+    # bench.py instrumentation: when a list, (start, end, count) CUDA events recorded
+    # on the context stream around every batched factorization are appended to it.
+    factor_event_sink = None
 
     def __init__(self, dev, FA: Planar, FB: Planar | None, kl: int, hermitian: bool, cache_bytes=None,
                  mv_a=None, mv_b=None):
@@ -190,10 +207,17 @@ class DeviceBandOps:
         zi = (ctypes.c_double * cnt)(*[z.imag for z in zs])
         FA, FB = self.FA, self.FB
         fr, fi, fs, piv, ps, aux, as_ = bb.args()
+        sink = DeviceBandOps.factor_event_sink
+        if sink is not None:
+            ev = (dev.torch.cuda.Event(enable_timing=True), dev.torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         dev.check(dev.lib.fb_band_factor_batched(
             dev.h, cnt, n, kl, zr, zi, FA.re, FA.im, FB.re if FB is not None else None,
             FB.im if FB is not None else None, FA.ld, fr, fi, fs, piv, ps, aux, as_,
             bb.info.data_ptr()), "band_factor_batched")
+        if sink is not None:
+            ev[1].record()
+            sink.append((ev[0], ev[1], cnt))
         self.factorizations += cnt
         bad = (ctypes.c_int * cnt)()
         rc = dev.lib.fb_read_info_batched(dev.h, cnt, bb.info.data_ptr(), bad)
@@ -414,19 +438,22 @@ class B200BandOps:
         return self._mult(self._ops.multiply_b, x)
 
 
-def _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, hermitian, device=None):
+def _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, hermitian, device=None,
+                   engine_kwargs=None):
     options = options or SolverOptions()
     fpm = FeastParams.coerce(fpm) if fpm is not None else feastinit()
     uplo = (uplo or "F").upper()
-    a = np.asarray(a)
+    if not _is_torch(a):
+        a = np.asarray(a)
     n = a.shape[1] if a.ndim == 2 else 0
-    single = a.dtype in (np.float32, np.complex64)
+    single = str(a.dtype).endswith(("float32", "complex64"))
     scalar = (np.complex64 if single else np.complex128) if hermitian else (np.float32 if single else np.float64)
     t = ("C" if single else "Z") if hermitian else ("S" if single else "D")
     routine = f"{t}FEAST_{'HB' if hermitian else 'SB'}{'GV' if b is not None else 'EV'}"
     cls = HermitianRci if hermitian else SymmetricRci
     kernel = cls(n, m0, emin, emax, fpm, seed=options.seed, block_size=options.block_size,
-                 dtype=scalar, routine_name=routine, device=device, host_mirror=False)
+                 dtype=scalar, routine_name=routine, device=device, host_mirror=False,
+                 **(engine_kwargs or {}))
     if uplo not in _UPLOS:
         kernel.abort(-101)
         return kernel.result
@@ -437,7 +464,8 @@ def _banded_driver(a, kla, b, klb, emin, emax, m0, uplo, fpm, options, x0, hermi
         kernel.abort(-105)
         return kernel.result
     if b is not None:
-        b = np.asarray(b)
+        if not _is_torch(b):
+            b = np.asarray(b)
         if klb is None or not 0 <= klb <= max(n - 1, 0):
             kernel.abort(-106)
             return kernel.result

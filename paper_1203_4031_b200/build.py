@@ -34,9 +34,7 @@ def build(force=False, verbose=False):
     procs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, "_" + src.replace(".cu", ".o"))
-        cmd = ["nvcc", *[f for f in FLAGS if f != "-shared"], "-c", "-dc" if False else "-c",
-               os.path.join(CSRC, src), "-o", obj]
-        cmd = [c for i, c in enumerate(cmd) if not (c == "-c" and i > 0 and cmd[i - 1] == "-c")]
+        cmd = ["nvcc", *[f for f in FLAGS if f != "-shared"], "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     failed = []

@@ -375,11 +375,8 @@ cudaError_t band_matvec_launch(int n, int kl, int m, const double* fbr, const do
   if (kl >= 0 && kl <= 16 && (!cplx || yi != nullptr)) {
     const size_t smem = sizeof(double) * (cplx ? 2 : 1) * (2 * kl + 1) * MV_RT;
     const MvFn fn = cplx ? matvec_fn<true>(kl) : matvec_fn<false>(kl);
-    static bool cfg[2][17] = {};
-    if (!cfg[cplx][kl]) {
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cfg[cplx][kl] = true;
-    }
+    static DevOnce cfg[2][17];
+    if (cfg[cplx][kl].first()) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int nt = m >= 96 ? 96 : (m >= 64 ? 64 : 32);
     fn<<<dim3(ceil_div(n, MV_RT), ceil_div(m, nt)), nt, smem, st>>>(n, m, fbr, fbi, ldb, xr, xi, ldx, yr,
                                                                      cplx ? yi : nullptr, ldy);

@@ -16,7 +16,7 @@ cudaError_t band_solve_launch(int n, int kl, int nrhs, const double* wr, const d
 
 // partitioned (SPIKE) band LU / solve, batched over shifts (band_spike.cu)
 bool band_spike_ok(int kl);
-void band_spike_set_part_target(int t);  // 0: default (FB_BAND_PART or 4096)
+void band_spike_set_part_target(int t);  // 0: default (4096 rows)
 int band_spike_parts(int n, int kl);
 size_t band_spike_aux_doubles(int n, int kl);
 size_t band_spike_solve_scratch_doubles(int n, int kl, int nrhs, int count);

@@ -1132,18 +1132,15 @@ PsFn psolve_bwd_fn(int kl, bool bulk) {
 cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
   const int nw = std::min(SNW, ceil_div(ps.nrhs, 32));
   const dim3 grid(ps.P * count, ceil_div(ps.nrhs, 32 * nw));  // shift fastest
-  int dev = 0;
-  cudaGetDevice(&dev);
   // bulk (TMA engine) staging needs 16-byte aligned right-hand-side rows
   const bool bulk = (ps.ldx & 1) == 0 && (ps.sx & 1) == 0 && ((uintptr_t)ps.xr & 15) == 0 && ((uintptr_t)ps.xi & 15) == 0;
-  static bool cfg[64][KLMAX + 1] = {};
-  if (dev < 64 && !cfg[dev][ps.kl]) {  // sized for the widest CTA (SNW warps)
+  static DevOnce cfg[KLMAX + 1];
+  if (cfg[ps.kl].first()) {  // sized for the widest CTA (SNW warps)
     cudaFuncSetAttribute(psolve_fwd_fn(ps.kl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sweep_xring_bytes(32 * SNW, SC));
     for (int b = 0; b < 2; ++b)
       cudaFuncSetAttribute(psolve_bwd_fn(ps.kl, b != 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sweep_xring_bytes(BNC, bwd_chunk(ps.kl)));
-    cfg[dev][ps.kl] = true;
   }
   PSArgs a = ps;
   a.count = count;
@@ -1162,10 +1159,7 @@ int g_part_target = 0;
 void band_spike_set_part_target(int t) { g_part_target = t; }
 
 int band_spike_parts(int n, int kl) {
-  if (g_part_target == 0) {
-    const char* e = getenv("FB_BAND_PART");
-    g_part_target = e && atoi(e) > 0 ? atoi(e) : 4096;
-  }
+  if (g_part_target == 0) g_part_target = 4096;
   const int minsz = std::max(2 * kl + 1, std::min(64, g_part_target));
   int P = (n + g_part_target - 1) / g_part_target;
   P = std::min(P, std::max(1, n / std::max(1, minsz)));
@@ -1264,12 +1258,10 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   rf.dr = dr; rf.di = di; rf.fr = fr; rf.fi = fi; rf.sa = sa; rf.info = info;
   {
     const size_t rsm = sizeof(double) * 3 * 2 * (size_t)(2 * kl) * (2 * kl);
-    static bool rcfg = false;
-    if (!rcfg) {
+    static DevOnce rcfg;
+    if (rcfg.first())
       cudaFuncSetAttribute(band_rfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(sizeof(double) * 3 * 2 * (2 * KLMAX) * (2 * KLMAX)));
-      rcfg = true;
-    }
     band_rfactor_kernel<<<count, RT, rsm, st>>>(rf);
   }
   count_launch();
@@ -1395,14 +1387,11 @@ cudaError_t band_spike_solve_accumulate(int count, int n, int kl, int nrhs, cons
   const int KS = (2 * kl + 3) / 4;
   const size_t smem = sizeof(double) * (size_t)std::min(FA_MAXG, terms.count) * 2 * KS * FA_NT * 32;
   const dim3 grid(P * fa.chunks, ceil_div(nrhs, FA_COLS));
-  int dev = 0;
-  cudaGetDevice(&dev);
-  static bool cfg[64] = {};
-  if (dev < 64 && !cfg[dev]) {
+  static DevOnce cfg;
+  if (cfg.first()) {
     const int mx = (int)(sizeof(double) * FA_MAXG * 2 * FA_KS * FA_NT * 32);
     cudaFuncSetAttribute(band_correct_accumulate_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(band_correct_accumulate_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cfg[dev] = true;
   }
   if (cq)
     band_correct_accumulate_kernel<true, 256><<<grid, 256, smem, st>>>(fa);

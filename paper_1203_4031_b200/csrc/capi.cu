@@ -111,8 +111,7 @@ int fb_ctx_create(int device, void* stream, fb_ctx** out) {
   }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  if (!getenv("FB_NO_LOOKAHEAD") &&
-      cudaStreamCreateWithPriority(&c->lu.side, cudaStreamNonBlocking, hi) == cudaSuccess) {
+  if (cudaStreamCreateWithPriority(&c->lu.side, cudaStreamNonBlocking, hi) == cudaSuccess) {
     cudaEventCreateWithFlags(&c->lu.ev_s, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->lu.ev_p, cudaEventDisableTiming);
   } else {
@@ -337,6 +336,17 @@ int fb_residuals(fb_ctx* c, int n, int m, const double* axr, const double* axi, 
   return set_err(c, fb::residual_launch(n, m, axr, axi, bxr, bxi, ld, lam, scale, res,
                                         (double*)c->scratch, c->stream),
                  "residuals");
+}
+
+int fb_residual_sums(fb_ctx* c, int n, int m, const double* axr, const double* axi, const double* bxr,
+                     const double* bxi, int64_t ld, const double* lam, double scale, double* sums) {
+  CTX_GUARD(c);
+  if (n < 0 || m < 0 || !sums) return FB_ERR_ARG;
+  int r = ensure_scratch(c, fb::residual_scratch_bytes(n > 0 ? n : 1, m));
+  if (r) return r;
+  return set_err(c, fb::residual_sums_launch(n, m, axr, axi, bxr, bxi, ld, lam, scale, sums,
+                                             (double*)c->scratch, c->stream),
+                 "residual_sums");
 }
 
 int fb_chol_check(fb_ctx* c, int m, const double* bre, const double* bim, int64_t ld, int* fail) {

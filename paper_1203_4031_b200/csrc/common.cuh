@@ -56,6 +56,18 @@ enum : int {
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
+// One-shot per (call site, device): cudaFuncSetAttribute applies to the current
+// device only, and one process may drive several devices (get_device(index)).
+struct DevOnce {
+  std::atomic<unsigned long long> mask{0};
+  bool first() {  // true exactly once per device at this site
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long b = 1ull << (d & 63);
+    return !(mask.fetch_or(b, std::memory_order_acq_rel) & b);
+  }
+};
+
 // One FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).
 // Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
 // d0,d1 = D[lane>>2][2*(lane&3) + {0,1}].

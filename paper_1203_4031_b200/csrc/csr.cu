@@ -452,13 +452,17 @@ cudaError_t bicgstab_launch(int phase, int n, int m, const long long* indptr, co
     key.l[0] = ldb; key.l[1] = ldx; key.l[2] = ld;
     key.tol = tol;
     key.i[0] = n; key.i[1] = m; key.i[2] = maxiter; key.i[3] = iters;
+    int cur_dev = 0;
+    cudaGetDevice(&cur_dev);
+    key.i[4] = cur_dev;  // graphs and the capture stream belong to one device
     struct Entry {
       Key k;
       cudaGraphExec_t exec;
     };
     static std::vector<Entry> cache;
     static std::mutex mu;
-    static cudaStream_t cap = nullptr;
+    static cudaStream_t caps[64] = {};
+    cudaStream_t& cap = caps[cur_dev & 63];
     std::lock_guard<std::mutex> lock(mu);
     cudaGraphExec_t exec = nullptr;
     for (auto& e : cache)

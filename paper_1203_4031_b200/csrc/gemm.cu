@@ -410,11 +410,10 @@ cudaError_t launch_t(const GemmParams& p, cudaStream_t st) {
   constexpr int PL = CPLX ? 2 : 1;
   size_t smem = sizeof(double) * STAGES * PL * (ATile<AKC>::kElems + ATile<!BNC>::kElems);
   auto kern = gemm_kernel<CPLX, AKC, BNC>;
-  static bool configured = false;  // attribute set once per instantiation
-  if (!configured) {
+  static DevOnce configured;  // attribute set once per instantiation and device
+  if (configured.first()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.splits * p.batch);
   kern<<<grid, THREADS, smem, st>>>(p);
@@ -440,18 +439,12 @@ bool fast_ok(const GemmParams& p) {
 cudaError_t launch_fast(const GemmParams& p, cudaStream_t st) {
   const size_t smem = sizeof(double) * STAGES * 2 * (ATile<true>::kElems + ATile<false>::kElems);
   const bool mode1 = p.alpha_re == -1.0 && p.alpha_im == 0.0 && p.beta_re == 1.0 && p.beta_im == 0.0;
-  static int nt = 0;
-  if (!nt) {
-    const char* e = getenv("FB_ZGEMM_THREADS");
-    nt = (e && atoi(e) == 128) ? 128 : 256;
-  }
-  auto kern = mode1 ? (nt == 128 ? zgemm_fast_kernel<1, 128> : zgemm_fast_kernel<1, 256>)
-                    : (nt == 128 ? zgemm_fast_kernel<0, 128> : zgemm_fast_kernel<0, 256>);
-  static bool configured[2] = {false, false};
-  if (!configured[mode1]) {
+  constexpr int nt = 256;
+  auto kern = mode1 ? zgemm_fast_kernel<1, 256> : zgemm_fast_kernel<0, 256>;
+  static DevOnce configured[2];
+  if (configured[mode1].first()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured[mode1] = true;
   }
   dim3 grid(ceil_div(p.n, BN), ceil_div(p.m, BM), p.batch);
   kern<<<grid, nt, smem, st>>>(p);

@@ -38,15 +38,8 @@ namespace fb {
 namespace {
 
 constexpr int PW = 32;                 // sub-panel width (= diagonal block size of dinv)
-static int outer_nb() {                // outer block (trailing-update K), FB_LU_NB overrides
-  static int nb = 0;
-  if (!nb) {
-    const char* e = getenv("FB_LU_NB");
-    nb = e ? atoi(e) : 256;  // 256: +3 % over 128 at N = 4096 and 8192 (profiles/r01_lu_nb_rpc_sweep.txt)
-    if (nb < 32 || nb % 32) nb = 256;
-  }
-  return nb;
-}
+// outer block (trailing-update K): 256 is +3 % over 128 at N = 4096 and 8192 (profiles/r01_lu_nb_rpc_sweep.txt)
+static int outer_nb() { return 256; }
 constexpr int LIST = 1 + 2 * 2 * PW;   // per-block swap list: cnt, dst[2PW], src[2PW]
 
 // S_b = z_b B - A (B == nullptr: identity); item b = blockIdx.y.
@@ -396,11 +389,8 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
   }
   // composed permutation and the sweeps' diagonal-block operators for the solves
   size_t psmem = sizeof(int) * (size_t)n;
-  static bool pcfg = false;
-  if (!pcfg) {
-    cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    pcfg = true;
-  }
+  static DevOnce pcfg;
+  if (pcfg.first()) cudaFuncSetAttribute(perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (psmem > 200 * 1024) return cudaErrorInvalidValue;
   perm_kernel<<<B, 256, psmem, st>>>(n, lists, const_cast<int*>(factor_perm(f.dinv, n)), 2 * sd);
   count_launch();

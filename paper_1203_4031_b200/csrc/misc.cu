@@ -8,6 +8,8 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include <algorithm>
+
 #include "misc.cuh"
 
 namespace fb {
@@ -185,6 +187,20 @@ __global__ void residual_final(int chunks, int m, const double* __restrict__ par
   res[j] = den > 0.0 ? num / den : __longlong_as_double(0x7ff0000000000000ll);
 }
 
+// (num, den) per column without the division: the row-sharded residual of the
+// multi-GPU path sums these over ranks first
+__global__ void residual_sums(int chunks, int m, const double* __restrict__ part, double* __restrict__ sums) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double num = 0.0, den = 0.0;
+  for (int c = 0; c < chunks; ++c) {
+    num += part[((size_t)c * m + j) * 2];
+    den += part[((size_t)c * m + j) * 2 + 1];
+  }
+  sums[2 * j] = num;
+  sums[2 * j + 1] = den;
+}
+
 // interleaved complex (n x m, ld in complex elements) <-> planar (ldp)
 __global__ void pack_kernel(int n, int m, const double* __restrict__ z, long long ldz,
                             double* __restrict__ re, double* __restrict__ im, long long ldp,
@@ -269,6 +285,17 @@ cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, 
   count_launch(2);
   residual_partial<<<chunks, 128, 0, st>>>(n, m, axr, axi, bxr, bxi, ld, lam, scale, scratch);
   residual_final<<<ceil_div(m, 128), 128, 0, st>>>(chunks, m, scratch, res);
+  return cudaGetLastError();
+}
+
+cudaError_t residual_sums_launch(int n, int m, const double* axr, const double* axi, const double* bxr,
+                                 const double* bxi, long long ld, const double* lam, double scale,
+                                 double* sums, double* scratch, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  int chunks = ceil_div(std::max(n, 1), RES_ROWS);
+  count_launch(2);
+  residual_partial<<<chunks, 128, 0, st>>>(n, m, axr, axi, bxr, bxi, ld, lam, scale, scratch);
+  residual_sums<<<ceil_div(m, 128), 128, 0, st>>>(chunks, m, scratch, sums);
   return cudaGetLastError();
 }
 

@@ -25,6 +25,9 @@ size_t residual_scratch_bytes(int n, int m);
 cudaError_t residual_launch(int n, int m, const double* axr, const double* axi, const double* bxr,
                             const double* bxi, long long ld, const double* lam, double scale,
                             double* res, double* scratch, cudaStream_t st);
+cudaError_t residual_sums_launch(int n, int m, const double* axr, const double* axi, const double* bxr,
+                                 const double* bxi, long long ld, const double* lam, double scale,
+                                 double* sums, double* scratch, cudaStream_t st);
 cudaError_t pack_launch(int n, int m, const double* z, long long ldz, double* re, double* im,
                         long long ldp, int to_planar, cudaStream_t st);
 

@@ -915,7 +915,6 @@ size_t panel_cluster_smem(int rpc) {
 
 int g_grid_max_blocks = 0;
 bool g_cluster_ok = false;
-bool g_probed = false;
 
 size_t panel_smem(int rpc) {
   return sizeof(double) * (2 * (size_t)rpc * SP + 4 * PW + 2 * REC + 4 * PW + 4 * SB * PW + 4 * MAXG);
@@ -970,8 +969,8 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
   a.xu = a.xrowr + 2 * 2 * PW;
   a.sxs = (long long)(panel_scratch_bytes() / sizeof(double));
   a.b0 = 0;
-  if (!g_probed) {
-    g_probed = true;
+  static DevOnce probed;  // attributes are per device; the probe results are the same on every B200
+  if (probed.first()) {
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
     cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(panel_kernel<PANEL_GRID>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap);
@@ -989,9 +988,6 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     int clusters = 0;
     cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, panel_cluster_kernel, &cfg);
     g_cluster_ok = (e == cudaSuccess && clusters >= 1);
-    if (getenv("FB_PANEL_DEBUG"))
-      fprintf(stderr, "[feastb200] panel cluster probe: %s, max active 16-CTA clusters = %d\n",
-              cudaGetErrorString(e), clusters);
     cudaGetLastError();
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, panel_kernel<PANEL_GRID>, PT, panel_smem(128));
@@ -1004,8 +1000,7 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     // GEMMs (384: fewest CTAs, +1-3 % at 8 shifts); a lone shift is panel-latency
     // bound and wants the shortest per-CTA column work (192: 28.2 vs 31.1 ms
     // for one N = 4096 LU)
-    static const int rforce = getenv("FB_PANEL_RPC") ? std::max(64, std::min(rpc_cluster, atoi(getenv("FB_PANEL_RPC")))) : 0;
-    const int rmin = rforce ? rforce : (count >= 4 ? 384 : 192);
+    const int rmin = count >= 4 ? 384 : 192;
     if (rows > 2 * PW) G = std::max(G, std::min(max_cluster, ceil_div(rows, rmin)));
     G = std::max(1, std::min(G, rows / PW));
     int rpc = ceil_div(rows, G);
@@ -1013,11 +1008,6 @@ cudaError_t panel_launch(PanelArgs a, int count, char* scratch, cudaStream_t st)
     a.rpc = rpc;
     // G == 1 runs the cluster kernel too (a 1-CTA cluster): its exchange stays
     // in shared memory, where the grid kernel would round-trip through L2
-    static const bool grid1 = getenv("FB_PANEL_GRID1") != nullptr;
-    if (G == 1 && grid1) {
-      panel_kernel<PANEL_GRID><<<dim3(1, count), PT, panel_smem(rpc), st>>>(a);
-      return cudaGetLastError();
-    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

@@ -721,11 +721,8 @@ size_t reduced_scratch_bytes(int m) { return sizeof(double) * (15 * (size_t)m * 
 template <bool C>
 static cudaError_t run_reduced(const RArgs& a, cudaStream_t st) {
   size_t smem = smem_for(a.m);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(reduced_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cfg = true;
-  }
+  static DevOnce cfg;
+  if (cfg.first()) cudaFuncSetAttribute(reduced_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   reduced_kernel<C><<<1, RT, smem, st>>>(a);
   count_launch();
   return cudaGetLastError();

@@ -632,13 +632,13 @@ static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, con
 
 // The right-hand sides of all items are read and rewritten by every step
 // (right-looking accumulators), so the batch is swept in groups whose
-// accumulators fit in L2 (FB_SWEEP_L2MB, default 64 MB): past that the
+// accumulators fit in L2 (64 MB): past that the
 // accumulator traffic spills to HBM (C3: 321 MB of X for 16 shifts).
 cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                          long long ld, long long slu, const double* dinv, const double* gmat, long long sdinv,
                          double* xre, double* xim, long long ldx, long long sx, cudaStream_t st) {
   if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
-  static const double budget = 1048576.0 * (getenv("FB_SWEEP_L2MB") ? atof(getenv("FB_SWEEP_L2MB")) : 64.0);
+  const double budget = 1048576.0 * 64.0;  // sweep working set per launch: about half the 126 MB L2
   const double item = 16.0 * (double)n * (double)nrhs;
   int group = count;
   if (count * item > 1.5 * budget) {  // C2's 84 MB stays one launch; C3's 321 MB goes in 3-shift groups

@@ -288,14 +288,23 @@ class DeviceDenseOps:
     def solve_adjoint(self, f, W: Planar):
         self._solve(f, W, True)
 
+    # ``rows`` = (r0, r1): multi-GPU row sharding -- only that row block of the
+    # product is computed (the kernel reads no other rows, kernel.py _row_block)
+    rows = None
+
+    def _mult(self, M: Planar, X: Planar, Y: Planar):
+        r0, r1 = self.rows if self.rows is not None else (0, self.n)
+        self.dev.gemm("N", "N", r1 - r0, X.cols, self.n, 1.0, M.rows_view(r0, r1), X, 0.0,
+                      Y.rows_view(r0, r1), cplx=self.hermitian)
+
     def multiply_a(self, X: Planar, Y: Planar):
-        self.dev.gemm("N", "N", self.n, X.cols, self.n, 1.0, self.A, X, 0.0, Y, cplx=self.hermitian)
+        self._mult(self.A, X, Y)
 
     def multiply_b(self, X: Planar, Y: Planar):
         if self.B is None:
             Y.copy_from(X)
         else:
-            self.dev.gemm("N", "N", self.n, X.cols, self.n, 1.0, self.B, X, 0.0, Y, cplx=self.hermitian)
+            self._mult(self.B, X, Y)
 
 
 class B200DenseOps:
@@ -406,6 +415,7 @@ def _dense_driver(a, b, emin, emax, m0, uplo, fpm, options, x0, hermitian, devic
         else:
             dev.upload(x0h[:, :m0], cplx=hermitian, out=kernel.X)
     ops = DeviceDenseOps(dev, A, B, hermitian)
+    ops.rows = kernel._rows if kernel._sharded() else None
     result = run_rci(kernel, ops, options)
     result.factorizations = ops.factorizations
     return result

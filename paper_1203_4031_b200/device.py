@@ -286,6 +286,13 @@ class Device:
                                    _P(BX.im), AX.ld, _P(lam_ptr), float(scale), _P(res_ptr))
         self.check(rc, "residuals")
 
+    def residual_sums(self, AX: Planar, BX: Planar, lam_ptr, scale, sums_ptr):
+        """(numerator, denominator) sums of the residuals over the rows of AX/BX
+        (a row block of the multi-GPU path), interleaved per column."""
+        rc = self.lib.fb_residual_sums(self.h, AX.rows, AX.cols, _P(AX.re), _P(AX.im), _P(BX.re),
+                                       _P(BX.im), AX.ld, _P(lam_ptr), float(scale), _P(sums_ptr))
+        self.check(rc, "residual_sums")
+
     def chol_check(self, Bq: Planar, m):
         fail = ctypes.c_int(0)
         rc = self.lib.fb_chol_check(self.h, m, _P(Bq.re), _P(Bq.im), Bq.ld, ctypes.byref(fail))

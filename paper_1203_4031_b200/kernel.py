@@ -143,7 +143,8 @@ class _RciKernel:
 
     def __init__(self, n, m0, emin, emax, fpm=None, *, seed=DEFAULT_SEED, block_size=None,
                  dtype=None, routine_name=None, device=None, host_mirror=True,
-                 adjoint_capable=True, points=None, q_reduce=None):
+                 adjoint_capable=True, points=None, q_reduce=None, rows=None, sum_reduce=None,
+                 flag_reduce=None):
         self.n = int(n)
         self.m0 = int(m0)
         self._m0_init = int(m0)
@@ -164,6 +165,14 @@ class _RciKernel:
         self._gen = None
         self._points = points          # contour indices served by this rank (None: all)
         self._q_reduce = q_reduce      # callable(Q planar) summing partial Q over ranks
+        # multi-GPU row sharding of the projection / Ritz / residual products
+        # (SURVEY.md §8e): this rank owns rows [r0, r1) of A*Q, B*Q, A*X, B*X;
+        # sum_reduce(torch tensor) all-reduces the reduced matrices, the
+        # residual sums and the next right-hand side; flag_reduce(code) -> the
+        # most severe abort code over the ranks (0: carry on)
+        self._rows = tuple(rows) if rows is not None else None
+        self._sum_reduce = sum_reduce
+        self._flag_reduce = flag_reduce
         self._solve_pass = None        # callable(Y, hermitian): batched solves of a pass
         self._pass_result = None       # callable(z, adjoint) -> Planar result of this pass, or None
         self._solve_pass_acc = None    # callable(Y, spec, radius, Q) -> bool: solves + accumulation fused
@@ -218,6 +227,7 @@ class _RciKernel:
         torch = dev.torch
         self.e_dev = torch.zeros(m, dtype=torch.float64, device=dev.tdev)
         self.res_dev = torch.zeros(m, dtype=torch.float64, device=dev.tdev)
+        self._res_sums = torch.zeros(2 * max(m, 1), dtype=torch.float64, device=dev.tdev)
 
     def _mirrors(self, n, m):
         if self.host_mirror:
@@ -320,6 +330,26 @@ class _RciKernel:
             yield task
             start += cols
 
+    def _row_block(self):
+        return self._rows if self._rows is not None else (0, self.n)
+
+    def _sharded(self):
+        return self._rows is not None and self._sum_reduce is not None
+
+    def _next_rhs(self):
+        """Y <- B*X (in W1) for the next contour pass.  Row-sharded multiplies
+        leave only this rank's rows of W1 valid, and every rank solves its
+        shifts against the WHOLE right-hand side: own rows, zeros elsewhere,
+        summed over the ranks."""
+        Yn = self.Y.cols_view(0, self.m0)
+        if self._sharded():
+            r0, r1 = self._row_block()
+            self.Y.zero_()   # the whole buffer is summed (columns past M0 stay zero)
+            Yn.rows_view(r0, r1).copy_from(self.W1.cols_view(0, self.m0).rows_view(r0, r1))
+            self._sum_reduce(self.Y.t)
+        else:
+            Yn.copy_from(self.W1.cols_view(0, self.m0))
+
     def _fill_random_y(self):
         nm = self.n * self._m0_init
         self.dev.splitmix(self.seed, 0, nm, self.Y)
@@ -368,7 +398,7 @@ class _RciKernel:
 
         if fpm.slot(5) == 1:
             yield from self._multiply_blocks(RciTask.MULTIPLY_B)
-            self.Y.cols_view(0, self.m0).copy_from(self.W1.cols_view(0, self.m0))
+            self._next_rhs()
         else:
             self._fill_random_y()
 
@@ -413,6 +443,15 @@ class _RciKernel:
                     self.W2.cols_view(0, m0).copy_from(self.Y.cols_view(0, m0))
                     yield RciTask.SOLVE_ADJOINT
                     self._accumulate(contour.weights[k], contour.radius, contour.theta[k], True)
+            if self._flag_reduce is not None:
+                # a rank that failed inside this pass reports through the pump
+                # (run_rci) with the same collective: all ranks leave together
+                code = self._flag_reduce(0)
+                if code:
+                    self.info = code
+                    if verbose:
+                        self._print_trailer()
+                    return
             if self._q_reduce is not None:
                 self._q_reduce(Q)
 
@@ -434,8 +473,20 @@ class _RciKernel:
             W1 = self.W1.cols_view(0, m0)
             AQ = self.AQ.cols_view(0, m0).rows_view(0, m0)
             BQ = self.BQ.cols_view(0, m0).rows_view(0, m0)
-            dev.gemm("C", "N", m0, m0, n, 1.0, Q, AP, 0.0, AQ)
-            dev.gemm("C", "N", m0, m0, n, 1.0, Q, W1, 0.0, BQ)
+            r0, r1 = self._row_block()
+            sharded = self._sharded()
+            # row block of this rank (the whole matrix on one GPU): A*Q and B*Q
+            # hold valid rows r0..r1 only when the ops shard the multiplies
+            Qb, APb, W1b = Q.rows_view(r0, r1), AP.rows_view(r0, r1), W1.rows_view(r0, r1)
+            if sharded:
+                self.AQ.zero_()   # the whole buffers are summed
+                self.BQ.zero_()
+            dev.gemm("C", "N", m0, m0, r1 - r0, 1.0, Qb, APb, 0.0, AQ)
+            dev.gemm("C", "N", m0, m0, r1 - r0, 1.0, Qb, W1b, 0.0, BQ)
+            if sharded:
+                # one all-reduce of the two reduced matrices (2 * M0^2 entries)
+                self._sum_reduce(self.AQ.t)
+                self._sum_reduce(self.BQ.t)
             dev.symmetrize(AQ)
             dev.symmetrize(BQ)
 
@@ -472,9 +523,17 @@ class _RciKernel:
             dev.gemm("N", "N", n, m0, m0, 1.0, Q, PHI, 0.0, X)
             AX = self.AX.cols_view(0, m0)
             BX = self.BX.cols_view(0, m0)
-            dev.gemm("N", "N", n, m0, m0, 1.0, AP, PHI, 0.0, AX)
-            dev.gemm("N", "N", n, m0, m0, 1.0, W1, PHI, 0.0, BX)
-            dev.residuals(AX, BX, self.e_dev.data_ptr(), scale, self.res_dev.data_ptr())
+            AXb, BXb = AX.rows_view(r0, r1), BX.rows_view(r0, r1)
+            dev.gemm("N", "N", r1 - r0, m0, m0, 1.0, AP.rows_view(r0, r1), PHI, 0.0, AXb)
+            dev.gemm("N", "N", r1 - r0, m0, m0, 1.0, W1.rows_view(r0, r1), PHI, 0.0, BXb)
+            if sharded:
+                sums = self._res_sums[:2 * m0]
+                dev.residual_sums(AXb, BXb, self.e_dev.data_ptr(), scale, sums.data_ptr())
+                self._sum_reduce(sums)
+                num, den = sums[0::2], sums[1::2]
+                self.res_dev[:m0] = dev.torch.where(den > 0, num / den, dev.torch.full_like(num, float("inf")))
+            else:
+                dev.residuals(AX, BX, self.e_dev.data_ptr(), scale, self.res_dev.data_ptr())
             lam = self.e_dev[:m0].cpu().numpy()
             res = self.res_dev[:m0].cpu().numpy()
             self.e[:m0] = lam
@@ -504,7 +563,7 @@ class _RciKernel:
             trace_prev = trace_cur
             self.loop += 1
             yield from self._multiply_blocks(RciTask.MULTIPLY_B)
-            self.Y.cols_view(0, self.m0).copy_from(self.W1.cols_view(0, self.m0))
+            self._next_rhs()
 
     def _finalize(self, info, verbose, tol):
         """kernel.py:446-466: spurious flagging, then filter_sort_flag ordering;

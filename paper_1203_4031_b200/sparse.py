@@ -250,15 +250,7 @@ class DeviceCsrOps:
         self.factorizations = 0
         self.row_order = None
         rows, cols = _union_pattern(a_full, b_full)
-        if solver == "iterative":
-            from ._bicgstab import DeviceBicgstab
-            # RCM order only schedules the SpMM rows (L2 reuse of gathered rows)
-            self.row_order = dev.torch.from_numpy(bandwidth_reducing_order(self.n, rows, cols)).to(dev.tdev)
-            self._it = DeviceBicgstab(dev, self.n, rows, cols, a_full, b_full, hermitian, iter_tol,
-                                      row_order=self.row_order)
-            self.mode = "iterative"
-            return
-        if solver != "direct":
+        if solver not in ("direct", "iterative"):
             raise ValueError(f"unknown solver {solver!r}")
         perm = bandwidth_reducing_order(self.n, rows, cols)
         self.row_order = dev.torch.from_numpy(perm).to(dev.tdev)    # SpMM row visiting order
@@ -266,9 +258,24 @@ class DeviceCsrOps:
         iperm[perm] = np.arange(self.n, dtype=np.int64)
         kl = int(np.abs(iperm[rows] - iperm[cols]).max()) if rows.size else 0
         self.kl = kl
+        if solver == "direct" and kl > _BAND_MAX_KL and self.n > dense_max_n:
+            # neither GPU LU applies (band kernels stop at bandwidth 127, the dense
+            # LU at n = 32768): the reference's sparse LU would still factor this
+            # pencil, so the inner systems go to the device BiCGStab instead of
+            # aborting with info -1 (unstructured 3-D meshes land here)
+            import warnings
+            warnings.warn(f"feast_*csr: reordered bandwidth {kl} at n = {self.n} is outside the GPU direct "
+                          f"solvers; using the iterative inner solver (tolerance {min(iter_tol, 1e-8):g})")
+            solver, iter_tol = "iterative", min(iter_tol, 1e-8)
+            self.solver = "iterative"
+        if solver == "iterative":
+            from ._bicgstab import DeviceBicgstab
+            # RCM order only schedules the SpMM rows (L2 reuse of gathered rows)
+            self._it = DeviceBicgstab(dev, self.n, rows, cols, a_full, b_full, hermitian, iter_tol,
+                                      row_order=self.row_order)
+            self.mode = "iterative"
+            return
         if kl <= 16 or (kl <= _BAND_MAX_KL and 8 * kl <= self.n) or self.n > dense_max_n:
-            if kl > _BAND_MAX_KL:
-                raise MemoryError(f"reordered bandwidth {kl} > {_BAND_MAX_KL} at n = {self.n}")
             from .banded import DeviceBandOps
             self.mode = "band"
             FA = dev.upload(self._band(a_full, iperm, kl), cplx=hermitian)

@@ -216,5 +216,5 @@ C5_INTERVAL = (-0.0174985, 0.0174041)
 C5_COUNT = 401
 # mid-gap endpoints around the 150 eigenvalues nearest 0 of the N = 12288
 # pencil (scipy eigh subset, tests/golden/make_golden.py c5m)
-C5M_INTERVAL = None
-C5M_COUNT = None
+C5M_INTERVAL = (-0.017610083116153735, 0.0174584899389215)
+C5M_COUNT = 150

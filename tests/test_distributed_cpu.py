@@ -139,3 +139,69 @@ def test_feast_intervals_subgroups(world, nint):
     out = mp.Manager().dict()
     mp.spawn(_interval_worker, args=(world, _free_port(), nint, out), nprocs=world, join=True)
     assert [out[r] for r in range(world)] == [1] * world
+
+
+@pytest.mark.parametrize("n,world", [(10, 1), (10, 3), (8192, 8), (7, 8), (4096, 2)])
+def test_row_blocks_partition(n, world):
+    from paper_1203_4031_b200.distributed import row_block
+    blocks = [row_block(n, r, world) for r in range(world)]
+    assert blocks[0][0] == 0 and blocks[-1][1] == n
+    for (a0, a1), (b0, b1) in zip(blocks, blocks[1:]):
+        assert a1 == b0 and a0 <= a1
+    sizes = [b - a for a, b in blocks]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _shard_worker(rank, world, port, fail_rank, out):
+    """Row-sharded projection / residual / next-right-hand-side algebra of the
+    multi-GPU path (kernel.py _run with rows/sum_reduce) on CPU tensors."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1203_4031_b200.distributed import make_flag_reduce, make_sum_reduce, row_block
+    rng = np.random.default_rng(11)
+    n, m0 = 41, 5
+    a = rng.standard_normal((n, n)); a = (a + a.T) / 2
+    h = rng.standard_normal((n, n)); b = np.eye(n) + 0.1 * h @ h.T / n
+    q = rng.standard_normal((n, m0))
+    lam = rng.standard_normal(m0)
+    r0, r1 = row_block(n, rank, world)
+    red = make_sum_reduce()
+    # A_Q, B_Q from row blocks
+    aq = torch.from_numpy(q[r0:r1].T @ (a[r0:r1] @ q))
+    bq = torch.from_numpy(q[r0:r1].T @ (b[r0:r1] @ q))
+    red(aq); red(bq)
+    # residual sums from row blocks
+    ax, bx = a[r0:r1] @ q, b[r0:r1] @ q
+    sums = torch.from_numpy(np.stack([np.abs(ax - lam * bx).sum(0), np.abs(0.3 * bx).sum(0)], 1).reshape(-1).copy())
+    red(sums)
+    # next right-hand side: own rows, zeros elsewhere
+    y = torch.zeros(n, m0, dtype=torch.float64)
+    y[r0:r1] = torch.from_numpy(b[r0:r1] @ q)
+    red(y)
+    flag = make_flag_reduce()
+    code = flag(-2 if rank == fail_rank else 0)
+    out[rank] = (aq.numpy(), bq.numpy(), sums.numpy(), y.numpy(), code)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_row_sharded_reductions_match_serial(fail_rank):
+    rng = np.random.default_rng(11)
+    n, m0 = 41, 5
+    a = rng.standard_normal((n, n)); a = (a + a.T) / 2
+    h = rng.standard_normal((n, n)); b = np.eye(n) + 0.1 * h @ h.T / n
+    q = rng.standard_normal((n, m0))
+    lam = rng.standard_normal(m0)
+    out = mp.Manager().dict()
+    mp.spawn(_shard_worker, args=(2, _free_port(), fail_rank, out), nprocs=2, join=True)
+    for rank in range(2):
+        aq, bq, sums, y, code = out[rank]
+        assert np.allclose(aq, q.T @ a @ q, rtol=0, atol=1e-12)
+        assert np.allclose(bq, q.T @ b @ q, rtol=0, atol=1e-12)
+        num, den = sums[0::2], sums[1::2]
+        assert np.allclose(num, np.abs(a @ q - lam * (b @ q)).sum(0), rtol=1e-13)
+        assert np.allclose(den, np.abs(0.3 * (b @ q)).sum(0), rtol=1e-13)
+        assert np.allclose(y, b @ q, rtol=0, atol=1e-13)
+        assert code == (-2 if fail_rank >= 0 else 0)
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][2], out[1][2])

@@ -233,3 +233,35 @@ def test_numpy_ops_adapter_under_run_rci(rng, solver):
     r = fb.run_rci(k, B200CsrOps(csr, None, solver, 1e-12), fb.SolverOptions())
     assert r.info == 0 and r.m == 6
     assert np.abs(r.e[:6] - ev[:6]).max() <= 1e-10 * max(abs(emin), abs(emax))
+
+
+def test_direct_solver_falls_back_to_iterative_outside_lu_range(rng):
+    """Bandwidth above the band kernels' limit AND n above the dense LU's limit
+    (forced here with dense_max_n): the reference's sparse LU would factor the
+    pencil, so DeviceCsrOps answers with the iterative inner solver (a warning)
+    instead of aborting with info -1."""
+    from paper_1203_4031_b200 import sparse
+    from paper_1203_4031_b200._driver import run_rci
+    from paper_1203_4031_b200.kernel import SymmetricRci
+    fb = _fb()
+    n = 300
+    a = np.zeros((n, n))
+    idx = np.arange(n)
+    a[idx, idx] = 4.0 + 0.5 * np.cos(idx)
+    off = 140                                     # an arrow-free pattern no ordering narrows below ~128
+    a[idx[:-off], idx[off:]] = a[idx[off:], idx[:-off]] = 0.3
+    a[idx[:-1], idx[1:]] = a[idx[1:], idx[:-1]] = -1.0
+    emin, emax = gap_interval(np.linalg.eigvalsh(a), 10, 18)
+    acsr = fb.CsrMatrix.from_dense(a)
+    dev = _dev()
+    with pytest.warns(UserWarning, match="iterative inner solver"):
+        ops = sparse.DeviceCsrOps(dev, acsr.expand_full(), None, False, "direct", 1e-3, dense_max_n=100)
+    if ops.kl <= 127:
+        pytest.skip("the reordering narrowed the pattern: boundary not reached")
+    assert ops.mode == "iterative"
+    k = SymmetricRci(n, 14, emin, emax, fb.feastinit(), host_mirror=False)
+    r = run_rci(k, ops, fb.SolverOptions())
+    ev = np.linalg.eigvalsh(a)
+    want = ev[(ev >= emin) & (ev <= emax)]
+    assert r.info == 0 and r.m == want.size
+    assert np.abs(np.sort(r.e[:r.m]) - want).max() <= 1e-9 * max(abs(emin), abs(emax))
