@@ -245,6 +245,7 @@ struct PSArgs {
   const int* ipiv;
   long long sp;
   const double2* us;  // slot-ordered U columns of item 0 (item k at + k*sa doubles)
+  const double* t4;   // kl = 16: U in 4-row DMMA fragment order (band_t4_kernel), else nullptr
   long long sa;
   double *xr, *xi;
   long long ldx, sx;
@@ -933,6 +934,229 @@ __global__ void __launch_bounds__(2 * BNC, 5) band_psolve_bwd_kernel(PSArgs a) {
   if constexpr (!BULK) cp_async_wait<0>();
 }
 
+// ---- backward sweep on the FP64 tensor pipe (kl = 16) -----------------------------
+// The SIMT sweeps above feed every complex multiply-add (4 DFMA) with one
+// 16-byte broadcast shared-memory load; the register-file fill of those loads
+// (512 B per warp and load), not the FP64 pipe, bounds them (~40 % of the pipe,
+// profiles/).  Here the sweep runs in steps of FOUR rows: the 4 x 4 diagonal
+// block is solved by substitution (SIMT, two quad shuffles), and the rank-4
+// update of the 32 rows above is a DMMA product W^T(8 columns x 8 rows) +=
+// X^T(8 x 4) * (-U^T)(4 x 8) per row tile, whose B fragments are read as one
+// distinct double per lane (256 B per warp and 256 multiply-adds): 7 x less
+// operand traffic per flop.  A warp owns 8 right-hand sides; the active rows
+// (36, plus the 4 entering next) live in 40 fixed accumulator slots, slot =
+// (distance from the partition's last row) mod 40, so the 10 steps of one turn
+// of the slots are unrolled with compile-time tile indices.  The factor is
+// re-ordered once per factorization into exactly this fragment order (T4).
+constexpr int T4_NT = 5, T4_SLOTS = 40, T4_PERIOD = 10;
+constexpr int T4_STEPD = T4_NT * 2 * 32 + 32;  // doubles per 4-row step: B fragments + the 4x4 block (re, im)
+constexpr int T4_S = 2;                        // steps per staged chunk
+constexpr int T4_WARPS = 4;                    // 32 right-hand sides per CTA
+constexpr int T4_NST = 5;                      // staged chunks in flight (9.7 KB each)
+constexpr int T4_CHUNKD = T4_S * T4_STEPD + 2 * 4 * T4_S * 8 * T4_WARPS;  // + entering rows [plane][row][32 columns]
+
+__host__ __device__ inline long long t4_steps(int n, int P) { return (part_sz(n, P) + 3) / 4; }
+
+struct T4Args {
+  int n, P;
+  const double *wr, *wi;
+  long long sw;
+  double* t4;  // item 0; item k at + k*sa doubles
+  long long sa;
+};
+
+__global__ void band_t4_kernel(T4Args a) {
+  constexpr int KV = 32, LW = 49;
+  const int k = blockIdx.y;
+  const double* Wp[2] = {a.wr + k * a.sw, a.wi + k * a.sw};
+  double* T = a.t4 + k * a.sa;
+  const long long spp = t4_steps(a.n, a.P), total = spp * a.P * T4_STEPD;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long gs = e / T4_STEPD;
+    const int r = (int)(e % T4_STEPD), part = (int)(gs / spp), s = (int)(gs % spp);
+    const int lo = part_lo(part, a.n, a.P), top = part_lo(part + 1, a.n, a.P) - 1;
+    double v = 0.0;
+    if (r < T4_NT * 64) {
+      const int t = r >> 6, plane = (r >> 5) & 1, l = r & 31, kk = l & 3, nn = l >> 2;
+      const int slot = 8 * t + nn;
+      const int delta = ((slot - 4 * s) % T4_SLOTS + T4_SLOTS) % T4_SLOTS;  // row = top - (4s + delta)
+      const int d = delta - kk;                                             // rows above the solved row kk
+      const int rcol = top - (4 * s + kk), rrow = rcol - d;
+      if (delta >= 4 && delta < 36 && d >= 1 && d <= KV && rrow >= lo) v = -Wp[plane][(long long)rcol * LW + KV - d];
+    } else {
+      const int idx = r - T4_NT * 64, c = idx >> 1, plane = idx & 1, kk = c >> 2, kp = c & 3;
+      const int rk = top - (4 * s + kk), rp = top - (4 * s + kp);
+      if (rk >= lo) {
+        if (kp == kk) {
+          const double dr = Wp[0][(long long)rk * LW + KV], di = Wp[1][(long long)rk * LW + KV];
+          const double den = dr * dr + di * di;
+          if (den > 0.0) v = plane ? -di / den : dr / den;
+        } else if (kp < kk) {
+          v = Wp[plane][(long long)rp * LW + KV - (kk - kp)];  // U(row rk, column rp)
+        }
+      }
+    }
+    T[e] = v;
+  }
+}
+
+__global__ void __launch_bounds__(T4_WARPS * 32, 4) band_psolve_bwd_t4_kernel(PSArgs a) {
+  // column group fastest, then shift: the CTAs that read the same T4 run together (L2)
+  const int ncg = (a.nrhs + 8 * T4_WARPS - 1) / (8 * T4_WARPS);
+  const int cgi = blockIdx.x % ncg, k = (blockIdx.x / ncg) % a.count, part = blockIdx.x / (ncg * a.count);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  const int col0 = cgi * 8 * T4_WARPS, col = col0 + warp * 8 + g;
+  const bool on = col < a.nrhs;
+  const int lo = part_lo(part, a.n, a.P), hi = part_lo(part + 1, a.n, a.P), top = hi - 1;
+  const long long spp = t4_steps(a.n, a.P);
+  const double* T4 = a.t4 + k * a.sa + (long long)part * spp * T4_STEPD;
+  double* Xr = a.xr + k * a.sx;
+  double* Xi = a.xi + k * a.sx;
+  extern __shared__ __align__(16) double sx[];  // [T4_NST][T4_CHUNKD]
+  __shared__ __align__(8) unsigned long long full[T4_NST];
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < T4_NST; ++b) mbar_init(&full[b], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int nsteps = (hi - lo + 3) / 4, nchunks = (nsteps + T4_S - 1) / T4_S;
+  // Staging of chunk c (steps c*T4_S ..): the factor fragments are one contiguous
+  // run -> one bulk copy (TMA engine) by an elected thread onto the chunk's
+  // mbarrier; the 4*T4_S entering right-hand-side rows (32 columns, 2 planes) are
+  // spread over the CTA as 8-byte cp.async (zero-filled where the row or column
+  // does not exist), one commit group per chunk.
+  constexpr int XE = 2 * 4 * T4_S * 8 * T4_WARPS;  // entering-row entries per chunk
+  auto stage = [&](int buf, int c) {
+    double* dst = sx + (size_t)buf * T4_CHUNKD;
+    const int s0 = c * T4_S;
+    if (tid == 0) {
+      const unsigned bytes = c < nchunks ? (unsigned)(T4_S * T4_STEPD * 8) : 0u;
+      mbar_arrive_expect_tx(&full[buf], bytes);
+      if (bytes) bulk_g2s(dst, T4 + (long long)s0 * T4_STEPD, bytes, &full[buf]);
+    }
+    double* xb = dst + T4_S * T4_STEPD;
+    const int rfirst = top - (4 * s0 + T4_SLOTS);  // entering rows of step s: top - (4s + 40 + kk)
+#pragma unroll
+    for (int e = tid; e < XE; e += T4_WARPS * 32) {
+      const int cc_ = e % (8 * T4_WARPS), rr = (e / (8 * T4_WARPS)) % (4 * T4_S), pl = e / (8 * T4_WARPS * 4 * T4_S);
+      const int r = rfirst - rr;
+      const bool ok = c < nchunks && r >= lo && col0 + cc_ < a.nrhs;
+      const double* src = (pl ? Xi : Xr) + (ok ? (long long)r * a.ldx + col0 + cc_ : 0);
+      cp_async8(xb + e, src, ok);
+    }
+    cp_async_commit();
+  };
+  // accumulator slots: tile t, lane (g, q) holds slots 8t + 2q + {0, 1} of column g
+  double cr[T4_NT][2], ci[T4_NT][2];
+#pragma unroll
+  for (int t = 0; t < T4_NT; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int r = top - (8 * t + 2 * q + e);
+      cr[t][e] = ci[t][e] = 0.0;
+      if (on && r >= lo) {
+        cr[t][e] = Xr[(long long)r * a.ldx + col];
+        ci[t][e] = Xi[(long long)r * a.ldx + col];
+      }
+    }
+#pragma unroll 1
+  for (int c = 0; c < T4_NST - 1; ++c) stage(c, c);
+  int buf = 0;
+  unsigned phase = 0;
+  const int quad = lane & ~3;
+  constexpr int CPT = T4_PERIOD / T4_S;  // chunks per turn of the slots
+#pragma unroll 1
+  for (int c0 = 0; c0 < nchunks; c0 += CPT) {
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int c = c0 + cc;  // chunks past nchunks: nothing staged, nothing stored
+      cp_async_wait<T4_NST - 2>();          // this thread's entering-row copies of chunk c
+      mbar_wait_parity(&full[buf], phase);  // the chunk's factor fragments
+      __syncthreads();                      // all copies of chunk c visible; chunk c-1's buffer is free
+      stage(buf == 0 ? T4_NST - 1 : buf - 1, c + T4_NST - 1);
+      const double* base = sx + (size_t)buf * T4_CHUNKD;
+#pragma unroll
+      for (int jj = 0; jj < T4_S; ++jj) {
+        const int u = cc * T4_S + jj;            // compile-time position in the turn
+        const int tu = (4 * u) / 8, h = u & 1;   // solved slots 4u..4u+3: tile tu, lanes q = 2h, 2h+1
+        const int s = c * T4_S + jj;
+        const double* sd = base + jj * T4_STEPD;
+        const double2* D = reinterpret_cast<const double2*>(sd + T4_NT * 64);  // [kk][kp]
+        // -- the 4 x 4 block by substitution: lane 2h holds rows 0, 1, lane 2h+1 rows 2, 3
+        const double w0r = cr[tu][0], w0i = ci[tu][0], w1r = cr[tu][1], w1i = ci[tu][1];
+        auto cmul = [](double ar, double ai, double2 b, double& orr, double& oi) {
+          orr = ar * b.x - ai * b.y;
+          oi = ar * b.y + ai * b.x;
+        };
+        double x0r, x0i, x1r, x1i, x2r, x2i, x3r, x3i, tr_, ti_;
+        cmul(w0r, w0i, D[0], x0r, x0i);
+        {
+          const double2 u10 = D[4];
+          tr_ = fma(-u10.x, x0r, fma(u10.y, x0i, w1r));
+          ti_ = fma(-u10.x, x0i, fma(-u10.y, x0r, w1i));
+          cmul(tr_, ti_, D[5], x1r, x1i);
+        }
+        const int srcA = quad | (2 * h);
+        x0r = __shfl_sync(0xffffffffu, x0r, srcA); x0i = __shfl_sync(0xffffffffu, x0i, srcA);
+        x1r = __shfl_sync(0xffffffffu, x1r, srcA); x1i = __shfl_sync(0xffffffffu, x1i, srcA);
+        {
+          const double2 u20 = D[8], u21 = D[9];
+          tr_ = fma(-u20.x, x0r, fma(u20.y, x0i, w0r));
+          ti_ = fma(-u20.x, x0i, fma(-u20.y, x0r, w0i));
+          tr_ = fma(-u21.x, x1r, fma(u21.y, x1i, tr_));
+          ti_ = fma(-u21.x, x1i, fma(-u21.y, x1r, ti_));
+          cmul(tr_, ti_, D[10], x2r, x2i);
+          const double2 u30 = D[12], u31 = D[13], u32 = D[14];
+          tr_ = fma(-u30.x, x0r, fma(u30.y, x0i, w1r));
+          ti_ = fma(-u30.x, x0i, fma(-u30.y, x0r, w1i));
+          tr_ = fma(-u31.x, x1r, fma(u31.y, x1i, tr_));
+          ti_ = fma(-u31.x, x1i, fma(-u31.y, x1r, ti_));
+          tr_ = fma(-u32.x, x2r, fma(u32.y, x2i, tr_));
+          ti_ = fma(-u32.x, x2i, fma(-u32.y, x2r, ti_));
+          cmul(tr_, ti_, D[15], x3r, x3i);
+        }
+        const int srcB = quad | (2 * h + 1);
+        x2r = __shfl_sync(0xffffffffu, x2r, srcB); x2i = __shfl_sync(0xffffffffu, x2i, srcB);
+        x3r = __shfl_sync(0xffffffffu, x3r, srcB); x3i = __shfl_sync(0xffffffffu, x3i, srcB);
+        // A fragment: lane (g, q) carries x_q of column g; the same lane stores it
+        const double ar = q == 0 ? x0r : (q == 1 ? x1r : (q == 2 ? x2r : x3r));
+        const double ai = q == 0 ? x0i : (q == 1 ? x1i : (q == 2 ? x2i : x3i));
+        const int rs = top - (4 * s + q);
+        if (on && rs >= lo) {
+          Xr[(long long)rs * a.ldx + col] = ar;
+          Xi[(long long)rs * a.ldx + col] = ai;
+        }
+        // the rows entering take the solved slots (first needed two steps on)
+        if ((q >> 1) == h) {
+          const double* xb = base + T4_S * T4_STEPD + (jj * 4 + 2 * (q & 1)) * 8 * T4_WARPS + warp * 8 + g;
+          cr[tu][0] = xb[0];
+          cr[tu][1] = xb[8 * T4_WARPS];
+          ci[tu][0] = xb[4 * T4_S * 8 * T4_WARPS];
+          ci[tu][1] = xb[(4 * T4_S + 1) * 8 * T4_WARPS];
+        }
+        // -- rank-4 update of every slot (B = -U^T in fragment order; 0 for the solved slots)
+        const double nai = -ai;
+#pragma unroll
+        for (int t = 0; t < T4_NT; ++t) {
+          const double br = sd[(t * 2) * 32 + lane], bi = sd[(t * 2 + 1) * 32 + lane];
+          dmma(cr[t][0], cr[t][1], ar, br);
+          dmma(cr[t][0], cr[t][1], nai, bi);
+          dmma(ci[t][0], ci[t][1], ar, bi);
+          dmma(ci[t][0], ci[t][1], ai, br);
+        }
+      }
+      if (++buf == T4_NST) {
+        buf = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // ---- fused spike correction + quadrature accumulation ---------------------------
 // Q -= sum_t coeff_t * (g_t - [V W]_t T_t): the correction product runs on the
 // FP64 tensor pipe with the accumulators starting from the partition solve g
@@ -1145,6 +1369,14 @@ cudaError_t psolve_launch(const PSArgs& ps, int count, cudaStream_t st) {
   PSArgs a = ps;
   a.count = count;
   psolve_fwd_fn(ps.kl)<<<grid, 32 * nw, sweep_xring_bytes(32 * nw, SC), st>>>(a);
+  if (ps.t4 && ((uintptr_t)ps.t4 & 15) == 0 && (ps.sa & 1) == 0) {  // kl = 16: tensor-pipe sweep
+    static DevOnce c4;
+    const size_t sm4 = sizeof(double) * T4_NST * T4_CHUNKD;
+    if (c4.first()) cudaFuncSetAttribute(band_psolve_bwd_t4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+    band_psolve_bwd_t4_kernel<<<dim3(ps.P * count * ceil_div(ps.nrhs, 8 * T4_WARPS)), 32 * T4_WARPS, sm4, st>>>(a);
+    count_launch(2);
+    return cudaGetLastError();
+  }
   const int ncb = ps.nrhs >= BNC ? BNC : 16 * ceil_div(ps.nrhs, 16);  // two lanes per right-hand side
   psolve_bwd_fn(ps.kl, bulk)<<<dim3(ps.P * count, ceil_div(ps.nrhs, ncb)), 2 * ncb,
                                sweep_xring_bytes(ncb, bwd_chunk(ps.kl)), st>>>(a);
@@ -1170,14 +1402,24 @@ int band_spike_parts(int n, int kl) {
 
 bool band_spike_ok(int kl) { return kl >= 1 && kl <= KLMAX; }
 
-// aux (per item, doubles): spikes | Dinv | F | Us [n][2kl+2] (re, im)
+// aux (per item, doubles): spikes | Dinv | F | Us [n][2kl+2] (re, im) | kl = 16: T4 (4-row DMMA fragments)
 static size_t aux_spike_part(int n, int kl) {
   const int P = band_spike_parts(n, kl);
   return (size_t)4 * kl * n + (size_t)12 * kl * kl * (P > 1 ? P - 1 : 0);
 }
-size_t band_spike_aux_doubles(int n, int kl) { return aux_spike_part(n, kl) + (size_t)2 * (2 * kl + 2) * n + 64; }
+static size_t aux_t4_doubles(int n, int kl) {
+  if (kl != KLMAX) return 0;
+  const int P = band_spike_parts(n, kl);
+  return (size_t)(t4_steps(n, P) * P + T4_S) * T4_STEPD;  // + one chunk of slack past the last partition
+}
+size_t band_spike_aux_doubles(int n, int kl) {
+  return aux_spike_part(n, kl) + (size_t)2 * (2 * kl + 2) * n + aux_t4_doubles(n, kl) + 64;
+}
 static const double2* slot_us(int n, int kl, const double* aux) {
   return reinterpret_cast<const double2*>(aux + aux_spike_part(n, kl));  // even offset: 16-byte aligned
+}
+static const double* slot_t4(int n, int kl, const double* aux) {
+  return kl == KLMAX ? aux + aux_spike_part(n, kl) + (size_t)2 * (2 * kl + 2) * n : nullptr;
 }
 
 size_t band_spike_solve_scratch_doubles(int n, int kl, int nrhs, int count) {
@@ -1235,6 +1477,15 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   band_slot_bwd_kernel<<<dim3((int)std::min<long long>((tu + 255) / 256, 8 * kSMs), count), 256, 0, st>>>(so);
   count_launch();
   if ((e = cudaGetLastError())) return e;
+  const double* t4 = slot_t4(n, kl, aux);
+  if (t4) {
+    T4Args ta{};
+    ta.n = n; ta.P = P; ta.wr = wr; ta.wi = wi; ta.sw = sw; ta.t4 = const_cast<double*>(t4); ta.sa = sa;
+    const long long tt = t4_steps(n, P) * P * T4_STEPD;
+    band_t4_kernel<<<dim3((int)std::min<long long>((tt + 255) / 256, 8 * kSMs), count), 256, 0, st>>>(ta);
+    count_launch();
+    if ((e = cudaGetLastError())) return e;
+  }
   if (P == 1) return cudaSuccess;
   double *sr, *si, *dr, *di, *fr, *fi;
   aux_ptrs(n, kl, aux, &sr, &si, &dr, &di, &fr, &fi);
@@ -1249,7 +1500,7 @@ cudaError_t band_spike_factor(int count, int n, int kl, const double* zr, const 
   PSArgs ps{};
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = 2 * kl;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
-  ps.us = us; ps.sa = sa;
+  ps.us = us; ps.t4 = t4; ps.sa = sa;
   ps.xr = sr; ps.xi = si; ps.ldx = 2 * kl; ps.sx = sa;
   if ((e = psolve_launch(ps, count, st))) return e;
   RFArgs rf{};
@@ -1280,6 +1531,7 @@ static cudaError_t solve_front(int count, int n, int kl, int nrhs, const double*
   ps.n = n; ps.kl = kl; ps.P = P; ps.nrhs = nrhs;
   ps.wr = wr; ps.wi = wi; ps.sw = sw; ps.ipiv = ipiv; ps.sp = sp;
   ps.us = slot_us(n, kl, aux);
+  ps.t4 = slot_t4(n, kl, aux);
   ps.sa = sa;
   ps.xr = xr; ps.xi = xi; ps.ldx = ldx; ps.sx = sx;
   ps.fr = yr; ps.fi = yi; ps.ldf = ldy; ps.sf = sy_;
