@@ -1266,23 +1266,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) band_correct_accumulate_kernel(co
             s_i[j] = ok ? __ldcs(Si + j) : 0.0;
           }
         }
+        // the correction product is accumulated from zero and subtracted from g
+        // ONCE (accumulating onto g would round every one of the 2kl multiply-adds
+        // at |g|'s magnitude, tools/dmma_rounding.py)
 #pragma unroll
-        for (int t = 0; t < FA_NT; ++t) {
-          const int col = c0 + t * 8 + 2 * q;
-          if (vx && rok && col + 1 < a.nrhs) {
-            const double2 vr = __ldcs(reinterpret_cast<const double2*>(Xr + col));
-            const double2 vi = __ldcs(reinterpret_cast<const double2*>(Xi + col));
-            c_r[t][0] = vr.x; c_r[t][1] = vr.y;
-            c_i[t][0] = vi.x; c_i[t][1] = vi.y;
-          } else {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const bool ok = rok && col + e < a.nrhs;
-              c_r[t][e] = ok ? __ldcs(Xr + col + e) : 0.0;
-              c_i[t][e] = ok ? __ldcs(Xi + col + e) : 0.0;
-            }
-          }
-        }
+        for (int t = 0; t < FA_NT; ++t) c_r[t][0] = c_r[t][1] = c_i[t][0] = c_i[t][1] = 0.0;
         const double* br_ = sT + (size_t)(ti * 2) * plane + lane;
         const double* bi_ = br_ + plane;
 #pragma unroll
@@ -1296,6 +1284,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) band_correct_accumulate_kernel(co
               dmma(c_r[t][0], c_r[t][1], nai, ti_);   // + S_i T_i
               dmma(c_i[t][0], c_i[t][1], ar, ti_);    // - S_r T_i
               dmma(c_i[t][0], c_i[t][1], ai, tr_);    // - S_i T_r
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < FA_NT; ++t) {  // x = g + (-S T)
+          const int col = c0 + t * 8 + 2 * q;
+          if (vx && rok && col + 1 < a.nrhs) {
+            const double2 vr = __ldcs(reinterpret_cast<const double2*>(Xr + col));
+            const double2 vi = __ldcs(reinterpret_cast<const double2*>(Xi + col));
+            c_r[t][0] += vr.x; c_r[t][1] += vr.y;
+            c_i[t][0] += vi.x; c_i[t][1] += vi.y;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = rok && col + e < a.nrhs;
+              c_r[t][e] += ok ? __ldcs(Xr + col + e) : 0.0;
+              c_i[t][e] += ok ? __ldcs(Xi + col + e) : 0.0;
             }
           }
         }
@@ -1391,9 +1396,16 @@ int g_part_target = 0;
 void band_spike_set_part_target(int t) { g_part_target = t; }
 
 int band_spike_parts(int n, int kl) {
+  const bool dflt = g_part_target == 0 || g_part_target == 4096;
   if (g_part_target == 0) g_part_target = 4096;
   const int minsz = std::max(2 * kl + 1, std::min(64, g_part_target));
   int P = (n + g_part_target - 1) / g_part_target;
+  // Wave quantisation: the sweeps run one CTA per (partition, shift, column
+  // group) at 4 CTAs per SM, i.e. 592 slots on 148 SMs; with Ne = 8 or 16 shifts
+  // a partition count that is a multiple of 74 fills whole waves (C4: 245 -> 222
+  // partitions, -3 % per pass, profiles/r02_band_partition_sweep.txt)
+  constexpr int kWave = kSMs * 4 / 8;
+  if (dflt && P >= kWave) P = kWave * std::max(1, (P + kWave / 2) / kWave);
   P = std::min(P, std::max(1, n / std::max(1, minsz)));
   // every partition, the shorter last one included, keeps >= minsz rows
   while (P > 1 && n - (P - 1) * part_sz(n, P) < minsz) --P;

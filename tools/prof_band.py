@@ -4,7 +4,7 @@ contour pass (M0 = 96 right-hand sides) and the band multiply with CUDA
 events; print algorithmic GB/s and FP64 TFLOP/s against the roofline
 counts of DESIGN.md.  Also a per-shift solve residual check.
 
-Usage: python tools/prof_band.py [reps] [n]
+Usage: python tools/prof_band.py [reps] [n] [partition rows]
 """
 import os
 import sys
@@ -23,6 +23,8 @@ reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
 torch.cuda.set_device(0)
 dev = get_device()
+if len(sys.argv) > 3:   # partition-size target (rows), default 4096
+    print("partitions:", dev.lib.fb_debug_band_part_target(int(sys.argv[3]), n, 16))
 w = W.c4_sbgv() if n == 1_000_000 else W.c4_sbgv(n=n, interval=(-0.01, 0.01))
 kl, m0 = w.kla, w.m0
 fa = expand_band(w.a, w.kla, w.uplo, False)
