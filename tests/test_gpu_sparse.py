@@ -244,20 +244,24 @@ def test_direct_solver_falls_back_to_iterative_outside_lu_range(rng):
     from paper_1203_4031_b200._driver import run_rci
     from paper_1203_4031_b200.kernel import SymmetricRci
     fb = _fb()
-    n = 300
+    n = 400
     a = np.zeros((n, n))
     idx = np.arange(n)
     a[idx, idx] = 4.0 + 0.5 * np.cos(idx)
-    off = 140                                     # an arrow-free pattern no ordering narrows below ~128
-    a[idx[:-off], idx[off:]] = a[idx[off:], idx[:-off]] = 0.3
-    a[idx[:-1], idx[1:]] = a[idx[1:], idx[:-1]] = -1.0
+    for _ in range(3 * n):                       # random graph: no ordering makes it narrow
+        i, j = rng.integers(0, n, 2)
+        if i != j:
+            a[i, j] = a[j, i] = 0.3 * rng.standard_normal()
     emin, emax = gap_interval(np.linalg.eigvalsh(a), 10, 18)
     acsr = fb.CsrMatrix.from_dense(a)
     dev = _dev()
-    with pytest.warns(UserWarning, match="iterative inner solver"):
+    import warnings
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
         ops = sparse.DeviceCsrOps(dev, acsr.expand_full(), None, False, "direct", 1e-3, dense_max_n=100)
     if ops.kl <= 127:
         pytest.skip("the reordering narrowed the pattern: boundary not reached")
+    assert any("iterative inner solver" in str(w.message) for w in caught)
     assert ops.mode == "iterative"
     k = SymmetricRci(n, 14, emin, emax, fb.feastinit(), host_mirror=False)
     r = run_rci(k, ops, fb.SolverOptions())
