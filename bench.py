@@ -123,6 +123,11 @@ class ClockSampler:
         return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in self.BITS]
 
     def _loop(self):
+        # NVML queries take the driver lock for tens of ms and stall the launching
+        # thread (a +40-60 ms step whenever one lands inside it): first sample
+        # 0.15 s into the timed region, then one per second
+        if self._stop.wait(0.15):
+            return
         while not self._stop.is_set():
             try:
                 if self._nvml is not None:
@@ -135,7 +140,7 @@ class ClockSampler:
                         self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(1.0)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._loop, daemon=True)

@@ -352,6 +352,51 @@ __global__ void __launch_bounds__(NT, 2) zgemm_fast_kernel(GemmParams p) {
     }
   }
   cp_async_wait<0>();
+  if (MODE == 1) {
+    // C += product: the loads of a half tile are issued together before any add
+    // or store (cre/cim may alias as far as the compiler knows, so a plain
+    // "c += v" loop serialises 32 load-add-store round trips per thread), as
+    // 16-byte accesses where the row pair is aligned
+    const bool v16 = (p.cs0 & 1) == 0 && ((uintptr_t)cre & 15) == 0 && ((uintptr_t)cim & 15) == 0;
+#pragma unroll
+    for (int a0 = 0; a0 < 4; a0 += 2) {
+      double2 lr[2][NB_], li[2][NB_];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < NB_; ++b) {
+          const int i = m0 + wm + (a0 + a) * 8 + (lane >> 2);
+          const int j = n0 + wn + b * 8 + 2 * (lane & 3);
+          const long long c = (long long)i * p.cs0 + j;
+          lr[a][b] = li[a][b] = make_double2(0.0, 0.0);
+          if (i < p.m && j + 1 < p.n && v16) {
+            lr[a][b] = *reinterpret_cast<const double2*>(cre + c);
+            li[a][b] = *reinterpret_cast<const double2*>(cim + c);
+          } else if (i < p.m) {
+            if (j < p.n) { lr[a][b].x = cre[c]; li[a][b].x = cim[c]; }
+            if (j + 1 < p.n) { lr[a][b].y = cre[c + 1]; li[a][b].y = cim[c + 1]; }
+          }
+        }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < NB_; ++b) {
+          const int i = m0 + wm + (a0 + a) * 8 + (lane >> 2);
+          const int j = n0 + wn + b * 8 + 2 * (lane & 3);
+          const long long c = (long long)i * p.cs0 + j;
+          const double2 orr = make_double2(lr[a][b].x + accr[a0 + a][b][0], lr[a][b].y + accr[a0 + a][b][1]);
+          const double2 oi = make_double2(li[a][b].x + acci[a0 + a][b][0], li[a][b].y + acci[a0 + a][b][1]);
+          if (i < p.m && j + 1 < p.n && v16) {
+            *reinterpret_cast<double2*>(cre + c) = orr;
+            *reinterpret_cast<double2*>(cim + c) = oi;
+          } else if (i < p.m) {
+            if (j < p.n) { cre[c] = orr.x; cim[c] = oi.x; }
+            if (j + 1 < p.n) { cre[c + 1] = orr.y; cim[c + 1] = oi.y; }
+          }
+        }
+    }
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -363,11 +408,6 @@ __global__ void __launch_bounds__(NT, 2) zgemm_fast_kernel(GemmParams p) {
         if (i >= p.m || j >= p.n) continue;
         const long long c = (long long)i * p.cs0 + j;
         const double vr = accr[a][b][e], vi = acci[a][b][e];
-        if (MODE == 1) {
-          cre[c] += vr;
-          cim[c] += vi;
-          continue;
-        }
         double outr = p.alpha_re * vr - p.alpha_im * vi;
         double outi = p.alpha_re * vi + p.alpha_im * vr;
         if (p.beta_re != 0.0 || p.beta_im != 0.0) {

@@ -11,13 +11,17 @@ python tools/prof_lub.py 4096 1 3 >> $O/r02_final_lub.txt 2>&1
 python tools/prof_reduced.py > $O/r02_final_reduced.txt 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file $O/r02_final_lu_metrics.csv python tools/prof_lub.py 4096 8 1 > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02_final_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+R=/tmp/fb_ncu; mkdir -p $R   # reports stay on the box (large); only the briefs come back
 NCU="ncu --set full --clock-control none --import-source on -f"
-$NCU -k regex:zgemm_fast -c 1 -o $O/r02_final_zgemm_trailing python tools/prof_lub.py 4096 8 1 > /dev/null 2>&1
-$NCU -k regex:sweep_kernel -c 1 -o $O/r02_final_sweep python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-banded > /dev/null 2>&1
-$NCU -k regex:panel_cluster -s 40 -c 1 -o $O/r02_final_panel python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-banded > /dev/null 2>&1
-$NCU -k regex:band_psolve_fwd -s 2 -c 1 -o $O/r02_final_band_fwd python tools/prof_band.py 1 > /dev/null 2>&1
-$NCU -k regex:band_psolve_bwd_t4 -s 2 -c 1 -o $O/r02_final_band_bwd python tools/prof_band.py 1 > /dev/null 2>&1
-$NCU -k regex:band_correct_accumulate -s 1 -c 1 -o $O/r02_final_band_fused python tools/prof_band.py 1 > /dev/null 2>&1
-$NCU -k regex:band_rsolve -c 1 -o $O/r02_final_band_rsolve python tools/prof_band.py 1 > /dev/null 2>&1
-$NCU -k regex:band_matvec -c 1 -o $O/r02_final_band_matvec python tools/prof_band.py 1 > /dev/null 2>&1
-ls $O/r02_final_*
+$NCU -k regex:zgemm_fast -c 1 -o $R/zgemm_trailing python tools/prof_lub.py 4096 8 1 > /dev/null 2>&1
+$NCU -k regex:sweep_kernel -c 1 -o $R/sweep python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-banded > /dev/null 2>&1
+$NCU -k regex:panel_cluster -s 40 -c 1 -o $R/panel python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-banded > /dev/null 2>&1
+$NCU -k regex:band_psolve_fwd -s 2 -c 1 -o $R/band_fwd python tools/prof_band.py 1 > /dev/null 2>&1
+$NCU -k regex:band_psolve_bwd_t4 -s 2 -c 1 -o $R/band_bwd python tools/prof_band.py 1 > /dev/null 2>&1
+$NCU -k regex:band_correct_accumulate -s 1 -c 1 -o $R/band_fused python tools/prof_band.py 1 > /dev/null 2>&1
+$NCU -k regex:band_rsolve -c 1 -o $R/band_rsolve python tools/prof_band.py 1 > /dev/null 2>&1
+$NCU -k regex:band_matvec -c 1 -o $R/band_matvec python tools/prof_band.py 1 > /dev/null 2>&1
+for k in zgemm_trailing sweep panel band_fwd band_bwd band_fused band_rsolve band_matvec; do
+  echo "## $k"; python tools/ncu_brief.py $R/$k.ncu-rep; python tools/ncu_opmix.py $R/$k.ncu-rep
+done > $O/r02_ncu_final_kernels.txt 2>&1
+ls -la $O/r02_final_* $O/r02_ncu_final_kernels.txt
