@@ -272,6 +272,7 @@ def banded_leg(dev, torch, reps=5):
     t_mvb = timed(lambda: ops.multiply_b(Y, X))
     del ops, FA, FB, FBc, Y, Q, X
     torch.cuda.empty_cache()
+    fb.feast_sb(w.a, w.kla, w.emin, w.emax, m0, b=w.b, klb=w.klb, uplo=w.uplo, fpm=w.fpm())   # warm-up (allocations)
     a, b = _events(torch)
     a.record()
     r = fb.feast_sb(w.a, w.kla, w.emin, w.emax, m0, b=w.b, klb=w.klb, uplo=w.uplo, fpm=w.fpm())
@@ -452,7 +453,7 @@ def run_gpu(args):
             # capture of the same workload (tools/prof_final.sh -> profiles/), or null
             traffic = None
             try:
-                with open(os.path.join(ROOT, "profiles", "r01_lu_traffic.json")) as f:
+                with open(os.path.join(ROOT, "profiles", "r02_lu_traffic.json")) as f:
                     tj = json.load(f)
                 if tj.get("n") == n and tj.get("count") == w.ne and world == 1:
                     traffic = tj["dram_bytes_per_call"]
