@@ -1268,7 +1268,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) band_correct_accumulate_kernel(co
         }
         // the correction product is accumulated from zero and subtracted from g
         // ONCE (accumulating onto g would round every one of the 2kl multiply-adds
-        // at |g|'s magnitude, tools/dmma_rounding.py)
+        // at |g|'s magnitude, tools/dmma_rounding.py); the loads of g are issued
+        // before the products so their latency hides behind the DMMAs
+        double g_r[FA_NT][2], g_i[FA_NT][2];
+#pragma unroll
+        for (int t = 0; t < FA_NT; ++t) {
+          const int col = c0 + t * 8 + 2 * q;
+          if (vx && rok && col + 1 < a.nrhs) {
+            const double2 vr = __ldcs(reinterpret_cast<const double2*>(Xr + col));
+            const double2 vi = __ldcs(reinterpret_cast<const double2*>(Xi + col));
+            g_r[t][0] = vr.x; g_r[t][1] = vr.y;
+            g_i[t][0] = vi.x; g_i[t][1] = vi.y;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = rok && col + e < a.nrhs;
+              g_r[t][e] = ok ? __ldcs(Xr + col + e) : 0.0;
+              g_i[t][e] = ok ? __ldcs(Xi + col + e) : 0.0;
+            }
+          }
+        }
 #pragma unroll
         for (int t = 0; t < FA_NT; ++t) c_r[t][0] = c_r[t][1] = c_i[t][0] = c_i[t][1] = 0.0;
         const double* br_ = sT + (size_t)(ti * 2) * plane + lane;
@@ -1288,22 +1307,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) band_correct_accumulate_kernel(co
           }
         }
 #pragma unroll
-        for (int t = 0; t < FA_NT; ++t) {  // x = g + (-S T)
-          const int col = c0 + t * 8 + 2 * q;
-          if (vx && rok && col + 1 < a.nrhs) {
-            const double2 vr = __ldcs(reinterpret_cast<const double2*>(Xr + col));
-            const double2 vi = __ldcs(reinterpret_cast<const double2*>(Xi + col));
-            c_r[t][0] += vr.x; c_r[t][1] += vr.y;
-            c_i[t][0] += vi.x; c_i[t][1] += vi.y;
-          } else {
+        for (int t = 0; t < FA_NT; ++t)  // x = g + (-S T)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const bool ok = rok && col + e < a.nrhs;
-              c_r[t][e] += ok ? __ldcs(Xr + col + e) : 0.0;
-              c_i[t][e] += ok ? __ldcs(Xi + col + e) : 0.0;
-            }
+          for (int e = 0; e < 2; ++e) {
+            c_r[t][e] += g_r[t][e];
+            c_i[t][e] += g_i[t][e];
           }
-        }
         const double cr = a.cr[t0 + ti], ci = a.ci[t0 + ti], hh = a.h[t0 + ti];
 #pragma unroll
         for (int t = 0; t < FA_NT; ++t)
@@ -1654,13 +1663,13 @@ cudaError_t band_spike_solve_accumulate(int count, int n, int kl, int nrhs, cons
   static DevOnce cfg;
   if (cfg.first()) {
     const int mx = (int)(sizeof(double) * FA_MAXG * 2 * FA_KS * FA_NT * 32);
-    cudaFuncSetAttribute(band_correct_accumulate_kernel<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(band_correct_accumulate_kernel<false, 384>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(band_correct_accumulate_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   }
   if (cq)
     band_correct_accumulate_kernel<true, 256><<<grid, 256, smem, st>>>(fa);
   else
-    band_correct_accumulate_kernel<false, 512><<<grid, 512, smem, st>>>(fa);
+    band_correct_accumulate_kernel<false, 384><<<grid, 384, smem, st>>>(fa);
   count_launch();
   return cudaGetLastError();
 }

@@ -305,3 +305,21 @@ def test_non_resident_factors_host_tier(monkeypatch):
     s = max(abs(lo), abs(hi))
     assert np.abs(host.e[:host.m] - full.e[:full.m]).max() <= 1e-12 * s
     assert np.array_equal(host.e[:host.m], refac.e[:refac.m])
+
+
+@pytest.mark.skipif(__import__("torch").cuda.device_count() < 2, reason="needs 2 GPUs in one process")
+def test_two_devices_in_one_process():
+    """Per-device kernel attributes (shared-memory opt-in, cluster sizes) are set
+    once per DEVICE: a second GPU driven from the same process gives the same
+    results as the first."""
+    import paper_1203_4031_b200 as fb
+    rng = np.random.default_rng(77)
+    n = 300
+    g = rng.standard_normal((n, n))
+    a = (g + g.T) / (2 * np.sqrt(n))
+    ev = np.linalg.eigvalsh(a)
+    lo, hi = 0.5 * (ev[139] + ev[140]), 0.5 * (ev[159] + ev[160])
+    r0 = fb.feast_sy(a, lo, hi, 40, device=0)
+    r1 = fb.feast_sy(a, lo, hi, 40, device=1)
+    assert r0.info == r1.info == 0 and r0.m == r1.m == 20
+    assert np.array_equal(r0.e[:20], r1.e[:20])

@@ -247,6 +247,28 @@ def test_residuals_match_oracle(dev):
     assert np.abs(got[ok] - ref[ok]).max() <= 1e-13 * np.abs(ref[ok]).max()
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_residual_sums_over_row_blocks(dev, cplx):
+    """fb_residual_sums (multi-GPU row sharding): the per-block numerator /
+    denominator sums add up to _column_residuals (kernel.py:147-153)."""
+    rng = np.random.default_rng(55)
+    n, m = 1100, 17
+    ax = rng.standard_normal((n, m)) + (1j * rng.standard_normal((n, m)) if cplx else 0)
+    bx = rng.standard_normal((n, m)) + (1j * rng.standard_normal((n, m)) if cplx else 0)
+    lam = rng.standard_normal(m)
+    AX, BX = dev.upload(ax, cplx=cplx), dev.upload(bx, cplx=cplx)
+    lt = dev.torch.tensor(lam, device=dev.tdev)
+    tot = np.zeros(2 * m)
+    for r0, r1 in ((0, 367), (367, 733), (733, n)):
+        st = dev.torch.empty(2 * m, dtype=dev.torch.float64, device=dev.tdev)
+        dev.residual_sums(AX.rows_view(r0, r1), BX.rows_view(r0, r1), lt.data_ptr(), 0.7, st.data_ptr())
+        tot += st.cpu().numpy()
+    ref = O.column_residuals(ax, bx, lam, 0.7)
+    got = tot[0::2] / tot[1::2]
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert np.allclose(tot[1::2], np.abs(0.7 * bx).sum(0), rtol=1e-13)
+
+
 def test_symmetrize(dev):
     rng = np.random.default_rng(6)
     a = rng.standard_normal((19, 19)) + 1j * rng.standard_normal((19, 19))
