@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfeastb200.so")
-SOURCES = ["capi.cu", "gemm.cu", "lu.cu", "panel.cu", "trsm.cu", "misc.cu", "reduced.cu", "reduced_cluster.cu", "band.cu", "band_spike.cu", "csr.cu"]
+SOURCES = ["capi.cu", "gemm.cu", "gemm_tma.cu", "lu.cu", "panel.cu", "trsm.cu", "misc.cu", "reduced.cu", "reduced_cluster.cu", "band.cu", "band_spike.cu", "csr.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-cudart", "static"]
 if os.environ.get("FB_BUILD_PROFILE"):   # in-kernel phase probes (tools/prof_lu.py PANEL_PROF=1)

@@ -48,4 +48,14 @@ inline cudaError_t gemm(int cplx, int m, int n, int k, Opnd a, Opnd b, double* c
   return gemm_launch(cplx, p, st);
 }
 
+// TMA-fed trailing update of the blocked LU (gemm_tma.cu): tensor maps over the
+// strided batch of factor matrices, made once per factorization
+struct LuTmaMaps {
+  alignas(64) unsigned char m[4 * 128];  // 4 CUtensorMap: (re, im) x (A box, B box)
+  bool ok = false;
+};
+bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, long long ld, long long slu, int count);
+cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long long ld, long long slu, int count, int m,
+                            int n, int k, int arow, int acol, int brow, int bcol, int crow, int ccol, cudaStream_t st);
+
 }  // namespace fb

@@ -293,6 +293,9 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
   };
   fill_int_kernel<<<ceil_div(B, 128), 128, 0, st>>>(f.info, 0x7fffffff, B);
   count_launch();
+  // tensor maps over the batch of factor matrices: the bulk trailing updates are TMA-fed (gemm_tma.cu)
+  LuTmaMaps tma;
+  lu_tma_maps_make(&tma, re, im, n, ld, slu, B);
   // factor outer block k on stream q (panels, in-block interchanges and updates)
   auto block_factor = [&](int k, cudaStream_t q) -> cudaError_t {
     const int nb = std::min(NB, n - k);
@@ -359,6 +362,8 @@ cudaError_t zgetrf_batched(int n, const LuBatch& f, char* scratch, cudaStream_t 
       }
     }
     const int below = n - (k + nb);
+    if (tma.ok && nb % 16 == 0 && (c_lo & 1) == 0 && below >= 64)
+      return lu_trailing_tma(tma, re, im, ld, slu, B, below, w, nb, k + nb, k, k, c_lo, k + nb, c_lo, q);
     return gemm(1, below, w, nb, op_n(re + (long long)(k + nb) * ld + k, im + (long long)(k + nb) * ld + k, ld),
                 op_n(re + (long long)k * ld + c_lo, im + (long long)k * ld + c_lo, ld),
                 re + (long long)(k + nb) * ld + c_lo, im + (long long)(k + nb) * ld + c_lo, ld, -1.0, 0.0, 1.0,
