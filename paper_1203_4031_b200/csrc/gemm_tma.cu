@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -60,10 +61,12 @@ __global__ void __launch_bounds__(TNT, 2)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_constant__ CUtensorMap map_aim,
                  const __grid_constant__ CUtensorMap map_bre, const __grid_constant__ CUtensorMap map_bim,
                  const TmaArgs p) {
-  extern __shared__ __align__(1024) unsigned char tsm[];
+  extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ __align__(8) unsigned long long full[TST], empty[TST];
-  // dynamic shared memory is 1024-byte aligned by declaration; the swizzle is a function of the address
-  unsigned char* base = tsm;
+  // the 128-byte swizzle is a function of the shared-memory ADDRESS: the tiles must start on a
+  // 1024-byte boundary of the shared window, wherever the CTA's dynamic region happens to begin
+  // (it is not 1024-aligned when the SM is shared with CTAs of other kernels)
+  unsigned char* base = tsm + ((1024u - (smem_u32(tsm) & 1023u)) & 1023u);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN, bz = blockIdx.z;
@@ -247,7 +250,7 @@ cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long lon
   a.cre = re + (long long)crow * ld + ccol;
   a.cim = im + (long long)crow * ld + ccol;
   a.ldc = ld; a.sc = slu;
-  const size_t smem = (size_t)TST * STAGE_BYTES;
+  const size_t smem = (size_t)TST * STAGE_BYTES + 1024;  // + slack to align the tiles to 1024 bytes
   static DevOnce cfg;
   if (cfg.first()) cudaFuncSetAttribute(zgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   zgemm_tma_kernel<<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mp[2], mp[3], a);

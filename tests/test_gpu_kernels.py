@@ -350,3 +350,25 @@ def test_expand_band_device_bitexact(dev, uplo, herm, kl, kl_to):
     got = expand_band_device(dev, ab, kl, uplo, herm, kl_to)
     g = got.plane(0).cpu().numpy() + (1j * got.plane(1).cpu().numpy() if herm else 0)
     assert np.array_equal(g, want)
+
+
+@pytest.mark.parametrize("n,count", [(1792, 4), (1100, 8)])
+def test_batched_lu_tma_trailing_update_with_lookahead(dev, n, count):
+    """Batched shifted LU large enough for the TMA-fed trailing update to run
+    concurrently with the look-ahead panels of the next block (gemm_tma.cu):
+    every shift's solve against numpy.  (The swizzled tiles must be aligned at
+    run time: a CTA's dynamic shared memory is not 1024-byte aligned when the
+    SM is shared with other kernels' CTAs -- n = 1792 x 4 shifts caught it.)"""
+    from paper_1203_4031_b200.dense import DeviceDenseOps
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    a = (a + a.conj().T) / 2
+    ops = DeviceDenseOps(dev, dev.upload(a, cplx=True), None, True)
+    zs = [complex(0.3 * k, 0.5 + 0.1 * k) for k in range(count)]
+    ops.prefactorize(zs)
+    y = rng.standard_normal((n, 12)) + 1j * rng.standard_normal((n, 12))
+    ops.solve_pass(dev.upload(y, cplx=True), False)
+    for z in zs:
+        x = dev.download(ops.pass_result(z, False))
+        s = z * np.eye(n) - a
+        assert np.abs(s @ x - y).max() <= 1e-13 * np.abs(s).max() * np.abs(x).max() * n
