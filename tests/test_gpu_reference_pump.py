@@ -136,6 +136,11 @@ def test_feastlib_run_rci_with_b200_ops_scaled_configs(fl, tag):
     m, loop, info, _ = (int(v) for v in g["scal"])
     s = max(abs(w.emin), abs(w.emax))
     assert (r.info, r.m) == (info, m)
-    assert abs(r.loop - loop) <= 1
+    # c3s shrinks M0 at loop 0 by a rounding-level Cholesky breakdown; the loop count
+    # follows the M0 it lands on -- the reference's own map (test_gpu_drivers.REF_TRAJECTORIES)
+    from test_gpu_drivers import REF_TRAJECTORIES
+    traj = REF_TRAJECTORIES.get(tag, {int(g["scal"][3]): loop})
+    assert r.m0 in traj, (r.m0, traj)
+    assert abs(r.loop - traj[r.m0]) <= 1
     assert np.abs(r.e[:m] - g["e"][:m]).max() <= 1e-10 * s
     assert np.max(r.res[:m]) <= 1e-10

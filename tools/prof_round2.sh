@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/r02_final_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 R=/tmp/fb_ncu; mkdir -p $R   # reports stay on the box (large); only the briefs come back
 NCU="ncu --set full --clock-control none --import-source on -f"
-$NCU -k regex:zgemm_fast -c 1 -o $R/zgemm_trailing python tools/prof_lub.py 4096 8 1 > /dev/null 2>&1
+$NCU -k regex:zgemm_tma -s 10 -c 1 -o $R/zgemm_trailing python tools/prof_lub.py 4096 8 1 > /dev/null 2>&1
 $NCU -k regex:sweep_kernel -c 1 -o $R/sweep python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-banded > /dev/null 2>&1
 $NCU -k regex:panel_cluster -s 40 -c 1 -o $R/panel python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-banded > /dev/null 2>&1
 $NCU -k regex:band_psolve_fwd -s 2 -c 1 -o $R/band_fwd python tools/prof_band.py 1 > /dev/null 2>&1
