@@ -55,6 +55,14 @@ struct LuTmaMaps {
   bool ok = false;
 };
 bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, long long ld, long long slu, int count);
+// the same four maps over a batch of rows x cols planar blocks (the sweeps' right-hand sides)
+bool lu_tma_maps_make_rect(LuTmaMaps* t, const double* re, const double* im, int rows, int cols, long long ld,
+                           long long stride, int count);
+// C(m x n) -= A(m x k at A-tensor [arow][acol]) * B(k x n at B-tensor [brow][bcol]) for every batch item;
+// A tiles come from ta, B tiles from tb; k is a multiple of 16 or ends at the tensors' edge
+cudaError_t zgemm_tma_sub(const LuTmaMaps& ta, const LuTmaMaps& tb, double* cre, double* cim, long long ldc,
+                          long long sc, int count, int m, int n, int k, int arow, int acol, int brow, int bcol,
+                          cudaStream_t st);
 cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long long ld, long long slu, int count, int m,
                             int n, int k, int arow, int acol, int brow, int bcol, int crow, int ccol, cudaStream_t st);
 

@@ -215,10 +215,11 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap* m, const double* base, int n, long long ld, long long batch_stride, int count, int box_rows) {
+bool make_map(CUtensorMap* m, const double* base, int rows, int cols, long long ld, long long batch_stride, int count,
+              int box_rows) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)count};
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)count};
   const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)batch_stride * 8};
   const cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -229,14 +230,48 @@ bool make_map(CUtensorMap* m, const double* base, int n, long long ld, long long
 
 }  // namespace
 
-bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, long long ld, long long slu, int count) {
+bool lu_tma_maps_make_rect(LuTmaMaps* t, const double* re, const double* im, int rows, int cols, long long ld,
+                           long long stride, int count) {
   t->ok = false;
-  if (n < 64 || (ld & 1) || (slu & 1) || ((uintptr_t)re & 15) || ((uintptr_t)im & 15)) return false;
+  if (rows < 1 || cols < 1 || (ld & 1) || (stride & 1) || ((uintptr_t)re & 15) || ((uintptr_t)im & 15)) return false;
+  if (count > 1 && stride <= 0) return false;
   static_assert(sizeof(t->m) >= 4 * sizeof(CUtensorMap), "LuTmaMaps storage");
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(t->m);
-  t->ok = make_map(m + 0, re, n, ld, slu, count, TM) && make_map(m + 1, im, n, ld, slu, count, TM) &&
-          make_map(m + 2, re, n, ld, slu, count, TK) && make_map(m + 3, im, n, ld, slu, count, TK);
+  const long long bs = count > 1 ? stride : (long long)rows * ld;  // any valid stride for a single item
+  t->ok = make_map(m + 0, re, rows, cols, ld, bs, count, TM) && make_map(m + 1, im, rows, cols, ld, bs, count, TM) &&
+          make_map(m + 2, re, rows, cols, ld, bs, count, TK) && make_map(m + 3, im, rows, cols, ld, bs, count, TK);
   return t->ok;
+}
+
+bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, long long ld, long long slu, int count) {
+  if (n < 64) {
+    t->ok = false;
+    return false;
+  }
+  return lu_tma_maps_make_rect(t, re, im, n, n, ld, slu, count);
+}
+
+static void tma_kernel_config(size_t smem) {
+  static DevOnce cfg;
+  if (cfg.first()) cudaFuncSetAttribute(zgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t zgemm_tma_sub(const LuTmaMaps& ta, const LuTmaMaps& tb, double* cre, double* cim, long long ldc,
+                          long long sc, int count, int m, int n, int k, int arow, int acol, int brow, int bcol,
+                          cudaStream_t st) {
+  if (m <= 0 || n <= 0 || k <= 0) return cudaSuccess;
+  if (!ta.ok || !tb.ok || (ldc & 1) || ((uintptr_t)cre & 15) || ((uintptr_t)cim & 15)) return cudaErrorNotSupported;
+  const CUtensorMap* mp = reinterpret_cast<const CUtensorMap*>(ta.m);
+  const CUtensorMap* mq = reinterpret_cast<const CUtensorMap*>(tb.m);
+  TmaArgs a{};
+  a.m = m; a.n = n; a.k = ceil_div(k, TK) * TK;  // a K tail reads zero-filled entries past the tensors' edge
+  a.arow = arow; a.acol = acol; a.brow = brow; a.bcol = bcol;
+  a.cre = cre; a.cim = cim; a.ldc = ldc; a.sc = sc;
+  const size_t smem = (size_t)TST * STAGE_BYTES + 1024;
+  tma_kernel_config(smem);
+  zgemm_tma_kernel<<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mq[2], mq[3], a);
+  count_launch();
+  return cudaGetLastError();
 }
 
 // C(m x n at M[crow][ccol]) -= A(m x k at M[arow][acol]) * B(k x n at M[brow][bcol]) for every batch item
@@ -251,8 +286,7 @@ cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long lon
   a.cim = im + (long long)crow * ld + ccol;
   a.ldc = ld; a.sc = slu;
   const size_t smem = (size_t)TST * STAGE_BYTES + 1024;  // + slack to align the tiles to 1024 bytes
-  static DevOnce cfg;
-  if (cfg.first()) cudaFuncSetAttribute(zgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tma_kernel_config(smem);
   zgemm_tma_kernel<<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mp[2], mp[3], a);
   count_launch();
   return cudaGetLastError();

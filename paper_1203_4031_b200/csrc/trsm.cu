@@ -41,6 +41,7 @@
 #include <utility>
 
 #include "common.cuh"
+#include "gemm.cuh"
 #include "trsm.cuh"
 
 namespace cg = cooperative_groups;
@@ -58,6 +59,8 @@ constexpr int PA = 36;                 // operator tile pitch (= 4 mod 16: confl
 constexpr int XP = CW + 4;             // X tile pitch (= 4 mod 16)
 constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 operator tile in shared memory
 constexpr int XTILE = 2 * BS * XP;     // doubles per planar 32 x CW X tile
+constexpr int SOB = 256;               // outer block of the blocked direct sweeps (= K of the TMA update)
+constexpr int SOB_MIN_N = 6144;        // below, the per-block sweep launches cost more than the faster updates gain (C2: +4 %)
 constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): T re/im [32][32], inv re/im [32] (padded)
 
 struct SweepArgs {
@@ -70,6 +73,7 @@ struct SweepArgs {
   long long ldx;
   long long slu, sdinv, sx;  // batch strides (item b: + b * stride)
   int *upd, *fin;             // dataflow counters [count][nblk][C] (zeroed per launch)
+  int gblk0, gnblk;           // sub-block sweeps: operator index of block 0 and the whole matrix's block count
 };
 
 __device__ __forceinline__ void offset_item(SweepArgs& a, long long b) {
@@ -257,7 +261,7 @@ __device__ __forceinline__ void acc_store(const SweepArgs& a, int b, int c0, con
 }
 
 __device__ __forceinline__ const double* op_ptr(const SweepArgs& a, int b) {
-  return a.gmat + ((size_t)a.variant * a.nblk + b) * GM_BLK;
+  return a.gmat + ((size_t)a.variant * a.gnblk + a.gblk0 + b) * GM_BLK;
 }
 
 // The diagonal-block operator of block b in processing coordinates (tdiag_kernel):
@@ -618,7 +622,7 @@ size_t gmat_doubles(int n) { return (size_t)4 * ceil_div(n, BS) * GM_BLK; }
 cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, long long ld, long long slu,
                         const double* dinv, long long sdinv, double* gmat, cudaStream_t st) {
   SweepArgs a{};
-  a.n = n; a.nblk = ceil_div(n, BS); a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
+  a.n = n; a.nblk = ceil_div(n, BS); a.gnblk = a.nblk; a.gblk0 = 0; a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.slu = slu; a.sdinv = sdinv; a.sx = 0;
   tdiag_kernel<<<dim3(a.nblk, 4, count), GT, 0, st>>>(a);
   count_launch();
@@ -628,7 +632,7 @@ cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, 
 static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                                     long long ld, long long slu, const double* dinv, const double* gmat,
                                     long long sdinv, double* xre, double* xim, long long ldx, long long sx,
-                                    cudaStream_t st);
+                                    cudaStream_t st, int gblk0 = 0, int gnblk = -1);
 
 // The right-hand sides of all items are read and rewritten by every step
 // (right-looking accumulators), so the batch is swept in groups whose
@@ -638,6 +642,36 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
                          long long ld, long long slu, const double* dinv, const double* gmat, long long sdinv,
                          double* xre, double* xim, long long ldx, long long sx, cudaStream_t st) {
   if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
+  // Direct sweeps (L forward, U backward) of large matrices run BLOCKED: the
+  // dataflow sweep above solves one 256-row diagonal block, then the update of
+  // all pending rows, X_pend -= M(pend, block) X_block, is ONE TMA-fed ZGEMM
+  // with K = 256 (95 % of the DMMA pipe against ~55 % for the streamed rank-32
+  // tile updates, and 8x less traffic on X).  The adjoint sweeps keep the
+  // streamed form: their update needs M^H tiles, and the TMA kernel fed with
+  // transposed 16 x 16 boxes (16 bulk loads per stage) returned stale B boxes
+  // intermittently with two CTAs per SM.
+  if (variant < 2 && n >= SOB_MIN_N && (ld % 2) == 0 && (ldx % 2) == 0 && (slu % 2) == 0 && (sx % 2) == 0) {
+    LuTmaMaps ma, mx;
+    if (lu_tma_maps_make(&ma, lre, lim, n, ld, slu, count) &&
+        lu_tma_maps_make_rect(&mx, xre, xim, n, nrhs, ldx, sx, count)) {
+      const int nob = ceil_div(n, SOB), gn = ceil_div(n, BS);
+      for (int t = 0; t < nob; ++t) {
+        const int ob = (variant == 0 ? t : nob - 1 - t) * SOB, rows = std::min(SOB, n - ob);
+        cudaError_t e = sweep_launch_one(variant, rows, nrhs, count, lre + (long long)ob * ld + ob,
+                                         lim + (long long)ob * ld + ob, ld, slu, dinv, gmat, sdinv,
+                                         xre + (long long)ob * ldx, xim + (long long)ob * ldx, ldx, sx, st, ob / BS, gn);
+        if (e != cudaSuccess) return e;
+        const int pend0 = variant == 0 ? ob + rows : 0, pend = variant == 0 ? n - (ob + rows) : ob;
+        if (pend > 0) {
+          // C = X[pend0.., :], A = M[pend0.., ob..ob+rows), B = X[ob..ob+rows, :]
+          e = zgemm_tma_sub(ma, mx, xre + (long long)pend0 * ldx, xim + (long long)pend0 * ldx, ldx, sx, count, pend,
+                            nrhs, rows, pend0, ob, ob, 0, st);
+          if (e != cudaSuccess) return e;
+        }
+      }
+      return cudaSuccess;
+    }
+  }
   const double budget = 1048576.0 * 64.0;  // sweep working set per launch: about half the 126 MB L2
   const double item = 16.0 * (double)n * (double)nrhs;
   int group = count;
@@ -658,9 +692,10 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
 static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                                     long long ld, long long slu, const double* dinv, const double* gmat,
                                     long long sdinv, double* xre, double* xim, long long ldx, long long sx,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, int gblk0, int gnblk) {
   SweepArgs a{};
   a.n = n; a.nrhs = nrhs; a.nblk = ceil_div(n, BS); a.variant = variant;
+  a.gblk0 = gblk0; a.gnblk = gnblk < 0 ? a.nblk : gnblk;
   a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.xre = xre; a.xim = xim; a.ldx = ldx;
   a.slu = slu; a.sdinv = sdinv; a.sx = sx;

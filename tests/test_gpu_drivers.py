@@ -95,7 +95,8 @@ def test_helloworld_golden_values(capsys):
 # Cholesky breakdown of the rank-deficient Q^H B Q (kernel.py:385-400) the
 # breakdown index is decided by rounding, and the loop count follows it; the
 # +-1 bar then applies to the reference trajectory with the same final M0.
-REF_TRAJECTORIES = {"c3s": {30: 6, 29: 4, 28: 1}}
+# c5s: k = 0..15 (profiles/r02_c5s_ref_sensitivity.txt): M0 36 or 35, 1-2 loops.
+REF_TRAJECTORIES = {"c3s": {30: 6, 29: 4, 28: 1}, "c5s": {36: 2, 35: 2}}
 
 
 @pytest.mark.parametrize("tag", ["c1s", "c2s", "c3s", "c5s", "c4s"])

@@ -136,7 +136,7 @@ def test_feastlib_run_rci_with_b200_ops_scaled_configs(fl, tag):
     m, loop, info, _ = (int(v) for v in g["scal"])
     s = max(abs(w.emin), abs(w.emax))
     assert (r.info, r.m) == (info, m)
-    # c3s shrinks M0 at loop 0 by a rounding-level Cholesky breakdown; the loop count
+    # c3s and c5s shrink M0 at loop 0 by a rounding-level Cholesky breakdown; the loop count
     # follows the M0 it lands on -- the reference's own map (test_gpu_drivers.REF_TRAJECTORIES)
     from test_gpu_drivers import REF_TRAJECTORIES
     traj = REF_TRAJECTORIES.get(tag, {int(g["scal"][3]): loop})
