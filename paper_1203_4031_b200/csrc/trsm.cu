@@ -647,9 +647,9 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
   // all pending rows, X_pend -= M(pend, block) X_block, is ONE TMA-fed ZGEMM
   // with K = 256 (95 % of the DMMA pipe against ~55 % for the streamed rank-32
   // tile updates, and 8x less traffic on X).  The adjoint sweeps keep the
-  // streamed form: their update needs M^H tiles, and the TMA kernel fed with
-  // transposed 16 x 16 boxes (16 bulk loads per stage) returned stale B boxes
-  // intermittently with two CTAs per SM.
+  // streamed form: their update needs M^H tiles, and the two transposed-tile
+  // variants of the TMA kernel that were tried returned a wrong 16-column
+  // sub-tile intermittently with two CTAs per SM.
   if (variant < 2 && n >= SOB_MIN_N && (ld % 2) == 0 && (ldx % 2) == 0 && (slu % 2) == 0 && (sx % 2) == 0) {
     LuTmaMaps ma, mx;
     if (lu_tma_maps_make(&ma, lre, lim, n, ld, slu, count) &&
