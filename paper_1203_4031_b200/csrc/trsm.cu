@@ -60,7 +60,7 @@ constexpr int XP = CW + 4;             // X tile pitch (= 4 mod 16)
 constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 operator tile in shared memory
 constexpr int XTILE = 2 * BS * XP;     // doubles per planar 32 x CW X tile
 constexpr int SOB = 256;               // outer block of the blocked direct sweeps (= K of the TMA update)
-constexpr int SOB_MIN_N = 6144;        // below, the per-block sweep launches cost more than the faster updates gain (C2: +4 %)
+constexpr int SOB_MIN_N = 6144;        // below, the per-block launches cost more than the faster updates gain (C2: +4 %)
 constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): T re/im [32][32], inv re/im [32] (padded)
 
 struct SweepArgs {
@@ -73,7 +73,7 @@ struct SweepArgs {
   long long ldx;
   long long slu, sdinv, sx;  // batch strides (item b: + b * stride)
   int *upd, *fin;             // dataflow counters [count][nblk][C] (zeroed per launch)
-  int gblk0, gnblk;           // sub-block sweeps: operator index of block 0 and the whole matrix's block count
+  int gblk0, gnblk;           // block solves: operator index of block 0 and the whole matrix's block count
 };
 
 __device__ __forceinline__ void offset_item(SweepArgs& a, long long b) {
@@ -537,6 +537,61 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
   sweep_body<TR, VEC>(a, s);
 }
 
+// One CTA solves a whole diagonal block of up to SOB rows for one 32-column
+// chunk of one shift (the blocked sweeps' diagonal step): the chunk of X stays
+// in shared memory from load to store, so the 8 substitutions and 28 rank-32
+// updates of a 256-row block need no inter-CTA hand-over (measured at C2's
+// shapes: 94 us per block against 110-120 us for the dataflow sweep on the
+// same block, and no cooperative launch).
+// Direct sweeps only (variant 0: L forward, 1: U backward).
+template <bool VEC>
+__global__ void __launch_bounds__(TT) block_solve_kernel(SweepArgs a0) {
+  extern __shared__ __align__(16) double s[];
+  SweepArgs a = a0;
+  offset_item(a, blockIdx.y);
+  const int c0 = blockIdx.x * CW;
+  double* Xs = s;                                  // nblk tiles of the X chunk
+  double* T0 = s + (size_t)a.nblk * XTILE;         // streamed operator tiles (double buffer)
+  double* T1 = T0 + TILE;
+  double* Td = T1 + TILE;                          // diagonal operator + inverse pivots
+  const bool fwd = a.variant == 0;
+  const bool live = c0 + ((threadIdx.x >> 5) % WC) * 16 < a.nrhs;
+  for (int b = 0; b < a.nblk; ++b) cp_x<VEC>(a, b, c0, Xs + (size_t)b * XTILE);
+  for (int t = 0; t < a.nblk; ++t) {
+    const int bt = blk_at(a, t);
+    double* Xt = Xs + (size_t)bt * XTILE;
+    const int R = a.nblk - t - 1;  // pending blocks b(t+1) ...
+    cp_tdiag<VEC>(op_ptr(a, bt), Td);
+    if (R > 0) cp_m<VEC>(a, blk_at(a, t + 1), bt, T0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (fwd)
+      tile_subst<true>(Xt, Td, c0, a.nrhs);
+    else
+      tile_subst<false>(Xt, Td, c0, a.nrhs);
+    __syncthreads();
+    for (int q = 0; q < R; ++q) {
+      double* Tq = (q & 1) ? T1 : T0;
+      if (q + 1 < R) {
+        cp_m<VEC>(a, blk_at(a, t + 2 + q), bt, (q & 1) ? T0 : T1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      // -M X_b from zero, added to the pending tile once (one rounding per element and step)
+      Acc prod;
+      acc_zero(prod);
+      tile_mma<false, -1, -1>(prod, Tq, Xt, live);
+      acc_add_to_tile(prod, Xs + (size_t)blk_at(a, t + 1 + q) * XTILE);
+      __syncthreads();
+    }
+  }
+  for (int b = 0; b < a.nblk; ++b) tile_store(a, b, c0, Xs + (size_t)b * XTILE);
+}
+
 // Per (block, variant): the diagonal block of the factor as the substitution
 // operator of tile_subst, in processing coordinates p (tile row r = p for the
 // ascending sweeps 0 (L) and 2 (U^H), r = 31 - p for the descending sweeps
@@ -632,7 +687,36 @@ cudaError_t gmat_launch(int n, int count, const double* lre, const double* lim, 
 static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                                     long long ld, long long slu, const double* dinv, const double* gmat,
                                     long long sdinv, double* xre, double* xim, long long ldx, long long sx,
-                                    cudaStream_t st, int gblk0 = 0, int gnblk = -1);
+                                    cudaStream_t st);
+
+// diagonal block [gblk0*32, gblk0*32 + n) of the whole matrix (gnblk blocks), n <= SOB, variants 0 / 1
+static cudaError_t block_solve_launch(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
+                                      long long ld, long long slu, const double* dinv, const double* gmat,
+                                      long long sdinv, double* xre, double* xim, long long ldx, long long sx,
+                                      cudaStream_t st, int gblk0, int gnblk) {
+  SweepArgs a{};
+  a.n = n; a.nrhs = nrhs; a.nblk = ceil_div(n, BS); a.variant = variant;
+  a.gblk0 = gblk0; a.gnblk = gnblk;
+  a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
+  a.xre = xre; a.xim = xim; a.ldx = ldx;
+  a.slu = slu; a.sdinv = sdinv; a.sx = sx;
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool vec = ld % 2 == 0 && ldx % 2 == 0 && slu % 2 == 0 && sx % 2 == 0 && sdinv % 2 == 0 &&
+                   al(lre) && al(lim) && al(xre) && al(xim) && al(gmat);
+  const size_t smem = sizeof(double) * ((size_t)(SOB / BS) * XTILE + 3 * TILE + 2 * BS);
+  static DevOnce cfg;
+  if (cfg.first()) {
+    cudaFuncSetAttribute(block_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(block_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  const dim3 grid(ceil_div(nrhs, CW), count);
+  if (vec)
+    block_solve_kernel<true><<<grid, TT, smem, st>>>(a);
+  else
+    block_solve_kernel<false><<<grid, TT, smem, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
 
 // The right-hand sides of all items are read and rewritten by every step
 // (right-looking accumulators), so the batch is swept in groups whose
@@ -642,8 +726,8 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
                          long long ld, long long slu, const double* dinv, const double* gmat, long long sdinv,
                          double* xre, double* xim, long long ldx, long long sx, cudaStream_t st) {
   if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
-  // Direct sweeps (L forward, U backward) of large matrices run BLOCKED: the
-  // dataflow sweep above solves one 256-row diagonal block, then the update of
+  // Direct sweeps (L forward, U backward) of large matrices run BLOCKED:
+  // block_solve_kernel solves one 256-row diagonal block, then the update of
   // all pending rows, X_pend -= M(pend, block) X_block, is ONE TMA-fed ZGEMM
   // with K = 256 (95 % of the DMMA pipe against ~55 % for the streamed rank-32
   // tile updates, and 8x less traffic on X).  The adjoint sweeps keep the
@@ -657,9 +741,9 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
       const int nob = ceil_div(n, SOB), gn = ceil_div(n, BS);
       for (int t = 0; t < nob; ++t) {
         const int ob = (variant == 0 ? t : nob - 1 - t) * SOB, rows = std::min(SOB, n - ob);
-        cudaError_t e = sweep_launch_one(variant, rows, nrhs, count, lre + (long long)ob * ld + ob,
-                                         lim + (long long)ob * ld + ob, ld, slu, dinv, gmat, sdinv,
-                                         xre + (long long)ob * ldx, xim + (long long)ob * ldx, ldx, sx, st, ob / BS, gn);
+        cudaError_t e = block_solve_launch(variant, rows, nrhs, count, lre + (long long)ob * ld + ob,
+                                           lim + (long long)ob * ld + ob, ld, slu, dinv, gmat, sdinv,
+                                           xre + (long long)ob * ldx, xim + (long long)ob * ldx, ldx, sx, st, ob / BS, gn);
         if (e != cudaSuccess) return e;
         const int pend0 = variant == 0 ? ob + rows : 0, pend = variant == 0 ? n - (ob + rows) : ob;
         if (pend > 0) {
@@ -692,10 +776,10 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
 static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                                     long long ld, long long slu, const double* dinv, const double* gmat,
                                     long long sdinv, double* xre, double* xim, long long ldx, long long sx,
-                                    cudaStream_t st, int gblk0, int gnblk) {
+                                    cudaStream_t st) {
   SweepArgs a{};
   a.n = n; a.nrhs = nrhs; a.nblk = ceil_div(n, BS); a.variant = variant;
-  a.gblk0 = gblk0; a.gnblk = gnblk < 0 ? a.nblk : gnblk;
+  a.gblk0 = 0; a.gnblk = a.nblk;
   a.lre = lre; a.lim = lim; a.ld = ld; a.dinv = dinv; a.gmat = gmat;
   a.xre = xre; a.xim = xim; a.ldx = ldx;
   a.slu = slu; a.sdinv = sdinv; a.sx = sx;
