@@ -51,7 +51,7 @@ inline cudaError_t gemm(int cplx, int m, int n, int k, Opnd a, Opnd b, double* c
 // TMA-fed trailing update of the blocked LU (gemm_tma.cu): tensor maps over the
 // strided batch of factor matrices, made once per factorization
 struct LuTmaMaps {
-  alignas(64) unsigned char m[4 * 128];  // 4 CUtensorMap: (re, im) x (A box, B box)
+  alignas(64) unsigned char m[6 * 128];  // 6 CUtensorMap: (re, im) x (A box, B box, transposed-A box)
   bool ok = false;
 };
 bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, long long ld, long long slu, int count);
@@ -59,10 +59,11 @@ bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, l
 bool lu_tma_maps_make_rect(LuTmaMaps* t, const double* re, const double* im, int rows, int cols, long long ld,
                            long long stride, int count);
 // C(m x n) -= A(m x k at A-tensor [arow][acol]) * B(k x n at B-tensor [brow][bcol]) for every batch item;
-// A tiles come from ta, B tiles from tb; k is a multiple of 16 or ends at the tensors' edge
+// A tiles come from ta, B tiles from tb; k is a multiple of 16 or ends at the tensors' edge.
+// conjt: A(r, kk) = conj(A-tensor[arow + kk][acol + r]) instead (the adjoint sweeps' M^H).
 cudaError_t zgemm_tma_sub(const LuTmaMaps& ta, const LuTmaMaps& tb, double* cre, double* cim, long long ldc,
                           long long sc, int count, int m, int n, int k, int arow, int acol, int brow, int bcol,
-                          cudaStream_t st);
+                          cudaStream_t st, bool conjt = false);
 cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long long ld, long long slu, int count, int m,
                             int n, int k, int arow, int acol, int brow, int bcol, int crow, int ccol, cudaStream_t st);
 

@@ -57,12 +57,19 @@ __device__ __forceinline__ void mbar_arrive(void* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// CONJT: the A operand is the conjugate TRANSPOSE of a block of the tensor (the adjoint sweeps'
+// M^H).  Its tile is ONE un-swizzled box per plane, 16 k-rows of 64 tensor columns ([k][row],
+// 512-byte rows), so a stage is the same 10 bulk loads as the direct form; the A fragments then
+// read 4 wavefronts instead of 2 (the four k of a step share their banks), well inside the
+// shared-memory time the DMMAs leave.
+template <bool CONJT>
 __global__ void __launch_bounds__(TNT, 2)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_constant__ CUtensorMap map_aim,
                  const __grid_constant__ CUtensorMap map_bre, const __grid_constant__ CUtensorMap map_bim,
                  const TmaArgs p) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ __align__(8) unsigned long long full[TST], empty[TST];
+  __shared__ volatile unsigned sink[TNT / 32];
   // the 128-byte swizzle is a function of the shared-memory ADDRESS: the tiles must start on a
   // 1024-byte boundary of the shared window, wherever the CTA's dynamic region happens to begin
   // (it is not 1024-aligned when the SM is shared with CTAs of other kernels)
@@ -83,8 +90,13 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
   auto issue = [&](int s, int kt) {  // elected thread
     unsigned char* st = base + (size_t)s * STAGE_BYTES;
     mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-    tma_load_3d(st, &map_are, p.acol + kt * TK, p.arow + m0, bz, &full[s]);
-    tma_load_3d(st + A_BYTES, &map_aim, p.acol + kt * TK, p.arow + m0, bz, &full[s]);
+    if (!CONJT) {
+      tma_load_3d(st, &map_are, p.acol + kt * TK, p.arow + m0, bz, &full[s]);
+      tma_load_3d(st + A_BYTES, &map_aim, p.acol + kt * TK, p.arow + m0, bz, &full[s]);
+    } else {  // A(r, k) = conj(M[arow + k][acol + r])
+      tma_load_3d(st, &map_are, p.acol + m0, p.arow + kt * TK, bz, &full[s]);
+      tma_load_3d(st + A_BYTES, &map_aim, p.acol + m0, p.arow + kt * TK, bz, &full[s]);
+    }
 #pragma unroll
     for (int j = 0; j < TN / 16; ++j) {
       tma_load_3d(st + 2 * A_BYTES + j * (TK * 128), &map_bre, p.bcol + n0 + 16 * j, p.brow + kt * TK, bz, &full[s]);
@@ -123,13 +135,15 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int r = wm + t * 8 + g;
-        const int off = r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + ((kk & 1) << 3);
+        const int off = CONJT ? kk * (TM * 8) + r * 8 : r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + ((kk & 1) << 3);
         const double ar = *reinterpret_cast<const double*>(st + off);
         const double ai = *reinterpret_cast<const double*>(st + A_BYTES + off);
-        // -(A B): re += (-ar) br + ai bi, im += (-ar) bi + (-ai) br
-        x[t] = __longlong_as_double(__double_as_longlong(ar) ^ 0x8000000000000000ull);
-        y[t] = ai;
-        z[t] = __longlong_as_double(__double_as_longlong(ai) ^ 0x8000000000000000ull);
+        const double nar = __longlong_as_double(__double_as_longlong(ar) ^ 0x8000000000000000ull);
+        const double nai = __longlong_as_double(__double_as_longlong(ai) ^ 0x8000000000000000ull);
+        // -(A B): re += (-ar) br + ai bi, im += (-ar) bi + (-ai) br; conj(A) flips the sign of ai
+        x[t] = nar;
+        y[t] = CONJT ? nai : ai;
+        z[t] = CONJT ? ai : nai;
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -146,9 +160,24 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
           dmma(acci[a][b][0], acci[a][b][1], z[a], br[b]);
         }
     }
-    // this warp is done with the stage; the elected thread refills it once all 8 warps are
+    // This warp is done with the stage; the elected thread refills it once all 8 warps are.
+    // The release must not overtake the fragment loads: an mbarrier arrive orders memory
+    // operations, but ptxas places it right after the last LDS is ISSUED (the DMMAs that consume
+    // the fragments follow), and under bank-conflict replays with two CTAs per SM the refill's
+    // bulk copy was seen to overwrite a B box before a late warp's loads had read it (one
+    // wrong 16-column sub-tile, about one launch sequence in three for the transposed form).
+    // Lane 0 therefore first stores a word that depends on every accumulator: the store cannot
+    // issue before the stage's DMMAs have completed, i.e. before all their operands returned.
+    unsigned dep = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) dep ^= (unsigned)__double2hiint(accr[a][b][0]) ^ (unsigned)__double2hiint(acci[a][b][0]);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (lane == 0) {
+      sink[warp] = dep;
+      mbar_arrive(&empty[stage]);
+    }
     if (tid == 0 && kt + TST < nk) {
       mbar_wait_parity(&empty[stage], phase);
       issue(stage, kt + TST);
@@ -216,15 +245,16 @@ EncodeFn encode_fn() {
 }
 
 bool make_map(CUtensorMap* m, const double* base, int rows, int cols, long long ld, long long batch_stride, int count,
-              int box_rows) {
+              int box_rows, int box_cols = 16) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)count};
   const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)batch_stride * 8};
-  const cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};  // 16 columns = one 128-byte swizzle row
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -235,11 +265,12 @@ bool lu_tma_maps_make_rect(LuTmaMaps* t, const double* re, const double* im, int
   t->ok = false;
   if (rows < 1 || cols < 1 || (ld & 1) || (stride & 1) || ((uintptr_t)re & 15) || ((uintptr_t)im & 15)) return false;
   if (count > 1 && stride <= 0) return false;
-  static_assert(sizeof(t->m) >= 4 * sizeof(CUtensorMap), "LuTmaMaps storage");
+  static_assert(sizeof(t->m) >= 6 * sizeof(CUtensorMap), "LuTmaMaps storage");
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(t->m);
   const long long bs = count > 1 ? stride : (long long)rows * ld;  // any valid stride for a single item
   t->ok = make_map(m + 0, re, rows, cols, ld, bs, count, TM) && make_map(m + 1, im, rows, cols, ld, bs, count, TM) &&
-          make_map(m + 2, re, rows, cols, ld, bs, count, TK) && make_map(m + 3, im, rows, cols, ld, bs, count, TK);
+          make_map(m + 2, re, rows, cols, ld, bs, count, TK) && make_map(m + 3, im, rows, cols, ld, bs, count, TK) &&
+          make_map(m + 4, re, rows, cols, ld, bs, count, TK, TM) && make_map(m + 5, im, rows, cols, ld, bs, count, TK, TM);
   return t->ok;
 }
 
@@ -253,12 +284,15 @@ bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, l
 
 static void tma_kernel_config(size_t smem) {
   static DevOnce cfg;
-  if (cfg.first()) cudaFuncSetAttribute(zgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cfg.first()) {
+    cudaFuncSetAttribute(zgemm_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(zgemm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
 }
 
 cudaError_t zgemm_tma_sub(const LuTmaMaps& ta, const LuTmaMaps& tb, double* cre, double* cim, long long ldc,
                           long long sc, int count, int m, int n, int k, int arow, int acol, int brow, int bcol,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool conjt) {
   if (m <= 0 || n <= 0 || k <= 0) return cudaSuccess;
   if (!ta.ok || !tb.ok || (ldc & 1) || ((uintptr_t)cre & 15) || ((uintptr_t)cim & 15)) return cudaErrorNotSupported;
   const CUtensorMap* mp = reinterpret_cast<const CUtensorMap*>(ta.m);
@@ -269,7 +303,11 @@ cudaError_t zgemm_tma_sub(const LuTmaMaps& ta, const LuTmaMaps& tb, double* cre,
   a.cre = cre; a.cim = cim; a.ldc = ldc; a.sc = sc;
   const size_t smem = (size_t)TST * STAGE_BYTES + 1024;
   tma_kernel_config(smem);
-  zgemm_tma_kernel<<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mq[2], mq[3], a);
+  const dim3 grid(ceil_div(n, TN), ceil_div(m, TM), count);
+  if (conjt)
+    zgemm_tma_kernel<true><<<grid, TNT, smem, st>>>(mp[4], mp[5], mq[2], mq[3], a);
+  else
+    zgemm_tma_kernel<false><<<grid, TNT, smem, st>>>(mp[0], mp[1], mq[2], mq[3], a);
   count_launch();
   return cudaGetLastError();
 }
@@ -287,7 +325,7 @@ cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long lon
   a.ldc = ld; a.sc = slu;
   const size_t smem = (size_t)TST * STAGE_BYTES + 1024;  // + slack to align the tiles to 1024 bytes
   tma_kernel_config(smem);
-  zgemm_tma_kernel<<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mp[2], mp[3], a);
+  zgemm_tma_kernel<false><<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mp[2], mp[3], a);
   count_launch();
   return cudaGetLastError();
 }

@@ -543,8 +543,7 @@ __global__ void __launch_bounds__(TT) sweep_kernel(SweepArgs a0) {
 // updates of a 256-row block need no inter-CTA hand-over (measured at C2's
 // shapes: 94 us per block against 110-120 us for the dataflow sweep on the
 // same block, and no cooperative launch).
-// Direct sweeps only (variant 0: L forward, 1: U backward).
-template <bool VEC>
+template <bool TR, bool VEC>
 __global__ void __launch_bounds__(TT) block_solve_kernel(SweepArgs a0) {
   extern __shared__ __align__(16) double s[];
   SweepArgs a = a0;
@@ -554,7 +553,7 @@ __global__ void __launch_bounds__(TT) block_solve_kernel(SweepArgs a0) {
   double* T0 = s + (size_t)a.nblk * XTILE;         // streamed operator tiles (double buffer)
   double* T1 = T0 + TILE;
   double* Td = T1 + TILE;                          // diagonal operator + inverse pivots
-  const bool fwd = a.variant == 0;
+  const bool fwd = a.variant == 0 || a.variant == 2;
   const bool live = c0 + ((threadIdx.x >> 5) % WC) * 16 < a.nrhs;
   for (int b = 0; b < a.nblk; ++b) cp_x<VEC>(a, b, c0, Xs + (size_t)b * XTILE);
   for (int t = 0; t < a.nblk; ++t) {
@@ -584,7 +583,7 @@ __global__ void __launch_bounds__(TT) block_solve_kernel(SweepArgs a0) {
       // -M X_b from zero, added to the pending tile once (one rounding per element and step)
       Acc prod;
       acc_zero(prod);
-      tile_mma<false, -1, -1>(prod, Tq, Xt, live);
+      tile_mma<TR, -1, (TR ? 1 : -1)>(prod, Tq, Xt, live);
       acc_add_to_tile(prod, Xs + (size_t)blk_at(a, t + 1 + q) * XTILE);
       __syncthreads();
     }
@@ -689,7 +688,7 @@ static cudaError_t sweep_launch_one(int variant, int n, int nrhs, int count, con
                                     long long sdinv, double* xre, double* xim, long long ldx, long long sx,
                                     cudaStream_t st);
 
-// diagonal block [gblk0*32, gblk0*32 + n) of the whole matrix (gnblk blocks), n <= SOB, variants 0 / 1
+// diagonal block [gblk0*32, gblk0*32 + n) of the whole matrix (gnblk blocks), n <= SOB
 static cudaError_t block_solve_launch(int variant, int n, int nrhs, int count, const double* lre, const double* lim,
                                       long long ld, long long slu, const double* dinv, const double* gmat,
                                       long long sdinv, double* xre, double* xim, long long ldx, long long sx,
@@ -706,14 +705,22 @@ static cudaError_t block_solve_launch(int variant, int n, int nrhs, int count, c
   const size_t smem = sizeof(double) * ((size_t)(SOB / BS) * XTILE + 3 * TILE + 2 * BS);
   static DevOnce cfg;
   if (cfg.first()) {
-    cudaFuncSetAttribute(block_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(block_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(block_solve_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(block_solve_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(block_solve_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(block_solve_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   const dim3 grid(ceil_div(nrhs, CW), count);
-  if (vec)
-    block_solve_kernel<true><<<grid, TT, smem, st>>>(a);
-  else
-    block_solve_kernel<false><<<grid, TT, smem, st>>>(a);
+  if (variant >= 2) {
+    if (vec)
+      block_solve_kernel<true, true><<<grid, TT, smem, st>>>(a);
+    else
+      block_solve_kernel<true, false><<<grid, TT, smem, st>>>(a);
+  } else if (vec) {
+    block_solve_kernel<false, true><<<grid, TT, smem, st>>>(a);
+  } else {
+    block_solve_kernel<false, false><<<grid, TT, smem, st>>>(a);
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -726,30 +733,31 @@ cudaError_t sweep_launch(int variant, int n, int nrhs, int count, const double* 
                          long long ld, long long slu, const double* dinv, const double* gmat, long long sdinv,
                          double* xre, double* xim, long long ldx, long long sx, cudaStream_t st) {
   if (n <= 0 || nrhs <= 0 || count <= 0) return cudaSuccess;
-  // Direct sweeps (L forward, U backward) of large matrices run BLOCKED:
-  // block_solve_kernel solves one 256-row diagonal block, then the update of
-  // all pending rows, X_pend -= M(pend, block) X_block, is ONE TMA-fed ZGEMM
-  // with K = 256 (95 % of the DMMA pipe against ~55 % for the streamed rank-32
-  // tile updates, and 8x less traffic on X).  The adjoint sweeps keep the
-  // streamed form: their update needs M^H tiles, and the two transposed-tile
-  // variants of the TMA kernel that were tried returned a wrong 16-column
-  // sub-tile intermittently with two CTAs per SM.
-  if (variant < 2 && n >= SOB_MIN_N && (ld % 2) == 0 && (ldx % 2) == 0 && (slu % 2) == 0 && (sx % 2) == 0) {
+  // Sweeps of large matrices run BLOCKED: block_solve_kernel solves one
+  // 256-row diagonal block, then the update of all pending rows,
+  // X_pend -= M(pend, block) X_block (M^H for the adjoint sweeps), is ONE
+  // TMA-fed ZGEMM with K = 256 (95 % of the DMMA pipe against ~55 % for the
+  // streamed rank-32 tile updates, and 8x less traffic on X).
+  if (n >= SOB_MIN_N && (ld % 2) == 0 && (ldx % 2) == 0 && (slu % 2) == 0 && (sx % 2) == 0) {
     LuTmaMaps ma, mx;
     if (lu_tma_maps_make(&ma, lre, lim, n, ld, slu, count) &&
         lu_tma_maps_make_rect(&mx, xre, xim, n, nrhs, ldx, sx, count)) {
       const int nob = ceil_div(n, SOB), gn = ceil_div(n, BS);
+      const bool asc = variant == 0 || variant == 2;  // L and U^H sweep forward, U and L^H backward
       for (int t = 0; t < nob; ++t) {
-        const int ob = (variant == 0 ? t : nob - 1 - t) * SOB, rows = std::min(SOB, n - ob);
+        const int ob = (asc ? t : nob - 1 - t) * SOB, rows = std::min(SOB, n - ob);
         cudaError_t e = block_solve_launch(variant, rows, nrhs, count, lre + (long long)ob * ld + ob,
                                            lim + (long long)ob * ld + ob, ld, slu, dinv, gmat, sdinv,
                                            xre + (long long)ob * ldx, xim + (long long)ob * ldx, ldx, sx, st, ob / BS, gn);
         if (e != cudaSuccess) return e;
-        const int pend0 = variant == 0 ? ob + rows : 0, pend = variant == 0 ? n - (ob + rows) : ob;
+        const int pend0 = asc ? ob + rows : 0, pend = asc ? n - (ob + rows) : ob;
         if (pend > 0) {
-          // C = X[pend0.., :], A = M[pend0.., ob..ob+rows), B = X[ob..ob+rows, :]
-          e = zgemm_tma_sub(ma, mx, xre + (long long)pend0 * ldx, xim + (long long)pend0 * ldx, ldx, sx, count, pend,
-                            nrhs, rows, pend0, ob, ob, 0, st);
+          // C = X[pend0.., :], B = X[ob..ob+rows, :]; A = M[pend0.., ob..ob+rows) for the direct sweeps,
+          // A(r, k) = conj(M[ob + k][pend0 + r]) for the adjoint ones
+          double* cr = xre + (long long)pend0 * ldx;
+          double* ci = xim + (long long)pend0 * ldx;
+          e = variant < 2 ? zgemm_tma_sub(ma, mx, cr, ci, ldx, sx, count, pend, nrhs, rows, pend0, ob, ob, 0, st, false)
+                          : zgemm_tma_sub(ma, mx, cr, ci, ldx, sx, count, pend, nrhs, rows, ob, pend0, ob, 0, st, true);
           if (e != cudaSuccess) return e;
         }
       }

@@ -376,11 +376,13 @@ def test_batched_lu_tma_trailing_update_with_lookahead(dev, n, count):
 
 @pytest.mark.parametrize("n,count,nrhs", [(6144, 2, 160), (6300, 1, 152)])
 def test_blocked_sweeps_large_n(dev, n, count, nrhs):
-    """Direct sweeps at n >= 6144 run blocked (trsm.cu: 256-row dataflow sweep +
-    one TMA-fed ZGEMM over the pending rows; the adjoint sweeps stay streamed):
-    (zB - A) x = y and (zB - A)^H x = y against numpy, ragged n and a column
-    count that is not a tile multiple included, and a repeated pass must be
-    bit-identical (a stale tile in any of the 2 x n/256 launches would differ)."""
+    """Sweeps at n >= 6144 run blocked (trsm.cu: a single-CTA solve of each
+    256-row diagonal block + one TMA-fed ZGEMM over the pending rows, M^H tiles
+    for the adjoint sweeps): (zB - A) x = y and (zB - A)^H x = y against numpy,
+    ragged n and a column count that is not a tile multiple included.  Repeated
+    passes must be bit-identical: before the stage release of the TMA kernel was
+    ordered after the fragment loads' completion (gemm_tma.cu), about one pass
+    in three of the (6144, 2, 160) case returned a wrong 16-column sub-tile."""
     from paper_1203_4031_b200.dense import DeviceDenseOps
     rng = np.random.default_rng(n)
     a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
@@ -397,7 +399,7 @@ def test_blocked_sweeps_large_n(dev, n, count, nrhs):
         if adj:
             s = s.conj().T
         assert np.abs(s @ x - y).max() <= 1e-13 * np.abs(s).max() * np.abs(x).max() * n
-    for _ in range(2):
+    for _ in range(4):
         ops.solve_pass(Y, True)
         for (z, adj), x in first.items():
             assert np.array_equal(dev.download(ops.pass_result(z, adj)), x)
