@@ -1,6 +1,8 @@
 // TMA-fed FP64 tensor-core ZGEMM for the bulk trailing update of the blocked LU,
 //     A22 -= L21 * U12        (dense.py:49, the rank-1 np.outer update, blocked K = 256)
-// for all shifts of a batch.  Every operand is a sub-block of the SAME strided
+// for all shifts of a batch, and for the pending-row updates of the blocked
+// triangular sweeps, X_pend -= M(pend, block) X_block (dense.py:62-87; M^H for the
+// adjoint sweeps: template CONJT, B tiles from a second set of maps over X).  Every operand is a sub-block of the SAME strided
 // batch of factor matrices (planar re / im, row-major, leading dimension ld),
 // so four 3-D tensor maps (plane x {A box, B box}) describe the whole batch
 // once per factorization and the kernel addresses tiles by coordinates:

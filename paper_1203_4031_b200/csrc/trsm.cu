@@ -26,6 +26,10 @@
 // complex as 4 real DMMAs on planar operands; each warp owns a 16x16 sub-tile
 // (8 independent accumulator chains).
 //
+// For N >= 6144 the sweeps run BLOCKED instead (sweep_launch): block_solve_kernel
+// solves each 256-row diagonal block with the chunk of X resident in shared
+// memory, and one TMA-fed ZGEMM (gemm_tma.cu, K = 256) updates all pending rows.
+//
 //   variant 0  L   forward  (direct solve, after the row gather P B)
 //   variant 1  U   backward (direct solve)
 //   variant 2  U^H forward  (adjoint solve)
