@@ -77,7 +77,11 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
   // (it is not 1024-aligned when the SM is shared with CTAs of other kernels)
   unsigned char* base = tsm + ((1024u - (smem_u32(tsm) & 1023u)) & 1023u);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
-  const int wm = (warp >> 2) * 32, wn = (warp & 3) * 16;
+  // warp -> 32 x 16 sub-tile.  The column group rotates with the tile row so that the warps of a
+  // ragged last column tile that own no valid column (they skip the k-loop: "live") idle a
+  // different SM sub-partition in every CTA -- warp w issues on sub-partition w % 4, and with a
+  // fixed mapping sub-partitions 0 / 1 would stay the bottleneck (M0 = 152: 3 tiles of 64)
+  const int wm = (warp >> 2) * 32, wn = ((warp + blockIdx.y + blockIdx.z) & 3) * 16;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN, bz = blockIdx.z;
   const int nk = p.k / TK;
   if (tid == 0) {
@@ -110,6 +114,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
 #pragma unroll 1
     for (int s = 0; s < TST && s < nk; ++s) issue(s, s);
   }
+  const bool live = n0 + wn < p.n;  // warp-uniform
   double accr[4][2][2], acci[4][2][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -123,44 +128,46 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
   for (int kt = 0; kt < nk; ++kt) {
     mbar_wait_parity(&full[stage], phase);
     const unsigned char* st = base + (size_t)stage * STAGE_BYTES;
+    if (live) {
 #pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4) {
-      const int kk = (s4 >> 1) * 8 + (s4 & 1) * 2 + (q & 1) + 4 * (q >> 1);
-      double x[4], y[4], z[4], br[2], bi[2];
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int kk = (s4 >> 1) * 8 + (s4 & 1) * 2 + (q & 1) + 4 * (q >> 1);
+        double x[4], y[4], z[4], br[2], bi[2];
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int n = wn + t * 8 + g;
-        const int off = (n >> 4) * 2048 + kk * 128 + ((((n & 15) >> 1) ^ (kk & 7)) << 4) + ((n & 1) << 3);
-        br[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + off);
-        bi[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + B_BYTES + off);
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int r = wm + t * 8 + g;
-        const int off = CONJT ? kk * (TM * 8) + r * 8 : r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + ((kk & 1) << 3);
-        const double ar = *reinterpret_cast<const double*>(st + off);
-        const double ai = *reinterpret_cast<const double*>(st + A_BYTES + off);
-        const double nar = __longlong_as_double(__double_as_longlong(ar) ^ 0x8000000000000000ull);
-        const double nai = __longlong_as_double(__double_as_longlong(ai) ^ 0x8000000000000000ull);
-        // -(A B): re += (-ar) br + ai bi, im += (-ar) bi + (-ai) br; conj(A) flips the sign of ai
-        x[t] = nar;
-        y[t] = CONJT ? nai : ai;
-        z[t] = CONJT ? ai : nai;
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          dmma(accr[a][b][0], accr[a][b][1], x[a], br[b]);
-          dmma(acci[a][b][0], acci[a][b][1], x[a], bi[b]);
+        for (int t = 0; t < 2; ++t) {
+          const int n = wn + t * 8 + g;
+          const int off = (n >> 4) * 2048 + kk * 128 + ((((n & 15) >> 1) ^ (kk & 7)) << 4) + ((n & 1) << 3);
+          br[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + off);
+          bi[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + B_BYTES + off);
         }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          dmma(accr[a][b][0], accr[a][b][1], y[a], bi[b]);
-          dmma(acci[a][b][0], acci[a][b][1], z[a], br[b]);
+        for (int t = 0; t < 4; ++t) {
+          const int r = wm + t * 8 + g;
+          const int off = CONJT ? kk * (TM * 8) + r * 8 : r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + ((kk & 1) << 3);
+          const double ar = *reinterpret_cast<const double*>(st + off);
+          const double ai = *reinterpret_cast<const double*>(st + A_BYTES + off);
+          const double nar = __longlong_as_double(__double_as_longlong(ar) ^ 0x8000000000000000ull);
+          const double nai = __longlong_as_double(__double_as_longlong(ai) ^ 0x8000000000000000ull);
+          // -(A B): re += (-ar) br + ai bi, im += (-ar) bi + (-ai) br; conj(A) flips the sign of ai
+          x[t] = nar;
+          y[t] = CONJT ? nai : ai;
+          z[t] = CONJT ? ai : nai;
         }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            dmma(accr[a][b][0], accr[a][b][1], x[a], br[b]);
+            dmma(acci[a][b][0], acci[a][b][1], x[a], bi[b]);
+          }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            dmma(accr[a][b][0], accr[a][b][1], y[a], bi[b]);
+            dmma(acci[a][b][0], acci[a][b][1], z[a], br[b]);
+          }
+      }
     }
     // This warp is done with the stage; the elected thread refills it once all 8 warps are.
     // The release must not overtake the fragment loads: an mbarrier arrive orders memory

@@ -63,8 +63,8 @@ constexpr int PA = 36;                 // operator tile pitch (= 4 mod 16: confl
 constexpr int XP = CW + 4;             // X tile pitch (= 4 mod 16)
 constexpr int TILE = 2 * BS * PA;      // doubles per planar 32x32 operator tile in shared memory
 constexpr int XTILE = 2 * BS * XP;     // doubles per planar 32 x CW X tile
-constexpr int SOB = 256;               // outer block of the blocked direct sweeps (= K of the TMA update)
-constexpr int SOB_MIN_N = 6144;        // below, the per-block launches cost more than the faster updates gain (C2: +4 %)
+constexpr int SOB = 256;               // outer block of the blocked sweeps (= K of the TMA update; 128 measured equal at C3, slower at C2)
+constexpr int SOB_MIN_N = 6144;        // below, the block solves cost more than the faster updates gain (C2: +3 %, C1: +6 %)
 constexpr int GM_BLK = 4 * BS * BS;    // per (variant, block): T re/im [32][32], inv re/im [32] (padded)
 
 struct SweepArgs {
