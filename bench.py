@@ -96,8 +96,9 @@ class ClockSampler:
     # NVML clocks-event reason bits: hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
     BITS = (0x8, 0x40, 0x20, 0x4)
 
-    def __init__(self, index):
+    def __init__(self, index, disabled=False):
         self.index = index
+        self.disabled = disabled
         self.samples = []
         self._stop = threading.Event()
         self._t = None
@@ -143,13 +144,15 @@ class ClockSampler:
             self._stop.wait(1.0)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._loop, daemon=True)
-        self._t.start()
+        if not self.disabled:
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
@@ -370,7 +373,7 @@ def run_gpu(args):
     fac_events = []
     DeviceDenseOps.lu_event_sink = fac_events
     DeviceBandOps.factor_event_sink = fac_events
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, disabled=args.no_clocks) as clk:
         step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev0.record()
         step_ev[0].record()
@@ -497,6 +500,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-banded", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true",
+                    help="diagnosis only: no NVML sampling thread during the timed region")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
