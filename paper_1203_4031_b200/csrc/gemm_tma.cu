@@ -170,19 +170,23 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
       }
     }
     // This warp is done with the stage; the elected thread refills it once all 8 warps are.
-    // The release must not overtake the fragment loads: an mbarrier arrive orders memory
-    // operations, but ptxas places it right after the last LDS is ISSUED (the DMMAs that consume
-    // the fragments follow), and under bank-conflict replays with two CTAs per SM the refill's
-    // bulk copy was seen to overwrite a B box before a late warp's loads had read it (one
-    // wrong 16-column sub-tile, about one launch sequence in three for the transposed form).
-    // Lane 0 therefore first stores a word that depends on every accumulator: the store cannot
-    // issue before the stage's DMMAs have completed, i.e. before all their operands returned.
+    // The refill is an ASYNC-proxy write (bulk tensor copy) to memory this warp has just read
+    // through the generic proxy (LDS): the release needs a proxy fence, and it must not overtake
+    // the loads.  Without either, ptxas placed the arrive right after the last LDS was ISSUED (the
+    // DMMAs that consume the fragments followed it), and under bank-conflict replays with two CTAs
+    // per SM the refill of a B box -- an L2 hit -- landed before a late warp had read the old box:
+    // one wrong 16-column sub-tile in about one sweep pass in three for the transposed form
+    // (tools/soak_blocked_sweeps.py).  Two measures, each clean on its own in 71 repeat passes:
+    //  * fence.proxy.async orders the generic-proxy reads before later async-proxy accesses;
+    //  * lane 0 first stores a word that depends on every accumulator, so the arrive cannot
+    //    issue before the stage's DMMAs -- hence all their operand loads -- have completed.
     unsigned dep = 0;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 2; ++b) dep ^= (unsigned)__double2hiint(accr[a][b][0]) ^ (unsigned)__double2hiint(acci[a][b][0]);
     __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     if (lane == 0) {
       sink[warp] = dep;
       mbar_arrive(&empty[stage]);
