@@ -852,6 +852,9 @@ __global__ void __launch_bounds__(2 * BNC, 5) band_psolve_bwd_kernel(PSArgs a) {
     if constexpr (BULK) {  // elected thread only
       unsigned bytes = 0;
       if (jl <= j1) bytes = (unsigned)(j1 - jl + 1) * NU * 16u;
+      // the buffer was read through the generic proxy (the __syncthreads that freed it orders
+      // those reads before this thread); the bulk copies write it through the async proxy
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive_expect_tx(&full[buf], bytes + 2u * nr * rowbytes);
       if (bytes) bulk_g2s(&su[buf][(size_t)(jl - (j1 - SCB + 1)) * NU], Us + (long long)jl * NU, bytes, &full[buf]);
       const double* fr = Xr + (long long)r0 * a.ldx + col0;
@@ -1034,6 +1037,9 @@ __global__ void __launch_bounds__(T4_WARPS * 32, 4) band_psolve_bwd_t4_kernel(PS
     const int s0 = c * T4_S;
     if (tid == 0) {
       const unsigned bytes = c < nchunks ? (unsigned)(T4_S * T4_STEPD * 8) : 0u;
+      // generic-proxy reads of the freed buffer (ordered before this thread by the
+      // __syncthreads that freed it) -> async-proxy refill
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_arrive_expect_tx(&full[buf], bytes);
       if (bytes) bulk_g2s(dst, T4 + (long long)s0 * T4_STEPD, bytes, &full[buf]);
     }
