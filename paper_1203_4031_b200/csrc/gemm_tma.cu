@@ -36,7 +36,7 @@ namespace fb {
 
 namespace {
 
-constexpr int TM = 64, TN = 64, TK = 16, TST = 3, TNT = 256;
+constexpr int TM = 64, TN = 64, TK = 16, TST = 3;
 constexpr int A_BYTES = TM * TK * 8, B_BYTES = TK * TN * 8;      // per plane
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;             // 32 KB
 
@@ -46,6 +46,7 @@ struct TmaArgs {
   int brow, bcol;           // B(0, 0) = M[brow][bcol]
   double *cre, *cim;        // C(0, 0) of batch item 0
   long long ldc, sc;        // C leading dimension and batch stride
+  int ncol0;                // first column of this launch (a 32-wide launch covers a ragged tail)
 };
 
 __device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, int c0, int c1, int c2, void* bar) {
@@ -64,14 +65,19 @@ __device__ __forceinline__ void mbar_arrive(void* bar) {
 // 512-byte rows), so a stage is the same 10 bulk loads as the direct form; the A fragments then
 // read 4 wavefronts instead of 2 (the four k of a step share their banks), well inside the
 // shared-memory time the DMMAs leave.
-template <bool CONJT>
-__global__ void __launch_bounds__(TNT, 2)
+// TNW = 64: the 8-warp CTA (two per SM).  TNW = 32: four warps on a 64 x 32 tile (three CTAs per
+// SM) for a ragged tail of at most 32 columns -- M0 = 152 is 2 x 64 + 24, and a third 64-wide
+// tile would spend a quarter of the update's tensor time on columns that do not exist.
+template <bool CONJT, int TNW>
+__global__ void __launch_bounds__(TNW * 4, TNW == 64 ? 2 : 3)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_constant__ CUtensorMap map_aim,
                  const __grid_constant__ CUtensorMap map_bre, const __grid_constant__ CUtensorMap map_bim,
                  const TmaArgs p) {
   extern __shared__ __align__(16) unsigned char tsm[];
+  constexpr int NWC = TNW / 16, NTH = 2 * NWC * 32;           // column groups, threads
+  constexpr int BB = TK * TNW * 8, SB = 2 * A_BYTES + 2 * BB;  // B plane and stage bytes
   __shared__ __align__(8) unsigned long long full[TST], empty[TST];
-  __shared__ volatile unsigned sink[TNT / 32];
+  __shared__ volatile unsigned sink[NTH / 32];
   // the 128-byte swizzle is a function of the shared-memory ADDRESS: the tiles must start on a
   // 1024-byte boundary of the shared window, wherever the CTA's dynamic region happens to begin
   // (it is not 1024-aligned when the SM is shared with CTAs of other kernels)
@@ -81,21 +87,21 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
   // ragged last column tile that own no valid column (they skip the k-loop: "live") idle a
   // different SM sub-partition in every CTA -- warp w issues on sub-partition w % 4, and with a
   // fixed mapping sub-partitions 0 / 1 would stay the bottleneck (M0 = 152: 3 tiles of 64)
-  const int wm = (warp >> 2) * 32, wn = ((warp + blockIdx.y + blockIdx.z) & 3) * 16;
-  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN, bz = blockIdx.z;
+  const int wm = (warp / NWC) * 32, wn = ((warp + blockIdx.y + blockIdx.z) % NWC) * 16;
+  const int m0 = blockIdx.y * TM, n0 = p.ncol0 + blockIdx.x * TNW, bz = blockIdx.z;
   const int nk = p.k / TK;
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < TST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TNT / 32);
+      mbar_init(&empty[s], NTH / 32);
     }
     mbar_fence_init();
   }
   __syncthreads();
   auto issue = [&](int s, int kt) {  // elected thread
-    unsigned char* st = base + (size_t)s * STAGE_BYTES;
-    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+    unsigned char* st = base + (size_t)s * SB;
+    mbar_arrive_expect_tx(&full[s], SB);
     if (!CONJT) {
       tma_load_3d(st, &map_are, p.acol + kt * TK, p.arow + m0, bz, &full[s]);
       tma_load_3d(st + A_BYTES, &map_aim, p.acol + kt * TK, p.arow + m0, bz, &full[s]);
@@ -104,9 +110,9 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
       tma_load_3d(st + A_BYTES, &map_aim, p.acol + m0, p.arow + kt * TK, bz, &full[s]);
     }
 #pragma unroll
-    for (int j = 0; j < TN / 16; ++j) {
+    for (int j = 0; j < NWC; ++j) {
       tma_load_3d(st + 2 * A_BYTES + j * (TK * 128), &map_bre, p.bcol + n0 + 16 * j, p.brow + kt * TK, bz, &full[s]);
-      tma_load_3d(st + 2 * A_BYTES + B_BYTES + j * (TK * 128), &map_bim, p.bcol + n0 + 16 * j, p.brow + kt * TK, bz,
+      tma_load_3d(st + 2 * A_BYTES + BB + j * (TK * 128), &map_bim, p.bcol + n0 + 16 * j, p.brow + kt * TK, bz,
                   &full[s]);
     }
   };
@@ -127,7 +133,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
   unsigned phase = 0;
   for (int kt = 0; kt < nk; ++kt) {
     mbar_wait_parity(&full[stage], phase);
-    const unsigned char* st = base + (size_t)stage * STAGE_BYTES;
+    const unsigned char* st = base + (size_t)stage * SB;
     if (live) {
 #pragma unroll
       for (int s4 = 0; s4 < 4; ++s4) {
@@ -138,7 +144,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap map_are, const __grid_const
           const int n = wn + t * 8 + g;
           const int off = (n >> 4) * 2048 + kk * 128 + ((((n & 15) >> 1) ^ (kk & 7)) << 4) + ((n & 1) << 3);
           br[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + off);
-          bi[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + B_BYTES + off);
+          bi[t] = *reinterpret_cast<const double*>(st + 2 * A_BYTES + BB + off);
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -295,11 +301,16 @@ bool lu_tma_maps_make(LuTmaMaps* t, const double* re, const double* im, int n, l
   return lu_tma_maps_make_rect(t, re, im, n, n, ld, slu, count);
 }
 
-static void tma_kernel_config(size_t smem) {
+constexpr size_t SMEM64 = (size_t)TST * STAGE_BYTES + 1024;                       // + slack to align the tiles to 1024 bytes
+constexpr size_t SMEM32 = (size_t)TST * (2 * A_BYTES + 2 * TK * 32 * 8) + 1024;  // the 32-column form
+
+static void tma_kernel_config() {
   static DevOnce cfg;
   if (cfg.first()) {
-    cudaFuncSetAttribute(zgemm_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(zgemm_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(zgemm_tma_kernel<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM64);
+    cudaFuncSetAttribute(zgemm_tma_kernel<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM64);
+    cudaFuncSetAttribute(zgemm_tma_kernel<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM32);
+    cudaFuncSetAttribute(zgemm_tma_kernel<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM32);
   }
 }
 
@@ -314,14 +325,28 @@ cudaError_t zgemm_tma_sub(const LuTmaMaps& ta, const LuTmaMaps& tb, double* cre,
   a.m = m; a.n = n; a.k = ceil_div(k, TK) * TK;  // a K tail reads zero-filled entries past the tensors' edge
   a.arow = arow; a.acol = acol; a.brow = brow; a.bcol = bcol;
   a.cre = cre; a.cim = cim; a.ldc = ldc; a.sc = sc;
-  const size_t smem = (size_t)TST * STAGE_BYTES + 1024;
-  tma_kernel_config(smem);
-  const dim3 grid(ceil_div(n, TN), ceil_div(m, TM), count);
-  if (conjt)
-    zgemm_tma_kernel<true><<<grid, TNT, smem, st>>>(mp[4], mp[5], mq[2], mq[3], a);
-  else
-    zgemm_tma_kernel<false><<<grid, TNT, smem, st>>>(mp[0], mp[1], mq[2], mq[3], a);
-  count_launch();
+  tma_kernel_config();
+  // 64-column tiles, and a ragged tail of at most 32 columns on the 32-column form
+  const int rem = n % TN, tail = (rem > 0 && rem <= 32) ? rem : 0;
+  const int wide = (n - tail + TN - 1) / TN;
+  if (wide > 0) {
+    const dim3 grid(wide, ceil_div(m, TM), count);
+    a.ncol0 = 0;
+    if (conjt)
+      zgemm_tma_kernel<true, 64><<<grid, 256, SMEM64, st>>>(mp[4], mp[5], mq[2], mq[3], a);
+    else
+      zgemm_tma_kernel<false, 64><<<grid, 256, SMEM64, st>>>(mp[0], mp[1], mq[2], mq[3], a);
+    count_launch();
+  }
+  if (tail > 0) {
+    const dim3 grid(1, ceil_div(m, TM), count);
+    a.ncol0 = n - tail;
+    if (conjt)
+      zgemm_tma_kernel<true, 32><<<grid, 128, SMEM32, st>>>(mp[4], mp[5], mq[2], mq[3], a);
+    else
+      zgemm_tma_kernel<false, 32><<<grid, 128, SMEM32, st>>>(mp[0], mp[1], mq[2], mq[3], a);
+    count_launch();
+  }
   return cudaGetLastError();
 }
 
@@ -336,9 +361,9 @@ cudaError_t lu_trailing_tma(const LuTmaMaps& t, double* re, double* im, long lon
   a.cre = re + (long long)crow * ld + ccol;
   a.cim = im + (long long)crow * ld + ccol;
   a.ldc = ld; a.sc = slu;
-  const size_t smem = (size_t)TST * STAGE_BYTES + 1024;  // + slack to align the tiles to 1024 bytes
-  tma_kernel_config(smem);
-  zgemm_tma_kernel<false><<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), TNT, smem, st>>>(mp[0], mp[1], mp[2], mp[3], a);
+  a.ncol0 = 0;
+  tma_kernel_config();
+  zgemm_tma_kernel<false, 64><<<dim3(ceil_div(n, TN), ceil_div(m, TM), count), 256, SMEM64, st>>>(mp[0], mp[1], mp[2], mp[3], a);
   count_launch();
   return cudaGetLastError();
 }
