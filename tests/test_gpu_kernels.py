@@ -374,12 +374,13 @@ def test_batched_lu_tma_trailing_update_with_lookahead(dev, n, count):
         assert np.abs(s @ x - y).max() <= 1e-13 * np.abs(s).max() * np.abs(x).max() * n
 
 
-@pytest.mark.parametrize("n,count,nrhs", [(6144, 2, 160), (6300, 1, 152)])
+@pytest.mark.parametrize("n,count,nrhs", [(6144, 2, 160), (6300, 1, 152), (6144, 1, 24)])
 def test_blocked_sweeps_large_n(dev, n, count, nrhs):
     """Sweeps at n >= 6144 run blocked (trsm.cu: a single-CTA solve of each
     256-row diagonal block + one TMA-fed ZGEMM over the pending rows, M^H tiles
     for the adjoint sweeps): (zB - A) x = y and (zB - A)^H x = y against numpy,
-    ragged n and a column count that is not a tile multiple included.  Repeated
+    ragged n, column counts that are not a tile multiple (the 32-column tail
+    form of the update kernel, alone for 24 columns) included.  Repeated
     passes must be bit-identical: before the stage release of the TMA kernel was
     ordered after the fragment loads' completion (gemm_tma.cu), about one pass
     in three of the (6144, 2, 160) case returned a wrong 16-column sub-tile."""
